@@ -1,0 +1,152 @@
+// Elementwise and reduction kernels (HBM-bound).
+//
+// K_ELTWISE: out = act(op(a, b, c)) over N x H x W x C with independent
+// 4-D strides per operand — stride 0 broadcasts (SE channel scale, per-
+// channel affine), channel-slice strides make concat zero-copy, and EW_COPY
+// doubles as the strided concat / layout fallback.  128-bit path when every
+// operand is channel-contiguous and aligned.
+// K_GLOBAL_POOL: mean over H x W per (n, c); one thread per 4 channels,
+// consecutive threads on consecutive channels (coalesced NHWC reads).
+#include "common.cuh"
+
+namespace sw {
+
+struct EwArgs {
+  const float* a;
+  const float* b;
+  const float* c;
+  float* out;
+  const float* scale;
+  const float* shift;
+  int N, H, W, C, op, act, nin, pre_relu;
+  int64_t as[4], bs[4], cs[4], os[4];
+};
+
+static EwArgs ew_args(const sw_op_desc& d) {
+  const int64_t* p = d.params;
+  EwArgs e;
+  e.a = reinterpret_cast<const float*>(d.ptrs[EP_A]);
+  e.b = reinterpret_cast<const float*>(d.ptrs[EP_B]);
+  e.c = reinterpret_cast<const float*>(d.ptrs[EP_C]);
+  e.out = reinterpret_cast<float*>(d.ptrs[EP_OUT]);
+  e.scale = reinterpret_cast<const float*>(d.ptrs[EP_SCALE]);
+  e.shift = reinterpret_cast<const float*>(d.ptrs[EP_SHIFT]);
+  e.N = (int)p[EW_N]; e.H = (int)p[EW_H]; e.W = (int)p[EW_W]; e.C = (int)p[EW_C];
+  e.op = (int)p[EW_OP]; e.act = (int)p[EW_ACT]; e.nin = (int)p[EW_NIN]; e.pre_relu = (int)p[EW_PRE_RELU];
+  for (int i = 0; i < 4; ++i) {
+    e.as[i] = p[EW_A_SN + i];
+    e.bs[i] = p[EW_B_SN + i];
+    e.cs[i] = p[EW_C_SN + i];
+    e.os[i] = p[EW_O_SN + i];
+  }
+  return e;
+}
+
+__device__ __forceinline__ int64_t off4(const int64_t* s, int n, int h, int w, int c) {
+  return n * s[0] + h * s[1] + w * s[2] + c * s[3];
+}
+
+__device__ __forceinline__ float ew_combine(const EwArgs& e, float x, float y, float z, int c) {
+  float v;
+  switch (e.op) {
+    case EW_ADD: v = x + (e.nin > 1 ? y : 0.f) + (e.nin > 2 ? z : 0.f); break;
+    case EW_MUL: v = x * y; break;
+    case EW_AFFINE: v = x * e.scale[c] + e.shift[c]; break;
+    default: v = x; break;
+  }
+  return apply_act(v, e.act);
+}
+
+__global__ void __launch_bounds__(256) ew_scalar_kernel(EwArgs e, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int c = (int)(idx % e.C);
+  int64_t t = idx / e.C;
+  int w = (int)(t % e.W);
+  t /= e.W;
+  int h = (int)(t % e.H);
+  int n = (int)(t / e.H);
+  float x = e.a[off4(e.as, n, h, w, c)];
+  if (e.pre_relu) x = fmaxf(x, 0.f);
+  float y = e.nin > 1 ? e.b[off4(e.bs, n, h, w, c)] : 0.f;
+  float z = e.nin > 2 ? e.c[off4(e.cs, n, h, w, c)] : 0.f;
+  e.out[off4(e.os, n, h, w, c)] = ew_combine(e, x, y, z, c);
+}
+
+__global__ void __launch_bounds__(256) ew_vec4_kernel(EwArgs e, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int CG = e.C / 4;
+  int c = (int)(idx % CG) * 4;
+  int64_t t = idx / CG;
+  int w = (int)(t % e.W);
+  t /= e.W;
+  int h = (int)(t % e.H);
+  int n = (int)(t / e.H);
+  float4 x = __ldg(reinterpret_cast<const float4*>(e.a + off4(e.as, n, h, w, c)));
+  if (e.pre_relu) {
+    x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+  }
+  float4 y = make_float4(0.f, 0.f, 0.f, 0.f), z = y;
+  if (e.nin > 1) y = __ldg(reinterpret_cast<const float4*>(e.b + off4(e.bs, n, h, w, c)));
+  if (e.nin > 2) z = __ldg(reinterpret_cast<const float4*>(e.c + off4(e.cs, n, h, w, c)));
+  float4 o;
+  o.x = ew_combine(e, x.x, y.x, z.x, c);
+  o.y = ew_combine(e, x.y, y.y, z.y, c + 1);
+  o.z = ew_combine(e, x.z, y.z, z.z, c + 2);
+  o.w = ew_combine(e, x.w, y.w, z.w, c + 3);
+  *reinterpret_cast<float4*>(e.out + off4(e.os, n, h, w, c)) = o;
+}
+
+static bool ew_vec_ok(const EwArgs& e, const sw_op_desc& d) {
+  if (e.C % 4) return false;
+  const int64_t* ss[4] = {e.as, e.bs, e.cs, e.os};
+  const uint64_t ps[4] = {d.ptrs[EP_A], d.ptrs[EP_B], d.ptrs[EP_C], d.ptrs[EP_OUT]};
+  for (int i = 0; i < 4; ++i) {
+    if (i >= 1 && i <= 2 && e.nin <= i) continue;
+    const int64_t* s = ss[i];
+    if (s[3] != 1 || s[0] % 4 || s[1] % 4 || s[2] % 4 || !aligned16(ps[i])) return false;
+  }
+  return true;
+}
+
+int launch_eltwise(const sw_op_desc& d, void* stream) {
+  EwArgs e = ew_args(d);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bool v4 = ew_vec_ok(e, d);
+  int64_t total = (int64_t)e.N * e.H * e.W * (v4 ? e.C / 4 : e.C);
+  if (total == 0) return 0;
+  int blocks = (int)cdiv(total, 256);
+  if (v4)
+    ew_vec4_kernel<<<blocks, 256, 0, st>>>(e, total);
+  else
+    ew_scalar_kernel<<<blocks, 256, 0, st>>>(e, total);
+  return (int)cudaGetLastError();
+}
+
+// Global average pool: out[n, c] = mean_hw(relu?(a[n, h, w, c])).
+__global__ void __launch_bounds__(128) global_pool_kernel(EwArgs e) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  int n = blockIdx.y;
+  if (c >= e.C) return;
+  float acc = 0.f;
+  const float* base = e.a + n * e.as[0] + c * e.as[3];
+  for (int h = 0; h < e.H; ++h)
+    for (int w = 0; w < e.W; ++w) {
+      float x = __ldg(base + h * e.as[1] + w * e.as[2]);
+      acc += e.pre_relu ? fmaxf(x, 0.f) : x;
+    }
+  acc /= (float)(e.H * e.W);
+  e.out[n * e.os[0] + c * e.os[3]] = apply_act(acc, e.act);
+}
+
+int launch_global_pool(const sw_op_desc& d, void* stream) {
+  EwArgs e = ew_args(d);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (e.N == 0 || e.C == 0) return 0;
+  dim3 grid((unsigned)cdiv(e.C, 128), (unsigned)e.N);
+  global_pool_kernel<<<grid, 128, 0, st>>>(e);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sw

@@ -1,0 +1,186 @@
+// Bandwidth-bound spatial kernels: depthwise convolution and k x k pooling.
+//
+// One thread owns one output pixel x VEC channels (VEC = 4 → 128-bit loads
+// and stores when channel strides are 1 and addresses/channels align), so a
+// warp reads 32*VEC consecutive channels of one input pixel per tap — fully
+// coalesced in NHWC; the k*k tap reuse across neighbouring pixels is served
+// by L1.  Epilogues fuse bias (folded BN), activation, a residual add (NASNet
+// cell combines, pooling branch + identity) and the strided store that makes
+// concat zero-copy.  Padding is top/left (may be negative for the NASNet
+// "pad-then-slice" shifts); out-of-range taps are zero (conv), skipped (max)
+// or excluded/counted per torch's count_include_pad rule (avg).
+#include "common.cuh"
+
+namespace sw {
+
+struct SpatialArgs {
+  const float* __restrict__ in;
+  float* __restrict__ out;
+  const float* __restrict__ w;     // depthwise weights [R][S][C]
+  const float* __restrict__ bias;  // [C]
+  const float* __restrict__ res;
+  int N, H, W, C, P, Q, R, S, sh, sw, ph, pw, act, pre_relu, has_res, mode, count_pad, pad_b, pad_r;
+  int64_t in_sn, in_sh, in_sw, in_sc;
+  int64_t out_sn, out_sh, out_sw;
+  int64_t res_sn, res_sh, res_sw;
+};
+
+static SpatialArgs spatial_args(const sw_op_desc& op) {
+  const int64_t* p = op.params;
+  SpatialArgs a;
+  a.in = reinterpret_cast<const float*>(op.ptrs[PT_IN]);
+  a.out = reinterpret_cast<float*>(op.ptrs[PT_OUT]);
+  a.w = reinterpret_cast<const float*>(op.ptrs[PT_W]);
+  a.bias = reinterpret_cast<const float*>(op.ptrs[PT_BIAS]);
+  a.res = reinterpret_cast<const float*>(op.ptrs[PT_RES]);
+  a.N = (int)p[SP_N]; a.H = (int)p[SP_H]; a.W = (int)p[SP_W]; a.C = (int)p[SP_C];
+  a.P = (int)p[SP_P]; a.Q = (int)p[SP_Q];
+  a.R = (int)p[SP_R]; a.S = (int)p[SP_S];
+  a.sh = (int)p[SP_STRIDE_H]; a.sw = (int)p[SP_STRIDE_W];
+  a.ph = (int)p[SP_PAD_H]; a.pw = (int)p[SP_PAD_W];
+  a.act = (int)p[SP_ACT]; a.pre_relu = (int)p[SP_PRE_RELU]; a.has_res = (int)p[SP_HAS_RES];
+  a.mode = (int)p[SP_POOL_MODE]; a.count_pad = (int)p[SP_COUNT_PAD];
+  a.pad_b = (int)p[SP_PAD_BOTTOM]; a.pad_r = (int)p[SP_PAD_RIGHT];
+  a.in_sn = p[SP_IN_SN]; a.in_sh = p[SP_IN_SH]; a.in_sw = p[SP_IN_SW]; a.in_sc = p[SP_IN_SC];
+  a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
+  a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
+  return a;
+}
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<1> {
+  using T = float;
+  static __device__ __forceinline__ float ld(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ void st(float* p, float v) { *p = v; }
+};
+template <>
+struct VecT<4> {
+  using T = float4;
+  static __device__ __forceinline__ float4 ld(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  static __device__ __forceinline__ void st(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+};
+
+__device__ __forceinline__ float relu1(float v) { return fmaxf(v, 0.f); }
+__device__ __forceinline__ float4 relu1(float4 v) {
+  return make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+}
+__device__ __forceinline__ void fma_acc(float& acc, float x, float w) { acc = fmaf(x, w, acc); }
+__device__ __forceinline__ void fma_acc(float4& acc, float4 x, float4 w) {
+  acc.x = fmaf(x.x, w.x, acc.x); acc.y = fmaf(x.y, w.y, acc.y);
+  acc.z = fmaf(x.z, w.z, acc.z); acc.w = fmaf(x.w, w.w, acc.w);
+}
+__device__ __forceinline__ void add_to(float& a, float b) { a += b; }
+__device__ __forceinline__ void add_to(float4& a, float4 b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+__device__ __forceinline__ void max_to(float& a, float b) { a = fmaxf(a, b); }
+__device__ __forceinline__ void max_to(float4& a, float4 b) {
+  a.x = fmaxf(a.x, b.x); a.y = fmaxf(a.y, b.y); a.z = fmaxf(a.z, b.z); a.w = fmaxf(a.w, b.w);
+}
+__device__ __forceinline__ void scale(float& a, float s) { a *= s; }
+__device__ __forceinline__ void scale(float4& a, float s) { a.x *= s; a.y *= s; a.z *= s; a.w *= s; }
+__device__ __forceinline__ float splat(float v, float) { return v; }
+__device__ __forceinline__ float4 splat(float v, float4) { return make_float4(v, v, v, v); }
+__device__ __forceinline__ float actv(float v, int act) { return apply_act(v, act); }
+__device__ __forceinline__ float4 actv(float4 v, int act) { return act4(v, act); }
+
+// KIND 0 = depthwise conv, 1 = pool
+template <int KIND, int VEC>
+__global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t total) {
+  using V = VecT<VEC>;
+  using T = typename V::T;
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int CG = a.C / VEC;
+  int cg = (int)(idx % CG);
+  int64_t t = idx / CG;
+  int q = (int)(t % a.Q);
+  t /= a.Q;
+  int p = (int)(t % a.P);
+  int n = (int)(t / a.P);
+  int c = cg * VEC;
+  const float* base = a.in + n * a.in_sn + c * a.in_sc;
+  const int ih0 = p * a.sh - a.ph, iw0 = q * a.sw - a.pw;
+  T acc = splat(0.f, T{});
+  if (KIND == 0) {
+    for (int r = 0; r < a.R; ++r) {
+      int ih = ih0 + r;
+      if (ih < 0 || ih >= a.H) continue;
+      for (int s = 0; s < a.S; ++s) {
+        int iw = iw0 + s;
+        if (iw < 0 || iw >= a.W) continue;
+        T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
+        if (a.pre_relu) x = relu1(x);
+        T wv = V::ld(a.w + (r * a.S + s) * a.C + c);
+        fma_acc(acc, x, wv);
+      }
+    }
+    if (a.bias) add_to(acc, V::ld(a.bias + c));
+  } else if (a.mode == 0) {  // max
+    acc = splat(-INFINITY, T{});
+    for (int r = 0; r < a.R; ++r) {
+      int ih = ih0 + r;
+      if (ih < 0 || ih >= a.H) continue;
+      for (int s = 0; s < a.S; ++s) {
+        int iw = iw0 + s;
+        if (iw < 0 || iw >= a.W) continue;
+        T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
+        if (a.pre_relu) x = relu1(x);
+        max_to(acc, x);
+      }
+    }
+  } else {  // avg
+    int cnt = 0;
+    for (int r = 0; r < a.R; ++r) {
+      int ih = ih0 + r;
+      if (ih < 0 || ih >= a.H) continue;
+      for (int s = 0; s < a.S; ++s) {
+        int iw = iw0 + s;
+        if (iw < 0 || iw >= a.W) continue;
+        T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
+        if (a.pre_relu) x = relu1(x);
+        add_to(acc, x);
+        ++cnt;
+      }
+    }
+    int div = cnt;
+    if (a.count_pad) {  // torch: window clipped to [-pad, H + pad_bottom)
+      int hs = ih0, he = min(ih0 + a.R, a.H + a.pad_b);
+      int ws = iw0, we = min(iw0 + a.S, a.W + a.pad_r);
+      div = (he - hs) * (we - ws);
+    }
+    scale(acc, div > 0 ? 1.f / (float)div : 0.f);
+  }
+  if (a.has_res) add_to(acc, V::ld(a.res + n * a.res_sn + p * a.res_sh + q * a.res_sw + c));
+  acc = actv(acc, a.act);
+  V::st(a.out + n * a.out_sn + p * a.out_sh + q * a.out_sw + c, acc);
+}
+
+static bool can_vec4(const SpatialArgs& a, const sw_op_desc& op, bool has_w) {
+  if (a.C % 4 || a.in_sc != 1) return false;
+  if (a.in_sn % 4 || a.in_sh % 4 || a.in_sw % 4 || a.out_sn % 4 || a.out_sh % 4 || a.out_sw % 4) return false;
+  if (!aligned16(op.ptrs[PT_IN]) || !aligned16(op.ptrs[PT_OUT])) return false;
+  if (has_w && (!aligned16(op.ptrs[PT_W]) || (op.ptrs[PT_BIAS] && !aligned16(op.ptrs[PT_BIAS])))) return false;
+  if (a.has_res && (!aligned16(op.ptrs[PT_RES]) || a.res_sn % 4 || a.res_sh % 4 || a.res_sw % 4)) return false;
+  return true;
+}
+
+template <int KIND>
+static int launch_spatial(const sw_op_desc& op, void* stream) {
+  SpatialArgs a = spatial_args(op);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bool v4 = can_vec4(a, op, KIND == 0);
+  int64_t total = (int64_t)a.N * a.P * a.Q * (v4 ? a.C / 4 : a.C);
+  if (total == 0) return 0;
+  int blocks = (int)cdiv(total, 256);
+  if (v4)
+    spatial_kernel<KIND, 4><<<blocks, 256, 0, st>>>(a, total);
+  else
+    spatial_kernel<KIND, 1><<<blocks, 256, 0, st>>>(a, total);
+  return (int)cudaGetLastError();
+}
+
+int launch_dwconv(const sw_op_desc& op, void* stream) { return launch_spatial<0>(op, stream); }
+int launch_pool(const sw_op_desc& op, void* stream) { return launch_spatial<1>(op, stream); }
+
+}  // namespace sw

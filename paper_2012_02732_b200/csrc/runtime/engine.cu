@@ -1,0 +1,352 @@
+// Device runtime of the AoT engine (include/streamweave_b200.h, group 2).
+//
+// The pre_run schedule (schedule.py:352-414: per-stream FIFOs of LAUNCH /
+// RECORD / WAIT in a global capture order) is realised op for op under CUDA
+// stream capture:
+//   origin stream:  [H2D input memcpy] → fork event
+//   logical stream s (one cudaStream_t each): wait(fork) → its FIFO, where
+//       LAUNCH t   = kernel of op t,
+//       RECORD e   = cudaEventRecord(event e)      (one event per sync edge),
+//       WAIT e     = cudaStreamWaitEvent(event e)
+//   → join event per stream → origin waits all → [D2H output memcpy]
+// and instantiated once into a cudaGraphExec_t.  Replay is one
+// cudaGraphLaunch: no per-op host scheduling remains (the paper's point).
+// The captured edge set is exactly MEG edges (stream-order edges for matched
+// edges, event edges for sync edges) + memcpy→stream heads + stream
+// tails→memcpy; sw_engine_graph_topology exposes it for that check.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../planner/planner.h"
+#include "ops.h"
+
+namespace {
+
+constexpr int kSlots = 4;
+
+struct Slot {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::unordered_map<cudaGraphNode_t, int64_t> node_task;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    node_task.clear();
+  }
+};
+
+}  // namespace
+
+struct sw_engine {
+  int device = 0;
+  cudaStream_t launch = nullptr;
+  std::vector<cudaStream_t> streams;  // logical stream pool (capture)
+  std::vector<cudaEvent_t> events;    // one per sync edge (schedule.py:370)
+  std::vector<cudaEvent_t> joins;
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  std::vector<sw_op_desc> ops;
+  uint64_t host_in = 0, dev_in = 0, host_out = 0, dev_out = 0;
+  int64_t in_bytes = 0, out_bytes = 0;
+  Slot slots[kSlots];
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return sw::fail(SW_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+#define CU(expr)                                      \
+  do {                                                \
+    cudaError_t _e = (expr);                          \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+int launch_task(const sw_op_desc& op, cudaStream_t st) {
+  int rc = 0;
+  switch (op.kind) {
+    case sw::K_CONV: rc = sw::launch_conv(op, st); break;
+    case sw::K_CONV_TC: rc = sw::launch_conv_tc(op, st); break;
+    case sw::K_DWCONV: rc = sw::launch_dwconv(op, st); break;
+    case sw::K_POOL: rc = sw::launch_pool(op, st); break;
+    case sw::K_ELTWISE: rc = sw::launch_eltwise(op, st); break;
+    case sw::K_GLOBAL_POOL: rc = sw::launch_global_pool(op, st); break;
+    default: return sw::fail(SW_VALUE_ERROR, "unknown kernel kind " + std::to_string(op.kind));
+  }
+  if (rc != 0) return cuda_fail((cudaError_t)rc, "kernel launch");
+  return SW_OK;
+}
+
+int ensure_streams(sw_engine* e, int64_t n) {
+  while ((int64_t)e->streams.size() < n) {
+    cudaStream_t s;
+    CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    e->streams.push_back(s);
+    cudaEvent_t j;
+    CU(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+    e->joins.push_back(j);
+  }
+  return SW_OK;
+}
+
+int ensure_events(sw_engine* e, int64_t n) {
+  while ((int64_t)e->events.size() < n) {
+    cudaEvent_t ev;
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->events.push_back(ev);
+  }
+  return SW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sw_engine_create(int32_t device, sw_engine** out) {
+  auto* e = new sw_engine();
+  e->device = device;
+  cudaError_t err = cudaSetDevice(device);
+  if (err != cudaSuccess) {
+    delete e;
+    return cuda_fail(err, "cudaSetDevice");
+  }
+  CU(cudaStreamCreateWithFlags(&e->launch, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+  CU(cudaEventCreate(&e->t0));
+  CU(cudaEventCreate(&e->t1));
+  *out = e;
+  return SW_OK;
+}
+
+int sw_engine_destroy(sw_engine* e) {
+  if (!e) return SW_OK;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->launch);
+  for (auto& s : e->slots) s.reset();
+  for (auto s : e->streams) cudaStreamDestroy(s);
+  for (auto ev : e->events) cudaEventDestroy(ev);
+  for (auto ev : e->joins) cudaEventDestroy(ev);
+  cudaEventDestroy(e->fork);
+  cudaEventDestroy(e->t0);
+  cudaEventDestroy(e->t1);
+  cudaStreamDestroy(e->launch);
+  delete e;
+  return SW_OK;
+}
+
+int sw_engine_set_ops(sw_engine* e, int64_t n, const sw_op_desc* ops) {
+  e->ops.assign(ops, ops + n);
+  return SW_OK;
+}
+
+int sw_engine_set_io(sw_engine* e, uint64_t host_in, uint64_t dev_in, int64_t in_bytes, uint64_t host_out,
+                     uint64_t dev_out, int64_t out_bytes) {
+  e->host_in = host_in;
+  e->dev_in = dev_in;
+  e->in_bytes = in_bytes;
+  e->host_out = host_out;
+  e->dev_out = dev_out;
+  e->out_bytes = out_bytes;
+  return SW_OK;
+}
+
+int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64_t* stream_len,
+                      const int32_t* op_kind, const int64_t* op_arg, int64_t n_order, const int64_t* order,
+                      int32_t with_io) {
+  if (slot < 0 || slot >= kSlots) return sw::fail(SW_VALUE_ERROR, "slot out of range");
+  CU(cudaSetDevice(e->device));
+  Slot& sl = e->slots[slot];
+  sl.reset();
+  int rc = ensure_streams(e, n_streams);
+  if (rc) return rc;
+  int64_t max_event = -1;
+  std::vector<int64_t> base(n_streams + 1, 0);
+  for (int64_t s = 0; s < n_streams; ++s) base[s + 1] = base[s] + stream_len[s];
+  for (int64_t k = 0; k < base[n_streams]; ++k)
+    if (op_kind[k] != SW_OP_LAUNCH) max_event = std::max(max_event, op_arg[k]);
+    else if (op_arg[k] < 0 || op_arg[k] >= (int64_t)e->ops.size())
+      return sw::fail(SW_GRAPH_ERROR, "schedule launches unknown task " + std::to_string(op_arg[k]));
+  rc = ensure_events(e, max_event + 1);
+  if (rc) return rc;
+
+  cudaStream_t origin = e->launch;
+  CU(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
+  auto abort_capture = [&](int code) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(origin, &g);
+    if (g) cudaGraphDestroy(g);
+    return code;
+  };
+  cudaError_t err;
+  if (with_io && e->in_bytes > 0) {
+    err = cudaMemcpyAsync(reinterpret_cast<void*>(e->dev_in), reinterpret_cast<const void*>(e->host_in),
+                          (size_t)e->in_bytes, cudaMemcpyHostToDevice, origin);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture H2D"));
+  }
+  err = cudaEventRecord(e->fork, origin);
+  if (err != cudaSuccess) return abort_capture(cuda_fail(err, "fork record"));
+  for (int64_t s = 0; s < n_streams; ++s) {
+    err = cudaStreamWaitEvent(e->streams[s], e->fork, 0);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "fork wait"));
+  }
+  std::vector<int64_t> cursor(n_streams, 0);
+  for (int64_t i = 0; i < n_order; ++i) {
+    int64_t s = order[i];
+    if (s < 0 || s >= n_streams || cursor[s] >= stream_len[s])
+      return abort_capture(sw::fail(SW_VALUE_ERROR, "capture order does not match the stream FIFOs"));
+    int64_t k = base[s] + cursor[s]++;
+    cudaStream_t st = e->streams[s];
+    if (op_kind[k] == SW_OP_LAUNCH) {
+      int64_t t = op_arg[k];
+      rc = launch_task(e->ops[t], st);
+      if (rc) return abort_capture(rc);
+      cudaStreamCaptureStatus status;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      err = cudaStreamGetCaptureInfo(st, &status, nullptr, nullptr, &deps, &ndeps);
+      if (err == cudaSuccess && ndeps == 1) sl.node_task[deps[0]] = t;
+    } else if (op_kind[k] == SW_OP_RECORD) {
+      err = cudaEventRecord(e->events[op_arg[k]], st);
+      if (err != cudaSuccess) return abort_capture(cuda_fail(err, "event record"));
+    } else {
+      err = cudaStreamWaitEvent(st, e->events[op_arg[k]], 0);
+      if (err != cudaSuccess) return abort_capture(cuda_fail(err, "event wait"));
+    }
+  }
+  for (int64_t s = 0; s < n_streams; ++s) {
+    err = cudaEventRecord(e->joins[s], e->streams[s]);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "join record"));
+    err = cudaStreamWaitEvent(origin, e->joins[s], 0);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "join wait"));
+  }
+  if (with_io && e->out_bytes > 0) {
+    err = cudaMemcpyAsync(reinterpret_cast<void*>(e->host_out), reinterpret_cast<const void*>(e->dev_out),
+                          (size_t)e->out_bytes, cudaMemcpyDeviceToHost, origin);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture D2H"));
+  }
+  CU(cudaStreamEndCapture(origin, &sl.graph));
+  CU(cudaGraphInstantiateWithFlags(&sl.exec, sl.graph, 0));
+  CU(cudaGraphUpload(sl.exec, e->launch));
+  return SW_OK;
+}
+
+int sw_engine_replay(sw_engine* e, int32_t slot) {
+  if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
+  return SW_OK;
+}
+
+int sw_engine_replay_sync(sw_engine* e, int32_t slot, int64_t* out_launch_ns) {
+  if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  auto a = std::chrono::steady_clock::now();
+  CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
+  auto b = std::chrono::steady_clock::now();
+  CU(cudaStreamSynchronize(e->launch));
+  if (out_launch_ns) *out_launch_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+  return SW_OK;
+}
+
+int sw_engine_time_replay(sw_engine* e, int32_t slot, int32_t iters, double* out_gpu_us, double* out_host_us) {
+  if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  if (iters < 1) iters = 1;
+  CU(cudaStreamSynchronize(e->launch));
+  double host_ns = 0;
+  CU(cudaEventRecord(e->t0, e->launch));
+  for (int i = 0; i < iters; ++i) {
+    auto a = std::chrono::steady_clock::now();
+    CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
+    auto b = std::chrono::steady_clock::now();
+    host_ns += (double)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+  }
+  CU(cudaEventRecord(e->t1, e->launch));
+  CU(cudaEventSynchronize(e->t1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, e->t0, e->t1));
+  *out_gpu_us = (double)ms * 1000.0 / iters;
+  *out_host_us = host_ns / 1000.0 / iters;
+  return SW_OK;
+}
+
+int sw_engine_launch_op(sw_engine* e, int64_t index) {
+  if (index < 0 || index >= (int64_t)e->ops.size()) return sw::fail(SW_VALUE_ERROR, "op index out of range");
+  return launch_task(e->ops[index], e->launch);
+}
+
+int sw_engine_run_eager(sw_engine* e, int64_t n, const int64_t* order) {
+  for (int64_t i = 0; i < n; ++i) {
+    int rc = sw_engine_launch_op(e, order[i]);
+    if (rc) return rc;
+  }
+  return SW_OK;
+}
+
+int sw_engine_synchronize(sw_engine* e) {
+  CU(cudaStreamSynchronize(e->launch));
+  CU(cudaGetLastError());
+  return SW_OK;
+}
+
+int sw_engine_graph_topology(sw_engine* e, int32_t slot, int64_t cap, int64_t* out_n_nodes, int32_t* out_node_kind,
+                             int64_t* out_node_task, int64_t* out_n_edges, int64_t* out_edges) {
+  if (slot < 0 || slot >= kSlots || !e->slots[slot].graph) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  Slot& sl = e->slots[slot];
+  size_t nn = 0;
+  CU(cudaGraphGetNodes(sl.graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CU(cudaGraphGetNodes(sl.graph, nodes.data(), &nn));
+  std::unordered_map<cudaGraphNode_t, int64_t> idx;
+  for (size_t i = 0; i < nn; ++i) idx[nodes[i]] = (int64_t)i;
+  *out_n_nodes = (int64_t)nn;
+  if ((int64_t)nn > cap) return sw::fail(SW_VALUE_ERROR, "topology buffer too small");
+  for (size_t i = 0; i < nn; ++i) {
+    cudaGraphNodeType t;
+    CU(cudaGraphNodeGetType(nodes[i], &t));
+    out_node_kind[i] = t == cudaGraphNodeTypeKernel ? 0 : (t == cudaGraphNodeTypeMemcpy ? 1 : 2);
+    auto it = sl.node_task.find(nodes[i]);
+    out_node_task[i] = it == sl.node_task.end() ? -1 : it->second;
+  }
+  size_t ne = 0;
+  CU(cudaGraphGetEdges(sl.graph, nullptr, nullptr, &ne));
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  if (ne) CU(cudaGraphGetEdges(sl.graph, from.data(), to.data(), &ne));
+  *out_n_edges = (int64_t)ne;
+  if ((int64_t)ne > cap) return sw::fail(SW_VALUE_ERROR, "topology buffer too small");
+  for (size_t i = 0; i < ne; ++i) {
+    out_edges[2 * i] = idx[from[i]];
+    out_edges[2 * i + 1] = idx[to[i]];
+  }
+  return SW_OK;
+}
+
+int sw_engine_profile_ops(sw_engine* e, int64_t n, const int64_t* order, int32_t reps, double* out_us) {
+  if (reps < 1) reps = 1;
+  CU(cudaStreamSynchronize(e->launch));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t t = order[i];
+    CU(cudaEventRecord(e->t0, e->launch));
+    for (int r = 0; r < reps; ++r) {
+      int rc = launch_task(e->ops[t], e->launch);
+      if (rc) return rc;
+    }
+    CU(cudaEventRecord(e->t1, e->launch));
+    CU(cudaEventSynchronize(e->t1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e->t0, e->t1));
+    out_us[i] = (double)ms * 1000.0 / reps;
+  }
+  return SW_OK;
+}
+
+int sw_engine_stream(sw_engine* e, uint64_t* out_stream) {
+  *out_stream = reinterpret_cast<uint64_t>(e->launch);
+  return SW_OK;
+}
+
+}  // extern "C"
