@@ -1,0 +1,381 @@
+"""Benchmark: Nimble-style AoT engine on B200 vs the reference CPU path.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config nasnet_mobile --batch 1]
+    python bench.py --impl reference ...        # the CPU path, same metric
+
+Workload (BASELINE.json north_star target): NASNet-A mobile, batch-1 fp32
+inference, multi-stream AoT CUDA-graph replay.  One step = one forward pass
+of one batch per GPU.  Multi-GPU = independent replicas (batch-1 latency does
+not shard), one process per GPU under torchrun, weak scaling.
+
+Printed JSON (rank 0): value = whole-job images/s with the input already in
+HBM (device-resident replay, L2 flushed between steps); e2e = the same metric
+through the public API call engine(x_host) (pinned H2D + graph + D2H inside
+the timed region).  Extra keys: batch-1 latency, the same engine's
+single-stream AoT replay and non-AoT eager launch loop, host launch overhead
+per iteration and its fraction of GPU time, Σ per-kernel roofline, roofline
+object for the dominant kernel family, CPU baseline, clocks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batch-1 inference latency (µs) + images/s on 1/2/4/8 B200; vs ref CPU path"
+UNIT = "images/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/sw_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend, init_method="env://")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reduce_max(world, value, device=None):
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------
+# reference arm: the CPU path (oracle restatement) on the host cores
+# ----------------------------------------------------------------------------
+
+def cpu_path_run(config, batch, steps, warmup, threads):
+    """The reference CPU path for this workload (SURVEY §8(d) mode 4): the
+    planner restatement (assign_streams + pre_run, oracle/planner.py, run once
+    as the reference does at prepare time) and the fp32 CPU forward of the same
+    module (oracle/numerics.py) per step."""
+    import torch
+    from oracle import planner as O
+    from oracle.numerics import cpu_forward
+    from paper_2012_02732_b200.networks import build_model, example_input
+    from paper_2012_02732_b200.trace import build_program
+
+    torch.set_num_threads(threads)
+    model, shape = build_model(config)
+    x = example_input(shape, batch=batch)
+    prog = build_program(model, x, fuse=True)
+    g = prog.graph
+    nodes = [(t.id, t.duration, t.demand, tuple((e.kind, e.size) for e in t.mem)) for t in g.nodes]
+    t0 = time.perf_counter()
+    f, plan, _ = O.assign(nodes, list(g.edges))
+    O.pre_run(nodes, list(g.edges), f, plan)
+    plan_s = time.perf_counter() - t0
+    for _ in range(warmup):
+        cpu_forward(model, x)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        cpu_forward(model, x)
+        times.append(time.perf_counter() - t)
+    return times, plan_s
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle.numerics import cpu_threads
+    threads = cpu_threads()
+    times, plan_s = cpu_path_run(args.config, args.batch, args.steps, args.warmup, threads)
+    mean = sum(times) / len(times)
+    value = args.batch / mean
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(mean * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded randn input, random-init weights)",
+        "config": {"workload": f"{args.config} batch-{args.batch} fp32 inference, CPU path",
+                   "batch_per_replica": args.batch},
+        "latency_us": round(mean * 1e6, 1),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} forward passes of {args.config} bs{args.batch} "
+                                   f"(torch CPU fp32, same module) + one oracle planner pass "
+                                   f"({plan_s * 1e3:.1f} ms)"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "planner_ms": round(plan_s * 1e3, 3),
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import Engine, task_cost
+    from paper_2012_02732_b200.networks import build_model, example_input
+    import ctypes as C
+
+    hbm, bf16, peak_src = load_peaks()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    model, shape = build_model(args.config)
+    x = example_input(shape, batch=args.batch, seed=1 + rank)
+    eng = Engine(model, multi_stream=True, device=local).prepare(x)
+    # correctness gate before timing (cheap at batch 1)
+    y = eng(x)
+    parity = None
+    if rank == 0 and args.batch <= 8:
+        from oracle.numerics import cpu_forward
+        ref = cpu_forward(model, x)
+        err = (y - ref).abs().max().item()
+        parity = {"max_abs_err": err, "ok": bool(torch.allclose(y, ref, rtol=1e-3, atol=1e-4))}
+
+    sh = C.c_uint64()
+    N.check(N.lib().sw_engine_stream(eng._h, C.byref(sh)))
+    stream = torch.cuda.ExternalStream(sh.value, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    eng.load_input_device(x)
+
+    def timed_replays(multi, steps):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        with torch.cuda.stream(stream):
+            for a, b in ev:
+                flush.zero_()
+                a.record(stream)
+                eng.replay(multi=multi)
+                b.record(stream)
+        torch.cuda.synchronize(dev)
+        return [a.elapsed_time(b) for a, b in ev]
+
+    for _ in range(args.warmup):
+        eng.replay(multi=True)
+        eng.replay(multi=False)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = timed_replays(True, args.steps)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clock_info = clocks.stop()
+    ms = sum(times) / len(times)
+    ms_max = reduce_max(world, ms, dev)
+    value = world * args.batch / (ms_max / 1e3)
+
+    # same engine, other modes (same flush discipline)
+    single = timed_replays(False, args.steps)
+    single_ms = sum(single) / len(single)
+
+    def eager_once():
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        eng.run_eager(python_loop=True)
+        eng.synchronize()
+        return time.perf_counter() - t
+
+    for _ in range(3):
+        eager_once()
+    eager = [eager_once() for _ in range(max(5, args.steps // 4))]
+    eager_ms = 1e3 * sum(eager) / len(eager)
+
+    # e2e through the public API: host tensor in, host tensor out
+    xh = x.clone()
+    for _ in range(3):
+        eng(xh)
+    e2e_times = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        eng(xh)
+        e2e_times.append(time.perf_counter() - t)
+    e2e_ms = 1e3 * sum(e2e_times) / len(e2e_times)
+    e2e_ms_max = reduce_max(world, e2e_ms, dev)
+
+    # host launch overhead per iteration (cudaGraphLaunch call) vs GPU time
+    gpu_us, host_us = eng.time_replay(multi=True, iters=200)
+
+    # per-task device times (eager, serialised) → dominant kernel family roofline
+    per_task = eng.profile_tasks(reps=10)
+    fam = {}
+    for t in eng.program.tasks:
+        f_, b_ = task_cost(t)
+        k = t.kind
+        d = fam.setdefault(k, {"us": 0.0, "flops": 0.0, "bytes": 0.0, "n": 0})
+        d["us"] += per_task[t.tid]
+        d["flops"] += f_
+        d["bytes"] += b_
+        d["n"] += 1
+    dom = max(fam, key=lambda k: fam[k]["us"])
+    dd = fam[dom]
+    achieved = dd["bytes"] / (dd["us"] * 1e-6) / 1e9
+    roof_sum = eng.roofline_sum_us(hbm, bf16)
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.skip_cpu:
+            from oracle.numerics import cpu_threads
+            thr = cpu_threads()
+            nsteps = max(3, int(args.cpu_seconds / 0.05))
+            t0 = time.perf_counter()
+            ct, plan_s = cpu_path_run(args.config, args.batch, nsteps, 2, thr)
+            cpu_val = args.batch / (sum(ct) / len(ct))
+            cpu = {"value": round(cpu_val, 3), "unit": UNIT, "cores": thr, "kind": "port",
+                   "sample": f"{nsteps} fp32 CPU forwards of {args.config} bs{args.batch} "
+                             f"(same module; oracle/numerics.py) + oracle planner "
+                             f"{plan_s * 1e3:.1f} ms; {time.perf_counter() - t0:.1f} s total"}
+        n_tasks = len(eng.program.tasks)
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded randn input, random-init weights, randomized BN stats)",
+            "config": {"workload": f"{args.config} batch-{args.batch} fp32 inference, "
+                                   f"multi-stream AoT CUDA-graph replay",
+                       "batch_per_replica": args.batch, "replicas": world,
+                       "parallelism": f"replicas{world}",
+                       "l2": "flushed (512 MB write) before every timed step"},
+            "latency_us": round(ms_max * 1e3, 2),
+            "modes": {
+                "multi_stream_aot_us": round(ms * 1e3, 2),
+                "single_stream_aot_us": round(single_ms * 1e3, 2),
+                "eager_non_aot_us": round(eager_ms * 1e3, 2),
+                "multi_over_single": round(single_ms / ms, 4),
+                "aot_over_eager": round(eager_ms / ms, 4),
+            },
+            "host_overhead": {"launch_us_per_iter": round(host_us, 3),
+                              "gpu_us_per_iter": round(gpu_us, 3),
+                              "fraction_of_gpu_time": round(host_us / gpu_us, 5)},
+            "roofline_sum_us": round(roof_sum, 3),
+            "latency_over_roofline_sum": round(ms * 1e3 / roof_sum, 3),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 5), "traffic": None,
+                         "kernel": f"{dom} family ({dd['n']} launches, "
+                                   f"{dd['us'] / n_tasks:.2f} µs avg/task)",
+                         "peak_source": peak_src},
+            "e2e": {"value": round(world * args.batch / (e2e_ms_max / 1e3), 3), "unit": UNIT,
+                    "ms_per_step": round(e2e_ms_max, 5),
+                    "h2d_bytes_per_step": int(eng.h_in.numel() * 4),
+                    "d2h_bytes_per_step": int(eng.out_bytes)},
+            "gpu_launches": n_tasks * args.steps,
+            "tasks": n_tasks, "streams": eng.assignment.num_streams, "syncs": len(eng.plan),
+            "clocks": clock_info,
+            "parity": parity,
+            "prepare_s": {k: round(v, 3) for k, v in eng.plan_seconds.items()},
+            "kernel_families_us": {k: round(v["us"], 2) for k, v in fam.items()},
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    eng.close()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="nasnet_mobile")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -28,7 +28,7 @@ struct ConvArgs {
   const float* __restrict__ res;
   int N, H, W, C, P, Q, K, R, S, sh, sw, ph, pw, act, pre_relu, has_res;
   int64_t in_sn, in_sh, in_sw, in_sc;
-  int64_t out_sn, out_sh, out_sw;
+  int64_t out_sn, out_sh, out_sw, out_sc;
   int64_t res_sn, res_sh, res_sw;
   int M, Kdim, split;
 };
@@ -49,6 +49,7 @@ static ConvArgs conv_args(const sw_op_desc& op) {
   a.act = (int)p[SP_ACT]; a.pre_relu = (int)p[SP_PRE_RELU]; a.has_res = (int)p[SP_HAS_RES];
   a.in_sn = p[SP_IN_SN]; a.in_sh = p[SP_IN_SH]; a.in_sw = p[SP_IN_SW]; a.in_sc = p[SP_IN_SC];
   a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
+  a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
   a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
   a.M = a.N * a.P * a.Q;
   a.Kdim = a.R * a.S * a.C;
@@ -63,7 +64,7 @@ __device__ __forceinline__ void conv_epilogue_store(const ConvArgs& a, int m, in
   int nb = t / a.P;
   v += a.bias ? a.bias[n] : 0.f;
   if (a.has_res) v += a.res[nb * a.res_sn + pp * a.res_sh + q * a.res_sw + n];
-  a.out[nb * a.out_sn + pp * a.out_sh + q * a.out_sw + n] = apply_act(v, a.act);
+  a.out[nb * a.out_sn + pp * a.out_sh + q * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
 }
 
 // BM x BN output tile, 4x4 micro-tile per thread, BK = 16, register-staged

@@ -150,3 +150,56 @@ int launch_global_pool(const sw_op_desc& d, void* stream) {
 }
 
 }  // namespace sw
+
+namespace sw {
+
+// Unfused concat (fuse=False programs only): one launch copies up to 7 dense
+// NHWC inputs into their channel slices of the output.
+struct ConcatArgs {
+  const float* in[7];
+  float* out;
+  int c_in[7];
+  int c_off[8];
+  int N, H, W, nin, ctot;
+  int64_t out_sc, out_sp;  // output channel stride, pixel stride
+  int64_t hw;
+};
+
+__global__ void __launch_bounds__(256) concat_kernel(ConcatArgs a, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int c = (int)(idx % a.ctot);
+  int64_t pix = idx / a.ctot;  // n*H*W + h*W + w
+  int i = 0;
+  while (i + 1 < a.nin && c >= a.c_off[i + 1]) ++i;
+  int cl = c - a.c_off[i];
+  float v = a.in[i][pix * a.c_in[i] + cl];
+  int64_t n = pix / a.hw, hw = pix % a.hw;
+  int64_t dst = (a.out_sc == 1) ? pix * a.out_sp + c : n * (int64_t)a.ctot * a.hw + c * a.out_sc + hw;
+  a.out[dst] = v;
+}
+
+int launch_concat(const sw_op_desc& d, void* stream) {
+  const int64_t* p = d.params;
+  ConcatArgs a;
+  a.N = (int)p[0]; a.H = (int)p[1]; a.W = (int)p[2]; a.nin = (int)p[3]; a.ctot = (int)p[4];
+  a.out_sc = p[5] ? p[5] : 1;
+  a.out_sp = p[6] ? p[6] : a.ctot;
+  a.hw = (int64_t)a.H * a.W;
+  if (a.nin < 1 || a.nin > 7) return (int)cudaErrorInvalidValue;
+  int off = 0;
+  for (int i = 0; i < a.nin; ++i) {
+    a.in[i] = reinterpret_cast<const float*>(d.ptrs[i]);
+    a.c_in[i] = (int)p[8 + i];
+    a.c_off[i] = off;
+    off += a.c_in[i];
+  }
+  a.c_off[a.nin] = off;
+  a.out = reinterpret_cast<float*>(d.ptrs[7]);
+  int64_t total = (int64_t)a.N * a.hw * a.ctot;
+  if (total == 0) return 0;
+  concat_kernel<<<(unsigned)cdiv(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a, total);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sw

@@ -21,7 +21,7 @@ struct SpatialArgs {
   const float* __restrict__ res;
   int N, H, W, C, P, Q, R, S, sh, sw, ph, pw, act, pre_relu, has_res, mode, count_pad, pad_b, pad_r;
   int64_t in_sn, in_sh, in_sw, in_sc;
-  int64_t out_sn, out_sh, out_sw;
+  int64_t out_sn, out_sh, out_sw, out_sc;
   int64_t res_sn, res_sh, res_sw;
 };
 
@@ -43,6 +43,7 @@ static SpatialArgs spatial_args(const sw_op_desc& op) {
   a.pad_b = (int)p[SP_PAD_BOTTOM]; a.pad_r = (int)p[SP_PAD_RIGHT];
   a.in_sn = p[SP_IN_SN]; a.in_sh = p[SP_IN_SH]; a.in_sw = p[SP_IN_SW]; a.in_sc = p[SP_IN_SC];
   a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
+  a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
   a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
   return a;
 }
@@ -153,11 +154,17 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
   }
   if (a.has_res) add_to(acc, V::ld(a.res + n * a.res_sn + p * a.res_sh + q * a.res_sw + c));
   acc = actv(acc, a.act);
-  V::st(a.out + n * a.out_sn + p * a.out_sh + q * a.out_sw + c, acc);
+  float* dst = a.out + n * a.out_sn + p * a.out_sh + q * a.out_sw + c * a.out_sc;
+  if (VEC == 1 || a.out_sc == 1) {
+    V::st(dst, acc);
+  } else {
+    const float* v = reinterpret_cast<const float*>(&acc);
+    for (int i = 0; i < VEC; ++i) dst[i * a.out_sc] = v[i];
+  }
 }
 
 static bool can_vec4(const SpatialArgs& a, const sw_op_desc& op, bool has_w) {
-  if (a.C % 4 || a.in_sc != 1) return false;
+  if (a.C % 4 || a.in_sc != 1 || a.out_sc != 1) return false;
   if (a.in_sn % 4 || a.in_sh % 4 || a.in_sw % 4 || a.out_sn % 4 || a.out_sh % 4 || a.out_sw % 4) return false;
   if (!aligned16(op.ptrs[PT_IN]) || !aligned16(op.ptrs[PT_OUT])) return false;
   if (has_w && (!aligned16(op.ptrs[PT_W]) || (op.ptrs[PT_BIAS] && !aligned16(op.ptrs[PT_BIAS])))) return false;

@@ -78,6 +78,7 @@ int launch_task(const sw_op_desc& op, cudaStream_t st) {
     case sw::K_POOL: rc = sw::launch_pool(op, st); break;
     case sw::K_ELTWISE: rc = sw::launch_eltwise(op, st); break;
     case sw::K_GLOBAL_POOL: rc = sw::launch_global_pool(op, st); break;
+    case sw::K_CONCAT: rc = sw::launch_concat(op, st); break;
     default: return sw::fail(SW_VALUE_ERROR, "unknown kernel kind " + std::to_string(op.kind));
   }
   if (rc != 0) return cuda_fail((cudaError_t)rc, "kernel launch");

@@ -20,7 +20,10 @@ enum KernelKind : int32_t {
   K_ELTWISE = 4,     // add / mul / affine / copy over up to 3 broadcastable operands
   K_GLOBAL_POOL = 5, // global average pool over H x W
   K_CONV_TC = 6,     // dense conv / GEMM on tcgen05 tensor cores (3xTF32)
+  K_CONCAT = 7,      // unfused channel concat of up to 7 dense NHWC inputs
 };
+// K_CONCAT params: 0 N, 1 H, 2 W, 3 n_in, 4 C_total, 5 out channel stride,
+// 6 out pixel stride, 8.. C_i; ptrs 0..6 inputs, 7 output.
 
 enum Act : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_RELU6 = 2, ACT_SILU = 3, ACT_SIGMOID = 4 };
 
@@ -34,14 +37,14 @@ enum SpatialParam : int {
   SP_PAD_H, SP_PAD_W,                  // top / left padding (may be negative)
   SP_ACT, SP_PRE_RELU,                 // epilogue act; ReLU applied to inputs on load
   SP_IN_SN, SP_IN_SH, SP_IN_SW, SP_IN_SC,
-  SP_OUT_SN, SP_OUT_SH, SP_OUT_SW,     // output channel stride is 1
+  SP_OUT_SN, SP_OUT_SH, SP_OUT_SW,     // output channel stride: SP_OUT_SC
   SP_RES_SN, SP_RES_SH, SP_RES_SW,     // residual (added before act), channel stride 1
   SP_HAS_RES,
   SP_POOL_MODE,                        // 0 max, 1 avg
   SP_COUNT_PAD,                        // avg: count_include_pad
   SP_PAD_BOTTOM, SP_PAD_RIGHT,         // avg count_include_pad window clamp
   SP_SPLIT_K,                          // K_CONV: split-K cluster size (1 = none)
-  SP_RESERVED
+  SP_OUT_SC                            // output channel stride (1 = NHWC, H*W = NCHW output)
 };
 // ptrs: 0 in, 1 out, 2 weight, 3 bias, 4 residual, 5 workspace
 enum SpatialPtr : int { PT_IN = 0, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS };
@@ -66,5 +69,6 @@ int launch_dwconv(const sw_op_desc& op, void* stream);
 int launch_pool(const sw_op_desc& op, void* stream);
 int launch_eltwise(const sw_op_desc& op, void* stream);
 int launch_global_pool(const sw_op_desc& op, void* stream);
+int launch_concat(const sw_op_desc& op, void* stream);
 
 }  // namespace sw

@@ -1,0 +1,459 @@
+"""The AoT engine: ``Engine(model).prepare(example)`` then ``engine(x)``.
+
+PAPER.md:66 wraps a model instance in a Nimble object; PAPER.md:268-274
+describes the pre-run with a dummy input under CUDA Stream Capture and the
+replay with CUDA Graph Launch.  Here:
+
+  prepare(example)
+    1. op-DAG builder (trace.py): fx trace → fused tasks → CompGraph
+    2. stream assignment (native, bit-exact with the reference)
+    3. pre_run (native): per-stream FIFOs, event ids, arena layout — the
+       reference arena (no frees: every tensor lives for the whole pass,
+       which is what keeps it race-free across streams) gives each
+       activation its offset in ONE device allocation
+    4. lowering: one sw_op_desc per task (kernel kind, tile variant, strides,
+       device pointers into the arena / packed weights)
+    5. AoT capture (native): the schedule op for op into CUDA graphs —
+       slot 0 multi-stream + H2D/D2H memcpy nodes, slot 1 single-stream +
+       memcpys, slots 2/3 the same without memcpys (device-resident inputs)
+  __call__(x)  one C-ABI call: pinned staging copy → cudaGraphLaunch → wait.
+
+There is no CPU path: on a host without the native library or without a
+CUDA device, prepare() raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .assign import StreamAssignment, SyncPlan, assign_streams_full
+from .errors import CudaError
+from .schedule import TaskSchedule, pre_run, schedule_arrays
+from .trace import ACT_NONE, Program, Task, View, build_program
+
+# kernel kinds / enums (csrc/runtime/ops.h)
+K_CONV, K_DWCONV, K_POOL, K_ELTWISE, K_GLOBAL_POOL, K_CONV_TC, K_CONCAT = 1, 2, 3, 4, 5, 6, 7
+EW_ADD, EW_MUL, EW_AFFINE, EW_COPY = 0, 1, 2, 3
+(SP_N, SP_H, SP_W, SP_C, SP_P, SP_Q, SP_K, SP_R, SP_S, SP_STRIDE_H, SP_STRIDE_W, SP_PAD_H,
+ SP_PAD_W, SP_ACT, SP_PRE_RELU, SP_IN_SN, SP_IN_SH, SP_IN_SW, SP_IN_SC, SP_OUT_SN, SP_OUT_SH,
+ SP_OUT_SW, SP_RES_SN, SP_RES_SH, SP_RES_SW, SP_HAS_RES, SP_POOL_MODE, SP_COUNT_PAD,
+ SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC) = range(32)
+PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS = range(6)
+(EW_N, EW_H, EW_W, EW_C, EW_OP, EW_ACT, EW_A_SN, EW_A_SH, EW_A_SW, EW_A_SC, EW_B_SN, EW_B_SH,
+ EW_B_SW, EW_B_SC, EW_C_SN, EW_C_SH, EW_C_SW, EW_C_SC, EW_O_SN, EW_O_SH, EW_O_SW, EW_O_SC,
+ EW_NIN, EW_PRE_RELU) = range(24)
+EP_A, EP_B, EP_C, EP_OUT, EP_SCALE, EP_SHIFT = range(6)
+
+NUM_SMS = 148
+SLOT_MULTI_IO, SLOT_SINGLE_IO, SLOT_MULTI, SLOT_SINGLE = 0, 1, 2, 3
+
+
+# ----------------------------------------------------------------------------
+# kernel selection
+# ----------------------------------------------------------------------------
+
+def pick_conv_variant(M: int, K: int, Kdim: int, R: int, S: int, pad, stride) -> tuple[int, int]:
+    """(variant, split_k) for the SIMT implicit-GEMM conv (csrc/kernels/conv.cu)."""
+    if M <= 8 and R == 1 and S == 1 and tuple(pad) == (0, 0):
+        return 8, 1
+    for v, bm, bn in ((3, 128, 64), (0, 64, 64), (1, 32, 64)):
+        if math.ceil(M / bm) * math.ceil(K / bn) >= NUM_SMS:
+            return v, 1
+    ctas = math.ceil(M / 32) * math.ceil(K / 32)
+    ksteps = math.ceil(Kdim / 16)
+    split = 1
+    while split < 8 and ctas * split * 2 <= 2 * NUM_SMS and ksteps // (split * 2) >= 4:
+        split *= 2
+    return 2, split
+
+
+# ----------------------------------------------------------------------------
+# lowering: Program tasks → sw_op_desc table
+# ----------------------------------------------------------------------------
+
+@dataclass
+class Lowered:
+    ops: object            # ctypes array of OpDesc
+    weights: list          # (name, np.ndarray) in packing order
+    weight_offsets: list
+    weight_bytes: int
+
+
+def _vptr(v: View, base_of) -> int:
+    return base_of(v.st) + 4 * v.elem_offset()
+
+
+def _strides(v: View):
+    return v.strides()
+
+
+def _pack_weights(prog: Program):
+    """Kernel-layout parameter arrays per task (host numpy, fp32)."""
+    arrays = {}
+    for t in prog.tasks:
+        n = t.node
+        if t.kind == "conv":
+            w = n.attrs["weight"].float().permute(0, 2, 3, 1).contiguous()  # [K][R][S][C]
+            arrays[(t.tid, "w")] = w.numpy().reshape(-1)
+            if n.attrs["bias"] is not None:
+                arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
+        elif t.kind == "dwconv":
+            w = n.attrs["weight"].float()[:, 0].permute(1, 2, 0).contiguous()  # [R][S][C]
+            arrays[(t.tid, "w")] = w.numpy().reshape(-1)
+            if n.attrs["bias"] is not None:
+                arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
+        elif t.kind == "affine":
+            arrays[(t.tid, "scale")] = n.attrs["scale"].float().numpy().reshape(-1)
+            arrays[(t.tid, "shift")] = n.attrs["shift"].float().numpy().reshape(-1)
+    return arrays
+
+
+def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict):
+    """Encode every task as an sw_op_desc; pointers via base_of(storage)."""
+    ops = (N.OpDesc * len(prog.tasks))()
+    for t in prog.tasks:
+        d = ops[t.tid]
+        p = d.params
+        q = d.ptrs
+        wptr = lambda key: weight_base + weight_offsets[(t.tid, key)] if (t.tid, key) in weight_offsets else 0  # noqa: E731
+        if t.kind in ("conv", "dwconv", "pool"):
+            n = t.node
+            x = t.inputs[0]
+            st_in = x.st
+            nb, h, w, c = st_in.n, st_in.h, st_in.w, x.c
+            o = t.out
+            oc = o.c
+            P, Q = o.st.h, o.st.w
+            if t.kind == "pool":
+                R, S = n.attrs["k"]
+            else:
+                R, S = n.attrs["k"]
+            sh, sw_ = n.attrs["stride"]
+            ph, pw = n.attrs["pad"]
+            vals = {SP_N: nb, SP_H: h, SP_W: w, SP_C: c, SP_P: P, SP_Q: Q, SP_K: oc, SP_R: R,
+                    SP_S: S, SP_STRIDE_H: sh, SP_STRIDE_W: sw_, SP_PAD_H: ph, SP_PAD_W: pw,
+                    SP_ACT: n.act, SP_PRE_RELU: int(n.pre_relu)}
+            isn, ish, isw, isc = _strides(x)
+            osn, osh, osw, osc = _strides(o)
+            vals.update({SP_IN_SN: isn, SP_IN_SH: ish, SP_IN_SW: isw, SP_IN_SC: isc,
+                         SP_OUT_SN: osn, SP_OUT_SH: osh, SP_OUT_SW: osw, SP_OUT_SC: osc})
+            if t.residual is not None:
+                r = t.residual
+                rsn, rsh, rsw, rsc = _strides(r)
+                if rsc != 1:
+                    raise NotImplementedError("residual with non-unit channel stride")
+                vals.update({SP_RES_SN: rsn, SP_RES_SH: rsh, SP_RES_SW: rsw, SP_HAS_RES: 1})
+                q[PT_RES] = _vptr(r, base_of)
+            if t.kind == "pool":
+                vals[SP_POOL_MODE] = 0 if n.attrs["mode"] == "max" else 1
+                vals[SP_COUNT_PAD] = int(n.attrs["cip"])
+                vals[SP_PAD_BOTTOM] = ph
+                vals[SP_PAD_RIGHT] = pw
+                d.kind = K_POOL
+            elif t.kind == "dwconv":
+                d.kind = K_DWCONV
+                q[PT_W] = wptr("w")
+                q[PT_BIAS] = wptr("b")
+            else:
+                d.kind = K_CONV
+                q[PT_W] = wptr("w")
+                q[PT_BIAS] = wptr("b")
+                M = nb * P * Q
+                Kdim = R * S * c
+                variant, split = pick_conv_variant(M, oc, Kdim, R, S, (ph, pw), (sh, sw_))
+                d.variant = variant
+                vals[SP_SPLIT_K] = split
+            for k, v in vals.items():
+                p[k] = int(v)
+            q[PT_IN] = _vptr(x, base_of)
+            q[PT_OUT] = _vptr(o, base_of)
+        elif t.kind in ("add", "mul", "affine", "act", "copy", "gpool"):
+            o = t.out
+            nb, oh, ow, oc = o.st.n, o.st.h, o.st.w, o.c
+            d.kind = K_GLOBAL_POOL if t.kind == "gpool" else K_ELTWISE
+            if t.kind == "gpool":
+                x = t.inputs[0]
+                nb, oh, ow, oc = x.st.n, x.st.h, x.st.w, x.c
+            vals = {EW_N: nb, EW_H: oh, EW_W: ow, EW_C: oc,
+                    EW_ACT: t.node.act if t.node is not None and t.kind != "act" else 0,
+                    EW_NIN: len(t.inputs)}
+            if t.kind == "act":
+                vals[EW_ACT] = t.node.attrs["act"]
+            vals[EW_OP] = {"add": EW_ADD, "mul": EW_MUL, "affine": EW_AFFINE, "act": EW_COPY,
+                           "copy": EW_COPY, "gpool": EW_COPY}[t.kind]
+            if t.kind == "gpool":
+                vals[EW_PRE_RELU] = int(t.node.pre_relu)
+            slots = ((EW_A_SN, EP_A), (EW_B_SN, EP_B), (EW_C_SN, EP_C))
+            for i, v in enumerate(t.inputs):
+                s = list(_strides(v))
+                # broadcast: size-1 dims of a smaller operand get stride 0
+                if t.kind != "gpool":
+                    if v.st.h == 1 and oh > 1:
+                        s[1] = 0
+                    if v.st.w == 1 and ow > 1:
+                        s[2] = 0
+                    if v.st.n == 1 and nb > 1:
+                        s[0] = 0
+                base_idx, ptr_idx = slots[i]
+                for j in range(4):
+                    p[base_idx + j] = int(s[j])
+                q[ptr_idx] = _vptr(v, base_of)
+            osn, osh, osw, osc = _strides(o)
+            for j, sv in enumerate((osn, osh, osw, osc)):
+                p[EW_O_SN + j] = int(sv)
+            for k, v in vals.items():
+                p[k] = int(v)
+            q[EP_OUT] = _vptr(o, base_of)
+            if t.kind == "affine":
+                q[EP_SCALE] = wptr("scale")
+                q[EP_SHIFT] = wptr("shift")
+        elif t.kind == "concat":
+            o = t.out
+            d.kind = K_CONCAT
+            if len(t.inputs) > 7:
+                raise NotImplementedError("concat of more than 7 tensors")
+            osn, osh, osw, osc = _strides(o)
+            vals = [o.st.n, o.st.h, o.st.w, len(t.inputs), o.c, osc, osw if osc == 1 else 0, 0]
+            for i, v in enumerate(vals):
+                p[i] = int(v)
+            for i, v in enumerate(t.inputs):
+                if v.st.nchw or v.c != v.st.c:
+                    raise NotImplementedError("unfused concat of strided inputs")
+                p[8 + i] = v.c
+                q[i] = _vptr(v, base_of)
+            q[7] = _vptr(o, base_of)
+        else:
+            raise NotImplementedError(t.kind)
+    return ops
+
+
+def task_cost(t: Task) -> tuple[float, float]:
+    """(flops, algorithmic bytes) of one task at fp32."""
+    o = t.out
+    out_elems = o.st.n * o.st.h * o.st.w * o.c
+    in_bytes = sum(v.st.n * v.st.h * v.st.w * v.c * 4 for v in t.inputs)
+    res_bytes = (t.residual.st.n * t.residual.st.h * t.residual.st.w * t.residual.c * 4) \
+        if t.residual is not None else 0
+    flops = 0.0
+    wbytes = 0
+    if t.kind == "conv":
+        R, S = t.node.attrs["k"]
+        c = t.inputs[0].c
+        flops = 2.0 * out_elems * R * S * c
+        wbytes = (o.c * R * S * c + o.c) * 4
+    elif t.kind == "dwconv":
+        R, S = t.node.attrs["k"]
+        flops = 2.0 * out_elems * R * S
+        wbytes = (o.c * R * S + o.c) * 4
+    elif t.kind == "pool":
+        R, S = t.node.attrs["k"]
+        flops = 1.0 * out_elems * R * S
+    else:
+        flops = float(out_elems)
+    return flops, float(in_bytes + res_bytes + wbytes + out_elems * 4)
+
+
+def roofline_us(t: Task, hbm_gbs: float, tflops: float) -> float:
+    f, b = task_cost(t)
+    return max(f / (tflops * 1e12), b / (hbm_gbs * 1e9)) * 1e6
+
+
+# ----------------------------------------------------------------------------
+# Engine
+# ----------------------------------------------------------------------------
+
+class Engine:
+    """Nimble-style AoT engine around a static ``nn.Module`` (eval mode, fp32)."""
+
+    def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
+                 device: int = 0):
+        self.model = model.eval()
+        self.multi_stream = multi_stream
+        self.fuse = fuse
+        self.device = device
+        self._h = None
+        self.prepared = False
+
+    # -- preparation ------------------------------------------------------
+    def prepare(self, example: torch.Tensor) -> "Engine":
+        lib = N.lib()
+        if not torch.cuda.is_available():
+            raise CudaError("Engine.prepare needs a CUDA device (there is no CPU fallback)")
+        t0 = time.perf_counter()
+        ex = example.detach().float().cpu().contiguous()
+        prog = build_program(self.model, ex, fuse=self.fuse)
+        t1 = time.perf_counter()
+        g = prog.graph
+        f, plan, meg = assign_streams_full(g)
+        ts = pre_run(g, f, plan)
+        single_f = StreamAssignment({t.id: 0 for t in g.nodes})
+        ts_single = pre_run(g, single_f, SyncPlan(()))
+        t2 = time.perf_counter()
+        self.program, self.graph = prog, g
+        self.assignment, self.plan, self.meg = f, plan, meg
+        self.schedule, self.schedule_single = ts, ts_single
+        self.plan_seconds = {"trace": t1 - t0, "assign+pre_run": t2 - t1}
+
+        dev = torch.device("cuda", self.device)
+        # activation arena: offsets straight from the reference arena layout
+        self.arena = torch.empty(max(ts.arena.total, 256), dtype=torch.uint8, device=dev)
+        abase = self.arena.data_ptr()
+        offset_of = {}
+        owned = {}
+        for st in prog.storages:
+            if st.owner >= 0:
+                owned.setdefault(st.owner, []).append(st)
+        for tid, sts in owned.items():
+            offs = ts.task_args[tid]
+            for st, off in zip(sts, offs):
+                offset_of[st.sid] = off
+        inp = prog.input_view.st
+        self.d_in = torch.empty(inp.n * inp.c * inp.h * inp.w, dtype=torch.float32, device=dev)
+        base_map = {}
+        for st in prog.storages:
+            if st.role == "input":
+                base_map[st.sid] = self.d_in.data_ptr()
+            else:
+                base_map[st.sid] = abase + offset_of[st.sid]
+        self.base_map = base_map
+
+        # packed parameters (one device allocation, 256-B aligned slices)
+        arrays = _pack_weights(prog)
+        woff = {}
+        total = 0
+        for key, a in arrays.items():
+            woff[key] = total
+            total += (a.nbytes + 255) // 256 * 256
+        host = np.zeros(max(total, 256) // 4, dtype=np.float32)
+        for key, a in arrays.items():
+            host[woff[key] // 4: woff[key] // 4 + a.size] = a
+        self.weights = torch.from_numpy(host).to(dev)
+        self.weight_bytes = total
+        self.ops = lower_program(prog, lambda st: base_map[st.sid], self.weights.data_ptr(), woff)
+
+        out = prog.output_view
+        self.out_shape = tuple(self.model_output_shape(prog))
+        self.h_in = torch.empty(ex.shape, dtype=torch.float32).pin_memory()
+        self.h_out = torch.empty(self.out_shape, dtype=torch.float32).pin_memory()
+        self.d_out_ptr = base_map[out.st.sid] + 4 * out.elem_offset()
+        self.out_bytes = self.h_out.numel() * 4
+
+        h = C.c_void_p()
+        N.check(lib.sw_engine_create(self.device, C.byref(h)))
+        self._h = h
+        N.check(lib.sw_engine_set_ops(h, len(prog.tasks), self.ops))
+        N.check(lib.sw_engine_set_io(h, self.h_in.data_ptr(), self.d_in.data_ptr(),
+                                     self.h_in.numel() * 4, self.h_out.data_ptr(),
+                                     self.d_out_ptr, self.out_bytes))
+        t3 = time.perf_counter()
+        self._capture(SLOT_MULTI_IO, ts, True)
+        self._capture(SLOT_SINGLE_IO, ts_single, True)
+        self._capture(SLOT_MULTI, ts, False)
+        self._capture(SLOT_SINGLE, ts_single, False)
+        self.plan_seconds["lower+capture"] = time.perf_counter() - t3
+        self.eager_order = np.asarray([op.arg for s in ts_single.streams for op in s],
+                                      dtype=np.int64)
+        self.prepared = True
+        return self
+
+    @staticmethod
+    def model_output_shape(prog: Program):
+        o = prog.output_view.st
+        return (o.n, o.c, o.h, o.w) if (o.h * o.w > 1) else (o.n, o.c)
+
+    def _capture(self, slot: int, ts: TaskSchedule, with_io: bool):
+        lens, kinds, args, order = schedule_arrays(ts)
+        N.check(N.lib().sw_engine_capture(self._h, slot, len(ts.streams), N.ptr64(lens),
+                                          N.ptr32(kinds), N.ptr64(args), len(ts.order),
+                                          N.ptr64(order), 1 if with_io else 0))
+
+    # -- execution --------------------------------------------------------
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        """End-to-end inference of one batch from host memory (public API)."""
+        if not self.prepared:
+            self.prepare(x)
+        self.h_in.copy_(x.detach().reshape(self.h_in.shape))
+        slot = SLOT_MULTI_IO if self.multi_stream else SLOT_SINGLE_IO
+        N.check(N.lib().sw_engine_replay_sync(self._h, slot, None))
+        return self.h_out.clone()
+
+    def load_input_device(self, x: torch.Tensor):
+        """Place a batch in the device input buffer (for device-resident replay)."""
+        self.d_in.copy_(x.detach().reshape(-1).to(self.d_in.device, torch.float32))
+
+    def replay(self, multi: bool = True, io: bool = False):
+        slot = (SLOT_MULTI_IO if multi else SLOT_SINGLE_IO) if io else \
+            (SLOT_MULTI if multi else SLOT_SINGLE)
+        N.check(N.lib().sw_engine_replay(self._h, slot))
+
+    def synchronize(self):
+        N.check(N.lib().sw_engine_synchronize(self._h))
+
+    def device_output(self) -> torch.Tensor:
+        o = self.program.output_view
+        st = o.st
+        n = st.n * st.c * st.h * st.w
+        base = self.base_map[st.sid] - self.arena.data_ptr()
+        flat = self.arena[base: base + 4 * n].view(torch.float32)
+        return flat.reshape(self.out_shape)
+
+    def run_eager(self, python_loop: bool = True):
+        """Non-AoT single-stream execution: one launch call per task."""
+        lib = N.lib()
+        if python_loop:
+            for t in self.eager_order:
+                N.check(lib.sw_engine_launch_op(self._h, int(t)))
+        else:
+            N.check(lib.sw_engine_run_eager(self._h, len(self.eager_order),
+                                            N.ptr64(self.eager_order)))
+
+    def time_replay(self, multi: bool = True, iters: int = 200, io: bool = False):
+        slot = (SLOT_MULTI_IO if multi else SLOT_SINGLE_IO) if io else \
+            (SLOT_MULTI if multi else SLOT_SINGLE)
+        gpu = C.c_double()
+        host = C.c_double()
+        N.check(N.lib().sw_engine_time_replay(self._h, slot, iters, C.byref(gpu), C.byref(host)))
+        return gpu.value, host.value
+
+    def profile_tasks(self, reps: int = 20) -> np.ndarray:
+        out = np.zeros(len(self.eager_order), dtype=np.float64)
+        N.check(N.lib().sw_engine_profile_ops(self._h, len(self.eager_order),
+                                              N.ptr64(self.eager_order), reps,
+                                              out.ctypes.data_as(C.POINTER(C.c_double))))
+        res = np.zeros_like(out)
+        res[self.eager_order] = out
+        return res
+
+    def graph_topology(self, slot: int = SLOT_MULTI):
+        cap = 4 * (len(self.program.tasks) + len(self.plan) + 16) + 4 * len(self.graph.edges)
+        nn_ = np.zeros(1, dtype=np.int64)
+        kinds = np.zeros(cap, dtype=np.int32)
+        task = np.zeros(cap, dtype=np.int64)
+        ne = np.zeros(1, dtype=np.int64)
+        edges = np.zeros(2 * cap, dtype=np.int64)
+        N.check(N.lib().sw_engine_graph_topology(self._h, slot, cap, N.ptr64(nn_), N.ptr32(kinds),
+                                                 N.ptr64(task), N.ptr64(ne), N.ptr64(edges)))
+        n = int(nn_[0])
+        e = int(ne[0])
+        return kinds[:n], task[:n], edges[:2 * e].reshape(-1, 2)
+
+    def roofline_sum_us(self, hbm_gbs: float, tflops: float) -> float:
+        return sum(roofline_us(t, hbm_gbs, tflops) for t in self.program.tasks)
+
+    def close(self):
+        if self._h is not None:
+            N.lib().sw_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

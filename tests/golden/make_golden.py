@@ -180,5 +180,48 @@ def main():
     print(f"wrote {len(cases)} cases to {out} ({os.path.getsize(out)} bytes)")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--networks" not in sys.argv:
     main()
+
+
+def network_cases():
+    """The op DAGs our builder emits for the BASELINE networks, planned by the
+    reference ("parity of streams is defined on the DAG the
+    builder emits: feed that same DAG to the reference")."""
+    sw, _ = _import_reference()
+    root = os.path.dirname(os.path.dirname(HERE))
+    sys.path.insert(0, root)
+    from paper_2012_02732_b200.networks import build_model, example_input
+    from paper_2012_02732_b200.trace import build_program
+    cases = []
+    for name in ("cell", "resnet50", "inception_v3", "nasnet_mobile", "mobilenet_v2",
+                 "efficientnet_b0"):
+        model, shape = build_model(name)
+        x = example_input(shape)
+        for fuse in (True, False):
+            prog = build_program(model, x, fuse=fuse)
+            text = graph_text(prog.graph)
+            g = sw.graph_from_json(text)
+            case = reference_case(sw, g, f"{name}:{'fused' if fuse else 'raw'}")
+            cases.append(case)
+    return cases
+
+
+def graph_text(g):
+    """graph_to_json of our CompGraph (same canonical format as the reference)."""
+    from paper_2012_02732_b200.graph import graph_to_json
+    return graph_to_json(g)
+
+
+def main_networks():
+    cases = network_cases()
+    out = os.path.join(HERE, "network_dags.json")
+    with open(out, "w") as fh:
+        json.dump({"generator": "tests/golden/make_golden.py --networks",
+                   "reference": "/root/reference/pkg/src/streamweave (v0.1.0)",
+                   "cases": cases}, fh, separators=(",", ":"))
+    print(f"wrote {len(cases)} cases to {out} ({os.path.getsize(out)} bytes)")
+
+
+if __name__ == "__main__" and "--networks" in sys.argv:
+    main_networks()

