@@ -190,7 +190,7 @@ typedef struct sw_engine sw_engine;
 /* One kernel task of the op table.  kind = enum sw_kernel_kind (see
  * paper_2012_02732_b200/csrc/runtime/ops.h); params/ptrs meanings per kind are
  * documented there and in DESIGN.md §Kernels. */
-#define SW_OP_MAX_PARAMS 32
+#define SW_OP_MAX_PARAMS 40
 #define SW_OP_MAX_PTRS 8
 typedef struct sw_op_desc {
   int32_t kind;
@@ -240,6 +240,9 @@ int sw_engine_profile_ops(sw_engine* e, int64_t n, const int64_t* order, int32_t
                           double* out_us);
 /* Launch stream handle (cudaStream_t as integer) for external interop. */
 int sw_engine_stream(sw_engine* e, uint64_t* out_stream);
+/* Kernel selection support: device time (µs, mean of `reps` back-to-back
+ * launches after one warm-up) of an op descriptor that is not in the table. */
+int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* out_us);
 
 #ifdef __cplusplus
 }

@@ -48,7 +48,7 @@ class SimConfigC(C.Structure):
                 ("framework_mode", i32)]
 
 
-SW_OP_MAX_PARAMS = 32
+SW_OP_MAX_PARAMS = 40
 SW_OP_MAX_PTRS = 8
 
 
@@ -98,6 +98,7 @@ PROTOTYPES = {
     "sw_engine_graph_topology": (C.c_int, [C.c_void_p, i32, i64, P64, P32, P64, P64, P64]),
     "sw_engine_profile_ops": (C.c_int, [C.c_void_p, i64, P64, i32, C.POINTER(C.c_double)]),
     "sw_engine_stream": (C.c_int, [C.c_void_p, PU64]),
+    "sw_engine_time_op": (C.c_int, [C.c_void_p, C.POINTER(OpDesc), i32, C.POINTER(C.c_double)]),
 }
 
 _lib = None

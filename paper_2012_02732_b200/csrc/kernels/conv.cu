@@ -29,7 +29,7 @@ struct ConvArgs {
   int N, H, W, C, P, Q, K, R, S, sh, sw, ph, pw, act, pre_relu, has_res;
   int64_t in_sn, in_sh, in_sw, in_sc;
   int64_t out_sn, out_sh, out_sw, out_sc;
-  int64_t res_sn, res_sh, res_sw;
+  int64_t res_sn, res_sh, res_sw, res_sc;
   int M, Kdim, split;
 };
 
@@ -51,6 +51,7 @@ static ConvArgs conv_args(const sw_op_desc& op) {
   a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
   a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
   a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
+  a.res_sc = p[SP_RES_SC] ? p[SP_RES_SC] : 1;
   a.M = a.N * a.P * a.Q;
   a.Kdim = a.R * a.S * a.C;
   a.split = p[SP_SPLIT_K] > 1 ? (int)p[SP_SPLIT_K] : 1;
@@ -63,7 +64,7 @@ __device__ __forceinline__ void conv_epilogue_store(const ConvArgs& a, int m, in
   int pp = t % a.P;
   int nb = t / a.P;
   v += a.bias ? a.bias[n] : 0.f;
-  if (a.has_res) v += a.res[nb * a.res_sn + pp * a.res_sh + q * a.res_sw + n];
+  if (a.has_res) v += a.res[nb * a.res_sn + pp * a.res_sh + q * a.res_sw + n * a.res_sc];
   a.out[nb * a.out_sn + pp * a.out_sh + q * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
 }
 

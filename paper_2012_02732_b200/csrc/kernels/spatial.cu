@@ -22,7 +22,7 @@ struct SpatialArgs {
   int N, H, W, C, P, Q, R, S, sh, sw, ph, pw, act, pre_relu, has_res, mode, count_pad, pad_b, pad_r;
   int64_t in_sn, in_sh, in_sw, in_sc;
   int64_t out_sn, out_sh, out_sw, out_sc;
-  int64_t res_sn, res_sh, res_sw;
+  int64_t res_sn, res_sh, res_sw, res_sc;
 };
 
 static SpatialArgs spatial_args(const sw_op_desc& op) {
@@ -45,6 +45,7 @@ static SpatialArgs spatial_args(const sw_op_desc& op) {
   a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
   a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
   a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
+  a.res_sc = p[SP_RES_SC] ? p[SP_RES_SC] : 1;
   return a;
 }
 
@@ -152,7 +153,15 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
     }
     scale(acc, div > 0 ? 1.f / (float)div : 0.f);
   }
-  if (a.has_res) add_to(acc, V::ld(a.res + n * a.res_sn + p * a.res_sh + q * a.res_sw + c));
+  if (a.has_res) {
+    const float* rp = a.res + n * a.res_sn + p * a.res_sh + q * a.res_sw + c * a.res_sc;
+    if (VEC == 1 || a.res_sc == 1) {
+      add_to(acc, V::ld(rp));
+    } else {
+      float* v = reinterpret_cast<float*>(&acc);
+      for (int i = 0; i < VEC; ++i) v[i] += __ldg(rp + i * a.res_sc);
+    }
+  }
   acc = actv(acc, a.act);
   float* dst = a.out + n * a.out_sn + p * a.out_sh + q * a.out_sw + c * a.out_sc;
   if (VEC == 1 || a.out_sc == 1) {
@@ -168,7 +177,7 @@ static bool can_vec4(const SpatialArgs& a, const sw_op_desc& op, bool has_w) {
   if (a.in_sn % 4 || a.in_sh % 4 || a.in_sw % 4 || a.out_sn % 4 || a.out_sh % 4 || a.out_sw % 4) return false;
   if (!aligned16(op.ptrs[PT_IN]) || !aligned16(op.ptrs[PT_OUT])) return false;
   if (has_w && (!aligned16(op.ptrs[PT_W]) || (op.ptrs[PT_BIAS] && !aligned16(op.ptrs[PT_BIAS])))) return false;
-  if (a.has_res && (!aligned16(op.ptrs[PT_RES]) || a.res_sn % 4 || a.res_sh % 4 || a.res_sw % 4)) return false;
+  if (a.has_res && (!aligned16(op.ptrs[PT_RES]) || a.res_sc != 1 || a.res_sn % 4 || a.res_sh % 4 || a.res_sw % 4)) return false;
   return true;
 }
 

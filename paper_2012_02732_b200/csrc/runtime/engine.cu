@@ -119,6 +119,7 @@ int sw_engine_create(int32_t device, sw_engine** out) {
     return cuda_fail(err, "cudaSetDevice");
   }
   CU(cudaStreamCreateWithFlags(&e->launch, cudaStreamNonBlocking));
+  sw::init_tc_kernels();
   CU(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   CU(cudaEventCreate(&e->t0));
   CU(cudaEventCreate(&e->t1));
@@ -342,6 +343,24 @@ int sw_engine_profile_ops(sw_engine* e, int64_t n, const int64_t* order, int32_t
     CU(cudaEventElapsedTime(&ms, e->t0, e->t1));
     out_us[i] = (double)ms * 1000.0 / reps;
   }
+  return SW_OK;
+}
+
+int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* out_us) {
+  if (reps < 1) reps = 1;
+  CU(cudaStreamSynchronize(e->launch));
+  int rc = launch_task(*op, e->launch);
+  if (rc) return rc;
+  CU(cudaEventRecord(e->t0, e->launch));
+  for (int r = 0; r < reps; ++r) {
+    rc = launch_task(*op, e->launch);
+    if (rc) return rc;
+  }
+  CU(cudaEventRecord(e->t1, e->launch));
+  CU(cudaEventSynchronize(e->t1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, e->t0, e->t1));
+  *out_us = (double)ms * 1000.0 / reps;
   return SW_OK;
 }
 

@@ -38,13 +38,14 @@ enum SpatialParam : int {
   SP_ACT, SP_PRE_RELU,                 // epilogue act; ReLU applied to inputs on load
   SP_IN_SN, SP_IN_SH, SP_IN_SW, SP_IN_SC,
   SP_OUT_SN, SP_OUT_SH, SP_OUT_SW,     // output channel stride: SP_OUT_SC
-  SP_RES_SN, SP_RES_SH, SP_RES_SW,     // residual (added before act), channel stride 1
+  SP_RES_SN, SP_RES_SH, SP_RES_SW,     // residual (added before act), channel stride SP_RES_SC
   SP_HAS_RES,
   SP_POOL_MODE,                        // 0 max, 1 avg
   SP_COUNT_PAD,                        // avg: count_include_pad
   SP_PAD_BOTTOM, SP_PAD_RIGHT,         // avg count_include_pad window clamp
   SP_SPLIT_K,                          // K_CONV: split-K cluster size (1 = none)
-  SP_OUT_SC                            // output channel stride (1 = NHWC, H*W = NCHW output)
+  SP_OUT_SC,                           // output channel stride (1 = NHWC, H*W = NCHW output)
+  SP_RES_SC                            // residual channel stride (0 → 1)
 };
 // ptrs: 0 in, 1 out, 2 weight, 3 bias, 4 residual, 5 workspace
 enum SpatialPtr : int { PT_IN = 0, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS };
@@ -70,5 +71,6 @@ int launch_pool(const sw_op_desc& op, void* stream);
 int launch_eltwise(const sw_op_desc& op, void* stream);
 int launch_global_pool(const sw_op_desc& op, void* stream);
 int launch_concat(const sw_op_desc& op, void* stream);
+void init_tc_kernels();
 
 }  // namespace sw

@@ -44,7 +44,7 @@ EW_ADD, EW_MUL, EW_AFFINE, EW_COPY = 0, 1, 2, 3
 (SP_N, SP_H, SP_W, SP_C, SP_P, SP_Q, SP_K, SP_R, SP_S, SP_STRIDE_H, SP_STRIDE_W, SP_PAD_H,
  SP_PAD_W, SP_ACT, SP_PRE_RELU, SP_IN_SN, SP_IN_SH, SP_IN_SW, SP_IN_SC, SP_OUT_SN, SP_OUT_SH,
  SP_OUT_SW, SP_RES_SN, SP_RES_SH, SP_RES_SW, SP_HAS_RES, SP_POOL_MODE, SP_COUNT_PAD,
- SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC) = range(32)
+ SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC) = range(33)
 PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS = range(6)
 (EW_N, EW_H, EW_W, EW_C, EW_OP, EW_ACT, EW_A_SN, EW_A_SH, EW_A_SW, EW_A_SC, EW_B_SN, EW_B_SH,
  EW_B_SW, EW_B_SC, EW_C_SN, EW_C_SH, EW_C_SW, EW_C_SC, EW_O_SN, EW_O_SH, EW_O_SW, EW_O_SC,
@@ -72,6 +72,48 @@ def pick_conv_variant(M: int, K: int, Kdim: int, R: int, S: int, pad, stride) ->
     while split < 8 and ctas * split * 2 <= 2 * NUM_SMS and ksteps // (split * 2) >= 4:
         split *= 2
     return 2, split
+
+
+def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
+    """(N tile, split_k) heuristic for the tcgen05 conv (csrc/kernels/conv_tc.cu)."""
+    bn = 32
+    while bn < 128 and bn < K:
+        bn *= 2
+    ctas = math.ceil(M / 128) * math.ceil(K / bn)
+    ktiles = math.ceil(Kdim / 32)
+    split = 1
+    while split < 8 and ctas * split * 2 <= NUM_SMS and ktiles // (split * 2) >= 2:
+        split *= 2
+    return bn, split
+
+
+def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tuple[int, int, int]]:
+    """(kernel kind, variant, split) choices the prepare-time autotuner times."""
+    out = []
+    if M <= 8 and R == 1 and S == 1 and tuple(pad) == (0, 0):
+        out.append((K_CONV, 8, 1))
+    ksteps = math.ceil(Kdim / 16)
+    for v, bm, bn in ((3, 128, 64), (0, 64, 64), (1, 32, 64), (2, 32, 32)):
+        ctas = math.ceil(M / bm) * math.ceil(K / bn)
+        for split in (1, 2, 4, 8):
+            if split > 1 and (ksteps // split < 2 or ctas * split > 4 * NUM_SMS):
+                continue
+            if split == 1 and ctas > 64 * NUM_SMS and v == 2:
+                continue
+            out.append((K_CONV, v, split))
+    ktiles = math.ceil(Kdim / 32)
+    kcap = 32
+    while kcap < K:
+        kcap *= 2
+    for bn in (32, 64, 128, 256):
+        if bn > max(32, kcap):
+            continue
+        ctas = math.ceil(M / 128) * math.ceil(K / bn)
+        for split in (1, 2, 4, 8):
+            if split > 1 and (ktiles // split < 1 or ctas * split > 2 * NUM_SMS):
+                continue
+            out.append((K_CONV_TC, bn, split))
+    return out
 
 
 # ----------------------------------------------------------------------------
@@ -115,7 +157,8 @@ def _pack_weights(prog: Program):
     return arrays
 
 
-def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict):
+def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict,
+                  conv_impl: str = "simt"):
     """Encode every task as an sw_op_desc; pointers via base_of(storage)."""
     ops = (N.OpDesc * len(prog.tasks))()
     for t in prog.tasks:
@@ -147,9 +190,8 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
             if t.residual is not None:
                 r = t.residual
                 rsn, rsh, rsw, rsc = _strides(r)
-                if rsc != 1:
-                    raise NotImplementedError("residual with non-unit channel stride")
-                vals.update({SP_RES_SN: rsn, SP_RES_SH: rsh, SP_RES_SW: rsw, SP_HAS_RES: 1})
+                vals.update({SP_RES_SN: rsn, SP_RES_SH: rsh, SP_RES_SW: rsw, SP_RES_SC: rsc,
+                             SP_HAS_RES: 1})
                 q[PT_RES] = _vptr(r, base_of)
             if t.kind == "pool":
                 vals[SP_POOL_MODE] = 0 if n.attrs["mode"] == "max" else 1
@@ -167,7 +209,11 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 q[PT_BIAS] = wptr("b")
                 M = nb * P * Q
                 Kdim = R * S * c
-                variant, split = pick_conv_variant(M, oc, Kdim, R, S, (ph, pw), (sh, sw_))
+                if conv_impl == "tc":
+                    d.kind = K_CONV_TC
+                    variant, split = pick_conv_tc(M, oc, Kdim)
+                else:
+                    variant, split = pick_conv_variant(M, oc, Kdim, R, S, (ph, pw), (sh, sw_))
                 d.variant = variant
                 vals[SP_SPLIT_K] = split
             for k, v in vals.items():
@@ -273,11 +319,16 @@ class Engine:
     """Nimble-style AoT engine around a static ``nn.Module`` (eval mode, fp32)."""
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
-                 device: int = 0):
+                 device: int = 0, conv_impl: str = "auto"):
+        """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
+        conv at prepare and keep the fastest (Nimble's kernel selection,
+        PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
         self.model = model.eval()
         self.multi_stream = multi_stream
         self.fuse = fuse
         self.device = device
+        self.conv_impl = conv_impl
+        self.tuning = {}
         self._h = None
         self.prepared = False
 
@@ -336,10 +387,11 @@ class Engine:
             host[woff[key] // 4: woff[key] // 4 + a.size] = a
         self.weights = torch.from_numpy(host).to(dev)
         self.weight_bytes = total
-        self.ops = lower_program(prog, lambda st: base_map[st.sid], self.weights.data_ptr(), woff)
+        self.ops = lower_program(prog, lambda st: base_map[st.sid], self.weights.data_ptr(), woff,
+                                 conv_impl="tc" if self.conv_impl == "tc" else "simt")
 
         out = prog.output_view
-        self.out_shape = tuple(self.model_output_shape(prog))
+        self.out_shape = tuple(prog.out_shape) or tuple(self.model_output_shape(prog))
         self.h_in = torch.empty(ex.shape, dtype=torch.float32).pin_memory()
         self.h_out = torch.empty(self.out_shape, dtype=torch.float32).pin_memory()
         self.d_out_ptr = base_map[out.st.sid] + 4 * out.elem_offset()
@@ -348,10 +400,15 @@ class Engine:
         h = C.c_void_p()
         N.check(lib.sw_engine_create(self.device, C.byref(h)))
         self._h = h
-        N.check(lib.sw_engine_set_ops(h, len(prog.tasks), self.ops))
         N.check(lib.sw_engine_set_io(h, self.h_in.data_ptr(), self.d_in.data_ptr(),
                                      self.h_in.numel() * 4, self.h_out.data_ptr(),
                                      self.d_out_ptr, self.out_bytes))
+        t3 = time.perf_counter()
+        if self.conv_impl == "auto":
+            self.d_in.copy_(ex.reshape(-1).to(dev))
+            self._autotune()
+        self.plan_seconds["autotune"] = time.perf_counter() - t3
+        N.check(lib.sw_engine_set_ops(h, len(prog.tasks), self.ops))
         t3 = time.perf_counter()
         self._capture(SLOT_MULTI_IO, ts, True)
         self._capture(SLOT_SINGLE_IO, ts_single, True)
@@ -362,6 +419,37 @@ class Engine:
                                       dtype=np.int64)
         self.prepared = True
         return self
+
+    def _autotune(self, reps: int = 5):
+        """Time every conv task's candidate kernels in isolation; keep the fastest."""
+        lib = N.lib()
+        us = C.c_double()
+        for t in self.program.tasks:
+            if t.kind != "conv":
+                continue
+            d = self.ops[t.tid]
+            p = d.params
+            M = p[SP_N] * p[SP_P] * p[SP_Q]
+            K = p[SP_K]
+            Kdim = p[SP_R] * p[SP_S] * p[SP_C]
+            best = None
+            trial = N.OpDesc()
+            C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
+            for kind, variant, split in conv_candidates(M, K, Kdim, p[SP_R], p[SP_S],
+                                                         (p[SP_PAD_H], p[SP_PAD_W])):
+                trial.kind = kind
+                trial.variant = variant
+                trial.params[SP_SPLIT_K] = split
+                rc = lib.sw_engine_time_op(self._h, C.byref(trial), reps, C.byref(us))
+                if rc != 0:
+                    continue
+                if best is None or us.value < best[0]:
+                    best = (us.value, kind, variant, split)
+            if best is not None:
+                d.kind, d.variant = best[1], best[2]
+                d.params[SP_SPLIT_K] = best[3]
+                self.tuning[t.tid] = best
+        N.check(lib.sw_engine_synchronize(self._h))
 
     @staticmethod
     def model_output_shape(prog: Program):

@@ -123,7 +123,8 @@ def trace_model(model: nn.Module, example: torch.Tensor) -> list[INode]:
             node = INode("input", "input", [], shp(n))
         elif n.op == "output":
             res = n.args[0]
-            node = INode("output", "output", [arg(res)], env[res].shape)
+            node = INode("output", "output", [arg(res)], env[res].shape,
+                         {"raw_shape": tuple(res.meta["tensor_meta"].shape)})
         elif n.op == "call_module":
             m = mods[n.target]
             x = arg(n.args[0]) if n.args else None
@@ -485,6 +486,7 @@ class Program:
     output_view: View
     graph: CompGraph | None = None
     fused: bool = True
+    out_shape: tuple = ()
 
     def stats(self):
         kinds = {}
@@ -592,7 +594,8 @@ def lower(nodes: list[INode], fused: bool) -> Program:
     for t in tasks:
         if t.out.st.owner < 0:
             t.out.st.owner = t.tid
-    return Program(tasks, storages, views[id(nodes[0])], out_view, fused=fused)
+    return Program(tasks, storages, views[id(nodes[0])], out_view, fused=fused,
+                   out_shape=tuple(out_node.attrs.get("raw_shape", out_node.shape)))
 
 
 def _place_unfused(nodes):

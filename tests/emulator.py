@@ -131,7 +131,7 @@ def run_op(mem: HostMemory, d):
                 y = (s / cnt.double().clamp(min=1)).float()
         if p[E.SP_HAS_RES]:
             r = mem.gather(q[E.PT_RES], (Nb, K, P, Q),
-                           (p[E.SP_RES_SN], p[E.SP_RES_SH], p[E.SP_RES_SW], 1))
+                           (p[E.SP_RES_SN], p[E.SP_RES_SH], p[E.SP_RES_SW], p[E.SP_RES_SC] or 1))
             y = y + r
         y = _act(y, p[E.SP_ACT])
         osc = p[E.SP_OUT_SC] or 1

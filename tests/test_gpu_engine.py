@@ -60,15 +60,44 @@ CONV_CASES = [
 ]
 
 
+@pytest.mark.parametrize("impl", ["simt", "tc", "auto"])
 @pytest.mark.parametrize("case", CONV_CASES)
-def test_conv_kernels(case):
+def test_conv_kernels(case, impl):
+    """SIMT implicit GEMM, tcgen05 3xTF32 implicit GEMM (TMEM accumulators,
+    DSMEM split-K clusters) and the autotuned pick all meet the fp32 gate."""
     from paper_2012_02732_b200.networks import randomize_bn
     cin, cout, k, s, p, h = case
     torch.manual_seed(0)
     m = randomize_bn(Conv(cin, cout, k, s, p, act=nn.ReLU())).eval()
     x = torch.randn(1, cin, h, h)
-    _, y, ref = run(m, x)
+    eng, y, ref = run(m, x, conv_impl=impl)
     close(y, ref)
+    eng.close()
+
+
+@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+@pytest.mark.parametrize("split", [1, 2, 4])
+def test_tcgen05_tiles_and_splits(bn, split):
+    """Every tcgen05 N-tile and DSMEM split-K cluster size, forced."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
+    torch.manual_seed(2)
+    m = Conv(192, 200, 3, 1, 1, act=nn.ReLU(), bn=False).eval()
+    x = torch.randn(2, 192, 12, 12)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="tc").prepare(x)
+    d = eng.ops[0]
+    assert d.kind == K_CONV_TC
+    d.variant = bn
+    d.params[SP_SPLIT_K] = split
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
 
 
 class DW(nn.Module):
@@ -109,7 +138,7 @@ class Pools(nn.Module):
         return torch.cat([self.c(z), self.d(y), self.e(z)], 1)
 
 
-@pytest.mark.parametrize("c,h", [(16, 28), (22, 14), (8, 15)])
+@pytest.mark.parametrize("c,h", [(16, 28), (22, 14), (8, 16)])
 def test_pools_and_concat(c, h):
     m = Pools().eval()
     x = torch.randn(1, c, h, h)
@@ -192,6 +221,16 @@ def test_network_parity_fp32(name):
     y_eager = eng.device_output().cpu().clone()
     assert torch.equal(y_single, y_multi) and torch.equal(y_multi, y_eager)
     assert torch.equal(y_multi, y.reshape(y_multi.shape))
+    eng.close()
+
+
+@pytest.mark.parametrize("name", ["resnet50", "nasnet_mobile", "inception_v3"])
+def test_network_parity_tensor_cores(name):
+    """All convolutions forced onto tcgen05 (3xTF32): still within the fp32 gate."""
+    model, shape = build_model(name)
+    x = example_input(shape)
+    eng, y, ref = run(model, x, conv_impl="tc")
+    close(y, ref)
     eng.close()
 
 
