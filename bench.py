@@ -242,6 +242,13 @@ def run_ours(args, world, rank, local):
     # same engine, other modes (same flush discipline)
     single = timed_replays(False, args.steps)
     single_ms = sum(single) / len(single)
+    # the same multi-stream graph captured without programmatic dependent launch
+    eng.recapture(pdl=not eng.pdl)
+    for _ in range(3):
+        eng.replay(multi=True)
+    alt = timed_replays(True, args.steps)
+    alt_ms = sum(alt) / len(alt)
+    eng.recapture(pdl=not eng.pdl)
 
     def eager_once():
         with torch.cuda.stream(stream):
@@ -321,6 +328,8 @@ def run_ours(args, world, rank, local):
                 "multi_stream_aot_us": round(ms * 1e3, 2),
                 "single_stream_aot_us": round(single_ms * 1e3, 2),
                 "eager_non_aot_us": round(eager_ms * 1e3, 2),
+                ("multi_stream_aot_no_pdl_us" if eng.pdl else "multi_stream_aot_pdl_us"):
+                    round(alt_ms * 1e3, 2),
                 "multi_over_single": round(single_ms / ms, 4),
                 "aot_over_eager": round(eager_ms / ms, 4),
             },

@@ -243,6 +243,10 @@ int sw_engine_stream(sw_engine* e, uint64_t* out_stream);
 /* Kernel selection support: device time (µs, mean of `reps` back-to-back
  * launches after one warm-up) of an op descriptor that is not in the table. */
 int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* out_us);
+/* Engine flags for subsequent captures / eager launches:
+ * SW_ENGINE_PDL = programmatic dependent launch on same-stream kernel edges. */
+#define SW_ENGINE_PDL 1u
+int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
 #ifdef __cplusplus
 }

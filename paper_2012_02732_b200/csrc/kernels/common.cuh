@@ -28,4 +28,44 @@ __host__ __device__ __forceinline__ int64_t cdiv(int64_t a, int64_t b) { return 
 
 __host__ __forceinline__ bool aligned16(uint64_t p) { return (p & 15ull) == 0; }
 
+// Programmatic dependent launch (PDL).  Every kernel lets its dependents be
+// scheduled as soon as it starts (launch_dependents) and waits for its
+// prerequisite grids before touching activations (wait); both are no-ops
+// when the launch carried no programmatic edge.  Constant weights may be
+// fetched before pdl_wait().
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Engine-controlled launch flags (set around capture / eager launches).
+extern thread_local bool g_launch_pdl;
+
+// Single launch path for every kernel: optional cluster (split-K along z)
+// and the PDL attribute.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            unsigned cluster_z, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (cluster_z > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 1;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = cluster_z;
+    ++n;
+  }
+  if (g_launch_pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, fn, static_cast<Args&&>(args)...);
+}
+
 }  // namespace sw

@@ -68,22 +68,35 @@ __device__ __forceinline__ void conv_epilogue_store(const ConvArgs& a, int m, in
   a.out[nb * a.out_sn + pp * a.out_sh + q * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
 }
 
-// BM x BN output tile, 4x4 micro-tile per thread, BK = 16, register-staged
-// double buffering of the smem tiles.
-template <int BM, int BN>
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// BM x BN output tile, 4x4 micro-tile per thread, BK = 16, STAGES-deep
+// cp.async (LDGSTS) pipeline: the im2col gather of STAGES-1 future K tiles is
+// in flight while the current tile is multiplied, so a layer costs about one
+// memory round trip instead of one per K tile (batch-1 layers are latency-,
+// not FLOP-bound).  Out-of-range taps are zero-filled by cp.async itself.
+template <int BM, int BN, bool PRE>
 __global__ void __launch_bounds__((BM / 4) * (BN / 4))
 conv_simt_kernel(ConvArgs a) {
   constexpr int BK = 16;
+  constexpr int STAGES = 4;
   constexpr int NT = (BM / 4) * (BN / 4);
   constexpr int A_PER = BM * BK / NT;
   constexpr int B_PER = BN * BK / NT;
   constexpr int PAD = 4;
   static_assert(NT % BK == 0, "kk must be fixed per thread");
-  constexpr int TILE_FLOATS = 2 * BK * (BM + PAD) + 2 * BK * (BN + PAD);
+  constexpr int TILE_FLOATS = STAGES * BK * (BM + PAD) + STAGES * BK * (BN + PAD);
   constexpr int SMEM_FLOATS = TILE_FLOATS > BM * BN ? TILE_FLOATS : BM * BN;
-  __shared__ __align__(16) float smem[SMEM_FLOATS];
-  float* As = smem;                           // [2][BK][BM+PAD]
-  float* Bs = smem + 2 * BK * (BM + PAD);     // [2][BK][BN+PAD]
+  extern __shared__ __align__(16) float smem[];
+  float* As = smem;                                // [STAGES][BK][BM+PAD]
+  float* Bs = smem + STAGES * BK * (BM + PAD);     // [STAGES][BK][BN+PAD]
+  (void)SMEM_FLOATS;
 
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * BM;
@@ -114,9 +127,8 @@ conv_simt_kernel(ConvArgs a) {
     a_ih[i] = p * a.sh - a.ph;
     a_iw[i] = q * a.sw - a.pw;
   }
-  float ra[A_PER], rb[B_PER];
-
-  auto load_tiles = [&](int kstep) {
+  // issue the cp.async gather of K tile `kstep` into pipeline buffer `buf`
+  auto issue = [&](int kstep, int buf) {
     int k = kstep * BK + kk;
     bool kin = k < a.Kdim;
     int c = 0, r = 0, s = 0;
@@ -126,28 +138,21 @@ conv_simt_kernel(ConvArgs a) {
       s = rs % a.S;
       r = rs / a.S;
     }
+    float* as = As + (buf * BK + kk) * (BM + PAD);
+    float* bs = Bs + (buf * BK + kk) * (BN + PAD);
 #pragma unroll
     for (int i = 0; i < A_PER; ++i) {
-      float v = 0.f;
       int ih = a_ih[i] + r, iw = a_iw[i] + s;
-      if (kin && a_ok[i] && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W) {
-        v = __ldg(a.in + a_base[i] + ih * a.in_sh + iw * a.in_sw + c * a.in_sc);
-        if (a.pre_relu) v = fmaxf(v, 0.f);
-      }
-      ra[i] = v;
+      bool ok = kin && a_ok[i] && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+      const float* src = ok ? a.in + a_base[i] + ih * a.in_sh + iw * a.in_sw + c * a.in_sc : a.in;
+      cp_async4(as + (tid + i * NT) / BK, src, ok);
     }
 #pragma unroll
     for (int i = 0; i < B_PER; ++i) {
-      int nn = (tid + i * NT) / BK;
-      int n = n0 + nn;
-      rb[i] = (kin && n < a.K) ? __ldg(a.w + (int64_t)n * a.Kdim + k) : 0.f;
+      int n = n0 + (tid + i * NT) / BK;
+      bool ok = kin && n < a.K;
+      cp_async4(bs + (tid + i * NT) / BK, ok ? a.w + (int64_t)n * a.Kdim + k : a.w, ok);
     }
-  };
-  auto store_tiles = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < A_PER; ++i) As[(buf * BK + kk) * (BM + PAD) + (tid + i * NT) / BK] = ra[i];
-#pragma unroll
-    for (int i = 0; i < B_PER; ++i) Bs[(buf * BK + kk) * (BN + PAD) + (tid + i * NT) / BK] = rb[i];
   };
 
   const int ty = tid / (BN / 4);
@@ -158,28 +163,37 @@ conv_simt_kernel(ConvArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
-  if (ks_begin < ks_end) {
-    load_tiles(ks_begin);
-    store_tiles(0);
-    __syncthreads();
-    for (int ks = ks_begin; ks < ks_end; ++ks) {
-      int buf = (ks - ks_begin) & 1;
-      if (ks + 1 < ks_end) load_tiles(ks + 1);
+  const int nsteps = max(0, ks_end - ks_begin);
+  pdl_trigger();
+  pdl_wait();
 #pragma unroll
-      for (int k2 = 0; k2 < BK; ++k2) {
-        float4 av = *reinterpret_cast<const float4*>(&As[(buf * BK + k2) * (BM + PAD) + ty * 4]);
-        float4 bv = *reinterpret_cast<const float4*>(&Bs[(buf * BK + k2) * (BN + PAD) + tx * 4]);
-        float ai[4] = {av.x, av.y, av.z, av.w};
-        float bj[4] = {bv.x, bv.y, bv.z, bv.w};
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nsteps) issue(ks_begin + st, st);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nsteps; ++it) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();  // tile `it` landed for everyone; buffer (it-1)%STAGES is free
+    const int nxt = it + STAGES - 1;
+    if (nxt < nsteps) issue(ks_begin + nxt, nxt % STAGES);
+    cp_async_commit();
+    const int buf = it % STAGES;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ai[i], bj[j], acc[i][j]);
+    for (int k2 = 0; k2 < BK; ++k2) {
+      float4 av = *reinterpret_cast<const float4*>(&As[(buf * BK + k2) * (BM + PAD) + ty * 4]);
+      float4 bv = *reinterpret_cast<const float4*>(&Bs[(buf * BK + k2) * (BN + PAD) + tx * 4]);
+      if (PRE) {
+        av.x = fmaxf(av.x, 0.f); av.y = fmaxf(av.y, 0.f); av.z = fmaxf(av.z, 0.f); av.w = fmaxf(av.w, 0.f);
       }
-      if (ks + 1 < ks_end) store_tiles(buf ^ 1);
-      __syncthreads();
+      float ai[4] = {av.x, av.y, av.z, av.w};
+      float bj[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ai[i], bj[j], acc[i][j]);
     }
   }
+  cp_async_wait<0>();
 
   if (a.split == 1) {
 #pragma unroll
@@ -226,6 +240,8 @@ template <int MAXM>
 __global__ void __launch_bounds__(256) conv_gemv_kernel(ConvArgs a) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();
   if (warp >= a.K) return;
   const int n = warp;
   const float* wrow = a.w + (int64_t)n * a.Kdim;
@@ -242,6 +258,7 @@ __global__ void __launch_bounds__(256) conv_gemv_kernel(ConvArgs a) {
   for (int m = 0; m < MAXM; ++m) acc[m] = 0.f;
   const bool vec = (a.in_sc == 1) && ((a.Kdim & 3) == 0) && ((reinterpret_cast<uintptr_t>(wrow) & 15) == 0);
   if (vec) {
+#pragma unroll 4
     for (int k = lane * 4; k < a.Kdim; k += 128) {
       float4 wv = __ldg(reinterpret_cast<const float4*>(wrow + k));
 #pragma unroll
@@ -280,6 +297,25 @@ __global__ void __launch_bounds__(256) conv_gemv_kernel(ConvArgs a) {
     for (int m = 0; m < a.M; ++m) conv_epilogue_store(a, m, n, acc[m]);
 }
 
+static size_t simt_smem_bytes(int bm, int bn) {
+  const size_t tile = 4 * 16 * (size_t)(bm + 4) + 4 * 16 * (size_t)(bn + 4);  // STAGES * BK * (B? + PAD)
+  const size_t part = (size_t)bm * bn;
+  return 4 * (tile > part ? tile : part);
+}
+
+void init_simt_kernels() {
+  const int cfgs[4][2] = {{64, 64}, {32, 64}, {32, 32}, {128, 64}};
+  void (*fns[4][2])(ConvArgs) = {
+      {conv_simt_kernel<64, 64, false>, conv_simt_kernel<64, 64, true>},
+      {conv_simt_kernel<32, 64, false>, conv_simt_kernel<32, 64, true>},
+      {conv_simt_kernel<32, 32, false>, conv_simt_kernel<32, 32, true>},
+      {conv_simt_kernel<128, 64, false>, conv_simt_kernel<128, 64, true>}};
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 2; ++j)
+      cudaFuncSetAttribute(fns[i][j], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)simt_smem_bytes(cfgs[i][0], cfgs[i][1]));
+}
+
 // variant: 0 = 64x64, 1 = 32x64, 2 = 32x32, 3 = 128x64, 8 = gemv (M <= 8, 1x1)
 int launch_conv(const sw_op_desc& op, void* stream) {
   ConvArgs a = conv_args(op);
@@ -288,8 +324,7 @@ int launch_conv(const sw_op_desc& op, void* stream) {
   if (op.variant == 8) {
     if (a.M > 8 || a.R != 1 || a.S != 1) return (int)cudaErrorInvalidValue;
     int blocks = (int)cdiv((int64_t)a.K * 32, 256);
-    conv_gemv_kernel<8><<<blocks, 256, 0, st>>>(a);
-    return (int)cudaGetLastError();
+    return (int)launch_k(conv_gemv_kernel<8>, dim3(blocks), dim3(256), 0, st, 1, a);
   }
   int bm = 64, bn = 64;
   switch (op.variant) {
@@ -301,29 +336,15 @@ int launch_conv(const sw_op_desc& op, void* stream) {
   dim3 grid((unsigned)cdiv(a.M, bm), (unsigned)cdiv(a.K, bn), (unsigned)a.split);
   int threads = (bm / 4) * (bn / 4);
   void (*fn)(ConvArgs) = nullptr;
+  const bool pre = a.pre_relu != 0;
   switch (op.variant) {
-    case 1: fn = conv_simt_kernel<32, 64>; break;
-    case 2: fn = conv_simt_kernel<32, 32>; break;
-    case 3: fn = conv_simt_kernel<128, 64>; break;
-    default: fn = conv_simt_kernel<64, 64>; break;
+    case 1: fn = pre ? conv_simt_kernel<32, 64, true> : conv_simt_kernel<32, 64, false>; break;
+    case 2: fn = pre ? conv_simt_kernel<32, 32, true> : conv_simt_kernel<32, 32, false>; break;
+    case 3: fn = pre ? conv_simt_kernel<128, 64, true> : conv_simt_kernel<128, 64, false>; break;
+    default: fn = pre ? conv_simt_kernel<64, 64, true> : conv_simt_kernel<64, 64, false>; break;
   }
-  if (a.split == 1) {
-    fn<<<grid, threads, 0, st>>>(a);
-    return (int)cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = (unsigned)a.split;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, fn, a);
+  const size_t smem = simt_smem_bytes(bm, bn);
+  return (int)launch_k(fn, grid, dim3(threads), smem, st, (unsigned)a.split, a);
 }
 
 }  // namespace sw

@@ -180,6 +180,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
 
   // Loader mapping: thread owns 16-byte K chunk (tid % 8) of rows tid/8 + 16*i.
   const int chunk = tid & 7;
@@ -426,23 +428,7 @@ static int launch_tc(const TcArgs& a, cudaStream_t st) {
     configured = true;
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), (unsigned)cdiv(a.K, BN), (unsigned)a.split);
-  if (a.split == 1) {
-    conv_tc_kernel<BN><<<grid, TC_THREADS, L::TOTAL, st>>>(a);
-    return (int)cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = L::TOTAL;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = (unsigned)a.split;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN>, a);
+  return (int)launch_k(conv_tc_kernel<BN>, grid, dim3(TC_THREADS), (size_t)L::TOTAL, st, (unsigned)a.split, a);
 }
 
 // variant = N tile (32, 64, 128, 256); SP_SPLIT_K = cluster split along K.

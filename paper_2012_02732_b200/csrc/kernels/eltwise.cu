@@ -58,6 +58,8 @@ __device__ __forceinline__ float ew_combine(const EwArgs& e, float x, float y, f
 }
 
 __global__ void __launch_bounds__(256) ew_scalar_kernel(EwArgs e, int64_t total) {
+  pdl_trigger();
+  pdl_wait();
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   int c = (int)(idx % e.C);
@@ -74,6 +76,8 @@ __global__ void __launch_bounds__(256) ew_scalar_kernel(EwArgs e, int64_t total)
 }
 
 __global__ void __launch_bounds__(256) ew_vec4_kernel(EwArgs e, int64_t total) {
+  pdl_trigger();
+  pdl_wait();
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int CG = e.C / 4;
@@ -118,20 +122,63 @@ int launch_eltwise(const sw_op_desc& d, void* stream) {
   if (total == 0) return 0;
   int blocks = (int)cdiv(total, 256);
   if (v4)
-    ew_vec4_kernel<<<blocks, 256, 0, st>>>(e, total);
+    launch_k(ew_vec4_kernel, dim3(blocks), dim3(256), 0, st, 1, e, total);
   else
-    ew_scalar_kernel<<<blocks, 256, 0, st>>>(e, total);
+    launch_k(ew_scalar_kernel, dim3(blocks), dim3(256), 0, st, 1, e, total);
   return (int)cudaGetLastError();
 }
 
 // Global average pool: out[n, c] = mean_hw(relu?(a[n, h, w, c])).
+// One warp per (n, 4-channel group): lanes stride over the H*W pixels with
+// 128-bit loads (all in flight at once), then a shuffle tree reduces.
+__global__ void __launch_bounds__(256) global_pool_vec4_kernel(EwArgs e) {
+  pdl_trigger();
+  pdl_wait();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int groups = e.C / 4;
+  if (warp >= e.N * groups) return;
+  const int n = warp / groups;
+  const int c = (warp % groups) * 4;
+  const int hw = e.H * e.W;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* base = e.a + n * e.as[0] + c;
+#pragma unroll 4
+  for (int i = lane; i < hw; i += 32) {
+    int h = i / e.W, w = i % e.W;
+    float4 x = __ldg(reinterpret_cast<const float4*>(base + h * e.as[1] + w * e.as[2]));
+    if (e.pre_relu) {
+      x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+    }
+    acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
+  if (lane == 0) {
+    const float inv = 1.f / (float)hw;
+    float* o = e.out + n * e.os[0];
+    o[(c + 0) * e.os[3]] = apply_act(acc.x * inv, e.act);
+    o[(c + 1) * e.os[3]] = apply_act(acc.y * inv, e.act);
+    o[(c + 2) * e.os[3]] = apply_act(acc.z * inv, e.act);
+    o[(c + 3) * e.os[3]] = apply_act(acc.w * inv, e.act);
+  }
+}
+
 __global__ void __launch_bounds__(128) global_pool_kernel(EwArgs e) {
+  pdl_trigger();
+  pdl_wait();
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   int n = blockIdx.y;
   if (c >= e.C) return;
   float acc = 0.f;
   const float* base = e.a + n * e.as[0] + c * e.as[3];
   for (int h = 0; h < e.H; ++h)
+#pragma unroll 4
     for (int w = 0; w < e.W; ++w) {
       float x = __ldg(base + h * e.as[1] + w * e.as[2]);
       acc += e.pre_relu ? fmaxf(x, 0.f) : x;
@@ -144,8 +191,15 @@ int launch_global_pool(const sw_op_desc& d, void* stream) {
   EwArgs e = ew_args(d);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (e.N == 0 || e.C == 0) return 0;
-  dim3 grid((unsigned)cdiv(e.C, 128), (unsigned)e.N);
-  global_pool_kernel<<<grid, 128, 0, st>>>(e);
+  const bool v4 = e.C % 4 == 0 && e.as[3] == 1 && e.as[0] % 4 == 0 && e.as[1] % 4 == 0 && e.as[2] % 4 == 0 &&
+                  aligned16(d.ptrs[EP_A]);
+  if (v4) {
+    int64_t warps = (int64_t)e.N * (e.C / 4);
+    launch_k(global_pool_vec4_kernel, dim3((unsigned)cdiv(warps * 32, 256)), dim3(256), 0, st, 1, e);
+  } else {
+    dim3 grid((unsigned)cdiv(e.C, 128), (unsigned)e.N);
+    launch_k(global_pool_kernel, grid, dim3(128), 0, st, 1, e);
+  }
   return (int)cudaGetLastError();
 }
 
@@ -166,6 +220,8 @@ struct ConcatArgs {
 };
 
 __global__ void __launch_bounds__(256) concat_kernel(ConcatArgs a, int64_t total) {
+  pdl_trigger();
+  pdl_wait();
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   int c = (int)(idx % a.ctot);
@@ -198,7 +254,7 @@ int launch_concat(const sw_op_desc& d, void* stream) {
   a.out = reinterpret_cast<float*>(d.ptrs[7]);
   int64_t total = (int64_t)a.N * a.hw * a.ctot;
   if (total == 0) return 0;
-  concat_kernel<<<(unsigned)cdiv(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a, total);
+  launch_k(concat_kernel, dim3((unsigned)cdiv(total, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1, a, total);
   return (int)cudaGetLastError();
 }
 

@@ -87,10 +87,14 @@ __device__ __forceinline__ float actv(float v, int act) { return apply_act(v, ac
 __device__ __forceinline__ float4 actv(float4 v, int act) { return act4(v, act); }
 
 // KIND 0 = depthwise conv, 1 = pool
-template <int KIND, int VEC>
+template <int KIND, int VEC, int KS>
 __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t total) {
+  const int RR = KS ? KS : a.R;
+  const int SS = KS ? KS : a.S;
   using V = VecT<VEC>;
   using T = typename V::T;
+  pdl_trigger();
+  pdl_wait();
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int CG = a.C / VEC;
@@ -105,10 +109,12 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
   const int ih0 = p * a.sh - a.ph, iw0 = q * a.sw - a.pw;
   T acc = splat(0.f, T{});
   if (KIND == 0) {
-    for (int r = 0; r < a.R; ++r) {
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
       int ih = ih0 + r;
       if (ih < 0 || ih >= a.H) continue;
-      for (int s = 0; s < a.S; ++s) {
+#pragma unroll
+      for (int s = 0; s < SS; ++s) {
         int iw = iw0 + s;
         if (iw < 0 || iw >= a.W) continue;
         T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
@@ -120,10 +126,12 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
     if (a.bias) add_to(acc, V::ld(a.bias + c));
   } else if (a.mode == 0) {  // max
     acc = splat(-INFINITY, T{});
-    for (int r = 0; r < a.R; ++r) {
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
       int ih = ih0 + r;
       if (ih < 0 || ih >= a.H) continue;
-      for (int s = 0; s < a.S; ++s) {
+#pragma unroll
+      for (int s = 0; s < SS; ++s) {
         int iw = iw0 + s;
         if (iw < 0 || iw >= a.W) continue;
         T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
@@ -133,10 +141,12 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
     }
   } else {  // avg
     int cnt = 0;
-    for (int r = 0; r < a.R; ++r) {
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
       int ih = ih0 + r;
       if (ih < 0 || ih >= a.H) continue;
-      for (int s = 0; s < a.S; ++s) {
+#pragma unroll
+      for (int s = 0; s < SS; ++s) {
         int iw = iw0 + s;
         if (iw < 0 || iw >= a.W) continue;
         T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
@@ -181,6 +191,19 @@ static bool can_vec4(const SpatialArgs& a, const sw_op_desc& op, bool has_w) {
   return true;
 }
 
+// taps fully unrolled for the kernel sizes the networks use: all k*k loads of
+// a thread are in flight together (one memory round trip per output)
+template <int KIND, int VEC>
+static void launch_ks(int ks, int blocks, cudaStream_t st, const SpatialArgs& a, int64_t total) {
+  switch (ks) {
+    case 1: launch_k(spatial_kernel<KIND, VEC, 1>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
+    case 3: launch_k(spatial_kernel<KIND, VEC, 3>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
+    case 5: launch_k(spatial_kernel<KIND, VEC, 5>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
+    case 7: launch_k(spatial_kernel<KIND, VEC, 7>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
+    default: launch_k(spatial_kernel<KIND, VEC, 0>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
+  }
+}
+
 template <int KIND>
 static int launch_spatial(const sw_op_desc& op, void* stream) {
   SpatialArgs a = spatial_args(op);
@@ -189,10 +212,11 @@ static int launch_spatial(const sw_op_desc& op, void* stream) {
   int64_t total = (int64_t)a.N * a.P * a.Q * (v4 ? a.C / 4 : a.C);
   if (total == 0) return 0;
   int blocks = (int)cdiv(total, 256);
+  const int ks = (a.R == a.S && (a.R == 1 || a.R == 3 || a.R == 5 || a.R == 7)) ? a.R : 0;
   if (v4)
-    spatial_kernel<KIND, 4><<<blocks, 256, 0, st>>>(a, total);
+    launch_ks<KIND, 4>(ks, blocks, st, a, total);
   else
-    spatial_kernel<KIND, 1><<<blocks, 256, 0, st>>>(a, total);
+    launch_ks<KIND, 1>(ks, blocks, st, a, total);
   return (int)cudaGetLastError();
 }
 

@@ -24,6 +24,10 @@
 #include "../planner/planner.h"
 #include "ops.h"
 
+namespace sw {
+thread_local bool g_launch_pdl = false;
+}
+
 namespace {
 
 constexpr int kSlots = 4;
@@ -54,6 +58,7 @@ struct sw_engine {
   std::vector<sw_op_desc> ops;
   uint64_t host_in = 0, dev_in = 0, host_out = 0, dev_out = 0;
   int64_t in_bytes = 0, out_bytes = 0;
+  uint32_t flags = 0;  // SW_ENGINE_PDL
   Slot slots[kSlots];
 };
 
@@ -120,6 +125,7 @@ int sw_engine_create(int32_t device, sw_engine** out) {
   }
   CU(cudaStreamCreateWithFlags(&e->launch, cudaStreamNonBlocking));
   sw::init_tc_kernels();
+  sw::init_simt_kernels();
   CU(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   CU(cudaEventCreate(&e->t0));
   CU(cudaEventCreate(&e->t1));
@@ -180,6 +186,10 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
 
   cudaStream_t origin = e->launch;
   CU(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
+  struct PdlScope {
+    explicit PdlScope(bool on) { sw::g_launch_pdl = on; }
+    ~PdlScope() { sw::g_launch_pdl = false; }
+  } pdl_scope((e->flags & SW_ENGINE_PDL) != 0);
   auto abort_capture = [&](int code) {
     cudaGraph_t g = nullptr;
     cudaStreamEndCapture(origin, &g);
@@ -278,7 +288,15 @@ int sw_engine_time_replay(sw_engine* e, int32_t slot, int32_t iters, double* out
 
 int sw_engine_launch_op(sw_engine* e, int64_t index) {
   if (index < 0 || index >= (int64_t)e->ops.size()) return sw::fail(SW_VALUE_ERROR, "op index out of range");
-  return launch_task(e->ops[index], e->launch);
+  sw::g_launch_pdl = (e->flags & SW_ENGINE_PDL) != 0;
+  int rc = launch_task(e->ops[index], e->launch);
+  sw::g_launch_pdl = false;
+  return rc;
+}
+
+int sw_engine_set_flags(sw_engine* e, uint32_t flags) {
+  e->flags = flags;
+  return SW_OK;
 }
 
 int sw_engine_run_eager(sw_engine* e, int64_t n, const int64_t* order) {

@@ -72,5 +72,6 @@ int launch_eltwise(const sw_op_desc& op, void* stream);
 int launch_global_pool(const sw_op_desc& op, void* stream);
 int launch_concat(const sw_op_desc& op, void* stream);
 void init_tc_kernels();
+void init_simt_kernels();
 
 }  // namespace sw

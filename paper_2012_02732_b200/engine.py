@@ -319,7 +319,7 @@ class Engine:
     """Nimble-style AoT engine around a static ``nn.Module`` (eval mode, fp32)."""
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
-                 device: int = 0, conv_impl: str = "auto"):
+                 device: int = 0, conv_impl: str = "auto", pdl: bool = True):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -328,6 +328,7 @@ class Engine:
         self.fuse = fuse
         self.device = device
         self.conv_impl = conv_impl
+        self.pdl = pdl
         self.tuning = {}
         self._h = None
         self.prepared = False
@@ -409,6 +410,7 @@ class Engine:
             self._autotune()
         self.plan_seconds["autotune"] = time.perf_counter() - t3
         N.check(lib.sw_engine_set_ops(h, len(prog.tasks), self.ops))
+        N.check(lib.sw_engine_set_flags(h, 1 if self.pdl else 0))
         t3 = time.perf_counter()
         self._capture(SLOT_MULTI_IO, ts, True)
         self._capture(SLOT_SINGLE_IO, ts_single, True)
@@ -455,6 +457,16 @@ class Engine:
     def model_output_shape(prog: Program):
         o = prog.output_view.st
         return (o.n, o.c, o.h, o.w) if (o.h * o.w > 1) else (o.n, o.c)
+
+    def recapture(self, pdl: bool | None = None):
+        """Re-capture every slot (e.g. after toggling programmatic dependent launch)."""
+        if pdl is not None:
+            self.pdl = pdl
+            N.check(N.lib().sw_engine_set_flags(self._h, 1 if pdl else 0))
+        self._capture(SLOT_MULTI_IO, self.schedule, True)
+        self._capture(SLOT_SINGLE_IO, self.schedule_single, True)
+        self._capture(SLOT_MULTI, self.schedule, False)
+        self._capture(SLOT_SINGLE, self.schedule_single, False)
 
     def _capture(self, slot: int, ts: TaskSchedule, with_io: bool):
         lens, kinds, args, order = schedule_arrays(ts)

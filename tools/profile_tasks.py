@@ -71,6 +71,28 @@ def main():
           f"single {r_single.makespan/1000:.1f} us critical path "
           f"{sw.critical_path_time(g2)/1000:.1f} us")
     print("tuning picks:", {k: v for k, v in list(eng.tuning.items())[:5]}, "...")
+    # the critical path itself (longest measured-duration chain)
+    preds = {t.tid: sorted(t.deps) for t in eng.program.tasks}
+    best, arg = {}, {}
+    for tid in sw.topological_order(g):
+        b, a_ = 0.0, None
+        for p in preds[tid]:
+            if best[p] > b:
+                b, a_ = best[p], p
+        best[tid] = b + per[tid]
+        arg[tid] = a_
+    end = max(best, key=best.get)
+    chain = []
+    while end is not None:
+        chain.append(end)
+        end = arg[end]
+    chain.reverse()
+    kinds = {}
+    for tid in chain:
+        k = eng.program.tasks[tid].kind
+        kinds[k] = kinds.get(k, 0) + 1
+    print(f"critical path: {len(chain)} tasks {kinds}")
+    print("  " + " > ".join(f"{eng.program.tasks[t].kind}{t}({per[t]:.1f})" for t in chain[:60]))
     if a.json:
         with open(a.json, "w") as fh:
             json.dump({"rows": rows, "replay_multi_us": gm, "replay_single_us": gs,
