@@ -9,14 +9,19 @@
 
 namespace sw {
 
+// Transcendental activations live out of line: batch-1 kernels run on cold
+// SMs, and every inlined copy of expf grows the code an SM must fetch.
+static __device__ __noinline__ float act_slow(float v, int act) {
+  if (act == ACT_SILU) return v / (1.f + expf(-v));
+  if (act == ACT_SIGMOID) return 1.f / (1.f + expf(-v));
+  return v;
+}
+
 __device__ __forceinline__ float apply_act(float v, int act) {
-  switch (act) {
-    case ACT_RELU: return fmaxf(v, 0.f);
-    case ACT_RELU6: return fminf(fmaxf(v, 0.f), 6.f);
-    case ACT_SILU: return v / (1.f + expf(-v));
-    case ACT_SIGMOID: return 1.f / (1.f + expf(-v));
-    default: return v;
-  }
+  if (act == ACT_NONE) return v;
+  if (act == ACT_RELU) return fmaxf(v, 0.f);
+  if (act == ACT_RELU6) return fminf(fmaxf(v, 0.f), 6.f);
+  return act_slow(v, act);
 }
 
 __device__ __forceinline__ float4 act4(float4 v, int act) {

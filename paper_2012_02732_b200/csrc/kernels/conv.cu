@@ -84,6 +84,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <int BM, int BN, bool PRE>
 __global__ void __launch_bounds__((BM / 4) * (BN / 4))
 conv_simt_kernel(ConvArgs a) {
+  // Code size matters as much as FLOPs here: at batch 1 every CTA starts on
+  // a cold SM, so loops outside the FMA micro-kernel stay rolled and the
+  // epilogue is one smem-staged loop shared with the split-K reduction.
   constexpr int BK = 16;
   constexpr int STAGES = 4;
   constexpr int NT = (BM / 4) * (BN / 4);
@@ -91,67 +94,59 @@ conv_simt_kernel(ConvArgs a) {
   constexpr int B_PER = BN * BK / NT;
   constexpr int PAD = 4;
   static_assert(NT % BK == 0, "kk must be fixed per thread");
-  constexpr int TILE_FLOATS = STAGES * BK * (BM + PAD) + STAGES * BK * (BN + PAD);
-  constexpr int SMEM_FLOATS = TILE_FLOATS > BM * BN ? TILE_FLOATS : BM * BN;
   extern __shared__ __align__(16) float smem[];
   float* As = smem;                                // [STAGES][BK][BM+PAD]
   float* Bs = smem + STAGES * BK * (BM + PAD);     // [STAGES][BK][BN+PAD]
-  (void)SMEM_FLOATS;
 
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * BM;
   const int n0 = blockIdx.y * BN;
   const int kk = tid % BK;
+  const int row = tid / BK;  // + i * (NT / BK)
 
   // K range of this split (cluster rank == blockIdx.z)
   const int ksteps_total = (a.Kdim + BK - 1) / BK;
   const int per = (ksteps_total + a.split - 1) / a.split;
   const int ks_begin = blockIdx.z * per;
-  const int ks_end = min(ksteps_total, ks_begin + per);
+  const int nsteps = max(0, min(ksteps_total, ks_begin + per) - ks_begin);
 
   // per-thread pixel decode for the A loads (fixed across K)
-  int64_t a_base[A_PER];
-  int a_ih[A_PER], a_iw[A_PER];
-  bool a_ok[A_PER];
+  int a_base[A_PER], a_ih[A_PER], a_iw[A_PER];
 #pragma unroll
   for (int i = 0; i < A_PER; ++i) {
-    int mm = (tid + i * NT) / BK;
-    int m = m0 + mm;
-    a_ok[i] = m < a.M;
-    int mq = a_ok[i] ? m : 0;
-    int q = mq % a.Q;
-    int t = mq / a.Q;
+    int m = m0 + row + i * (NT / BK);
+    int q = m % a.Q;
+    int t = m / a.Q;
     int p = t % a.P;
     int nb = t / a.P;
-    a_base[i] = nb * a.in_sn;
-    a_ih[i] = p * a.sh - a.ph;
+    a_base[i] = nb * (int)a.in_sn;
+    a_ih[i] = m < a.M ? p * a.sh - a.ph : -(1 << 28);  // out-of-range row: never valid
     a_iw[i] = q * a.sw - a.pw;
   }
-  // issue the cp.async gather of K tile `kstep` into pipeline buffer `buf`
+  const int in_sh = (int)a.in_sh, in_sw = (int)a.in_sw, in_sc = (int)a.in_sc;
+
+  // cp.async gather of K tile `kstep` into pipeline buffer `buf`
   auto issue = [&](int kstep, int buf) {
-    int k = kstep * BK + kk;
-    bool kin = k < a.Kdim;
-    int c = 0, r = 0, s = 0;
-    if (kin) {
-      c = k % a.C;
-      int rs = k / a.C;
-      s = rs % a.S;
-      r = rs / a.S;
-    }
-    float* as = As + (buf * BK + kk) * (BM + PAD);
-    float* bs = Bs + (buf * BK + kk) * (BN + PAD);
+    const int k = kstep * BK + kk;
+    const bool kin = k < a.Kdim;
+    const int c = k % a.C;
+    const int rs = k / a.C;
+    const int s = rs % a.S;
+    const int r = rs / a.S;
+    float* as = As + (buf * BK + kk) * (BM + PAD) + row;
+    float* bs = Bs + (buf * BK + kk) * (BN + PAD) + row;
 #pragma unroll
     for (int i = 0; i < A_PER; ++i) {
-      int ih = a_ih[i] + r, iw = a_iw[i] + s;
-      bool ok = kin && a_ok[i] && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-      const float* src = ok ? a.in + a_base[i] + ih * a.in_sh + iw * a.in_sw + c * a.in_sc : a.in;
-      cp_async4(as + (tid + i * NT) / BK, src, ok);
+      const int ih = a_ih[i] + r, iw = a_iw[i] + s;
+      const bool ok = kin && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
+      const float* src = a.in + (ok ? a_base[i] + ih * in_sh + iw * in_sw + c * in_sc : 0);
+      cp_async4(as + i * (NT / BK), src, ok);
     }
 #pragma unroll
     for (int i = 0; i < B_PER; ++i) {
-      int n = n0 + (tid + i * NT) / BK;
-      bool ok = kin && n < a.K;
-      cp_async4(bs + (tid + i * NT) / BK, ok ? a.w + (int64_t)n * a.Kdim + k : a.w, ok);
+      const int n = n0 + row + i * (NT / BK);
+      const bool ok = kin && n < a.K;
+      cp_async4(bs + i * (NT / BK), a.w + (ok ? (size_t)n * a.Kdim + k : 0), ok);
     }
   };
 
@@ -163,30 +158,31 @@ conv_simt_kernel(ConvArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
-  const int nsteps = max(0, ks_end - ks_begin);
   pdl_trigger();
   pdl_wait();
-#pragma unroll
+#pragma unroll 1
   for (int st = 0; st < STAGES - 1; ++st) {
     if (st < nsteps) issue(ks_begin + st, st);
     cp_async_commit();
   }
+#pragma unroll 1
   for (int it = 0; it < nsteps; ++it) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();  // tile `it` landed for everyone; buffer (it-1)%STAGES is free
     const int nxt = it + STAGES - 1;
     if (nxt < nsteps) issue(ks_begin + nxt, nxt % STAGES);
     cp_async_commit();
-    const int buf = it % STAGES;
-#pragma unroll
+    const float* at = As + (it % STAGES) * BK * (BM + PAD) + ty * 4;
+    const float* bt = Bs + (it % STAGES) * BK * (BN + PAD) + tx * 4;
+#pragma unroll 4
     for (int k2 = 0; k2 < BK; ++k2) {
-      float4 av = *reinterpret_cast<const float4*>(&As[(buf * BK + k2) * (BM + PAD) + ty * 4]);
-      float4 bv = *reinterpret_cast<const float4*>(&Bs[(buf * BK + k2) * (BN + PAD) + tx * 4]);
+      float4 av = *reinterpret_cast<const float4*>(at + k2 * (BM + PAD));
+      float4 bv = *reinterpret_cast<const float4*>(bt + k2 * (BN + PAD));
       if (PRE) {
         av.x = fmaxf(av.x, 0.f); av.y = fmaxf(av.y, 0.f); av.z = fmaxf(av.z, 0.f); av.w = fmaxf(av.w, 0.f);
       }
-      float ai[4] = {av.x, av.y, av.z, av.w};
-      float bj[4] = {bv.x, bv.y, bv.z, bv.w};
+      const float ai[4] = {av.x, av.y, av.z, av.w};
+      const float bj[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -194,45 +190,41 @@ conv_simt_kernel(ConvArgs a) {
     }
   }
   cp_async_wait<0>();
-
-  if (a.split == 1) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      int m = m0 + ty * 4 + i;
-      if (m >= a.M) continue;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int n = n0 + tx * 4 + j;
-        if (n < a.K) conv_epilogue_store(a, m, n, acc[i][j]);
-      }
-    }
-    return;
-  }
-
-  // split-K: reduce partial tiles across the cluster through DSMEM.
-  cg::cluster_group cluster = cg::this_cluster();
-  float* part = smem;  // BM*BN floats, reuses the operand tiles
   __syncthreads();
+
+  // stage the tile in smem (reusing the operand buffers), then one rolled
+  // epilogue loop; split-K ranks of a cluster reduce through DSMEM first
+  float* part = smem;  // [BM][BN]
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) part[(ty * 4 + i) * BN + tx * 4 + j] = acc[i][j];
-  cluster.sync();
-  const int rank = (int)cluster.block_rank();
-  const int nranks = (int)cluster.num_blocks();
-  const int chunk = (BM * BN + nranks - 1) / nranks;
-  const int e_begin = rank * chunk;
-  const int e_end = min(BM * BN, e_begin + chunk);
+    *reinterpret_cast<float4*>(&part[(ty * 4 + i) * BN + tx * 4]) =
+        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  int e_begin = 0, e_end = BM * BN, nranks = 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  if (a.split > 1) {
+    cluster.sync();
+    nranks = (int)cluster.num_blocks();
+    const int chunk = (BM * BN + nranks - 1) / nranks;
+    e_begin = (int)cluster.block_rank() * chunk;
+    e_end = min(BM * BN, e_begin + chunk);
+  } else {
+    __syncthreads();
+  }
+#pragma unroll 1
   for (int e = e_begin + tid; e < e_end; e += NT) {
-    int mm = e / BN, nn = e % BN;
-    int m = m0 + mm, n = n0 + nn;
+    const int m = m0 + e / BN, n = n0 + e % BN;
     if (m >= a.M || n >= a.K) continue;
-    float v = 0.f;
-    for (int r = 0; r < nranks; ++r) v += cluster.map_shared_rank(part, r)[e];
+    float v = part[e];
+    if (nranks > 1) {
+      v = 0.f;
+#pragma unroll 1
+      for (int r = 0; r < nranks; ++r) v += cluster.map_shared_rank(part, r)[e];
+    }
     conv_epilogue_store(a, m, n, v);
   }
-  cluster.sync();
+  if (a.split > 1) cluster.sync();
 }
+
 
 // Small-M 1x1 conv / linear (batch-1 classifier heads, 1x1-spatial layers):
 // one warp per output channel streams its weight row once with 128-bit loads.
@@ -258,7 +250,7 @@ __global__ void __launch_bounds__(256) conv_gemv_kernel(ConvArgs a) {
   for (int m = 0; m < MAXM; ++m) acc[m] = 0.f;
   const bool vec = (a.in_sc == 1) && ((a.Kdim & 3) == 0) && ((reinterpret_cast<uintptr_t>(wrow) & 15) == 0);
   if (vec) {
-#pragma unroll 4
+#pragma unroll 1
     for (int k = lane * 4; k < a.Kdim; k += 128) {
       float4 wv = __ldg(reinterpret_cast<const float4*>(wrow + k));
 #pragma unroll
@@ -293,8 +285,11 @@ __global__ void __launch_bounds__(256) conv_gemv_kernel(ConvArgs a) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     acc[m] = v;
   }
-  if (lane == 0)
-    for (int m = 0; m < a.M; ++m) conv_epilogue_store(a, m, n, acc[m]);
+  if (lane == 0) {
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m)
+      if (m < a.M) conv_epilogue_store(a, m, n, acc[m]);
+  }
 }
 
 static size_t simt_smem_bytes(int bm, int bn) {

@@ -241,35 +241,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     } else {
-#pragma unroll
+      // generic strides / C % 4 != 0 (first layer): rolled to keep code small
+#pragma unroll 1
       for (int i = 0; i < A_ROWS; ++i) {
         float e[4];
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < 4; ++j) {
-          int kk = k + j;
-          float v = 0.f;
-          if (kk < a.Kdim && a_ok[i]) {
-            int c = kk % a.C;
-            int rs = kk / a.C;
-            int s = rs % a.S, r = rs / a.S;
-            int ih = a_ih[i] + r, iw = a_iw[i] + s;
-            if (ih >= 0 && ih < a.H && iw >= 0 && iw < a.W) {
-              v = __ldg(a.in + a_base[i] + ih * a.in_sh + iw * a.in_sw + c * a.in_sc);
-              if (a.pre_relu) v = fmaxf(v, 0.f);
-            }
-          }
-          e[j] = v;
+          const int kk = k + j;
+          const int c = kk % a.C;
+          const int rs = kk / a.C;
+          const int ih = a_ih[i] + rs / a.S, iw = a_iw[i] + rs % a.S;
+          const bool ok = kk < a.Kdim && a_ok[i] && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
+          float v = __ldg(a.in + (ok ? a_base[i] + ih * a.in_sh + iw * a.in_sw + c * a.in_sc : 0));
+          if (a.pre_relu) v = fmaxf(v, 0.f);
+          e[j] = ok ? v : 0.f;
         }
         ra[i] = make_float4(e[0], e[1], e[2], e[3]);
       }
-#pragma unroll
+#pragma unroll 1
       for (int i = 0; i < B_ROWS; ++i) {
-        int n = n0 + row0 + 16 * i;
+        const int n = n0 + row0 + 16 * i;
         float e[4];
-#pragma unroll
+#pragma unroll 1
         for (int j = 0; j < 4; ++j) {
-          int kk = k + j;
-          e[j] = (kk < a.Kdim && n < a.K) ? __ldg(a.w + (int64_t)n * a.Kdim + kk) : 0.f;
+          const int kk = k + j;
+          const bool ok = kk < a.Kdim && n < a.K;
+          const float v = __ldg(a.w + (ok ? (int64_t)n * a.Kdim + kk : 0));
+          e[j] = ok ? v : 0.f;
         }
         rb[i] = make_float4(e[0], e[1], e[2], e[3]);
       }
@@ -332,55 +330,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   const int m = m0 + row;
   const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
 
-  if (a.split == 1) {
+  // TMEM → smem tile (rows = TMEM lanes) → one rolled epilogue loop, shared
+  // with the split-K DSMEM reduction; keeps the kernel's code footprint small
+  float* part = reinterpret_cast<float*>(smem);  // [128][BN]; operand smem is free now
+  __syncthreads();
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      if (iters > 0) {
-        tmem_ld16(t_row + c0, v);
-      } else {
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    float v[16];
+    if (iters > 0) {
+      tmem_ld16(t_row + c0, v);
+    } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-      }
-      if (m < a.M) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          int n = n0 + c0 + j;
-          if (n < a.K) tc_epilogue_store(a, m, n, v[j]);
-        }
-      }
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
     }
-  } else {
-    // split-K: park the partial tile in smem, reduce across the cluster via DSMEM
-    cg::cluster_group cluster = cg::this_cluster();
-    float* part = reinterpret_cast<float*>(smem);
-    __syncthreads();  // all MMAs done (waited above); operand smem is free
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      if (iters > 0) {
-        tmem_ld16(t_row + c0, v);
-      } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) part[row * BN + c0 + j] = v[j];
-    }
-    cluster.sync();
-    const int rank = (int)cluster.block_rank();
-    const int nr = (int)cluster.num_blocks();
-    const int chunk_e = (TC_BM * BN + nr - 1) / nr;
-    const int e0 = rank * chunk_e, e1 = min(TC_BM * BN, e0 + chunk_e);
-    for (int e = e0 + tid; e < e1; e += TC_THREADS) {
-      int mm = m0 + e / BN, nn = n0 + e % BN;
-      if (mm >= a.M || nn >= a.K) continue;
-      float s = 0.f;
-      for (int r2 = 0; r2 < nr; ++r2) s += cluster.map_shared_rank(part, r2)[e];
-      tc_epilogue_store(a, mm, nn, s);
-    }
-    cluster.sync();
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
+  (void)m;
+  int e0 = 0, e1 = TC_BM * BN, nr = 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  if (a.split > 1) {
+    cluster.sync();
+    nr = (int)cluster.num_blocks();
+    const int chunk_e = (TC_BM * BN + nr - 1) / nr;
+    e0 = (int)cluster.block_rank() * chunk_e;
+    e1 = min(TC_BM * BN, e0 + chunk_e);
+  } else {
+    __syncthreads();
+  }
+#pragma unroll 1
+  for (int e = e0 + tid; e < e1; e += TC_THREADS) {
+    const int mm = m0 + e / BN, nn = n0 + e % BN;
+    if (mm >= a.M || nn >= a.K) continue;
+    float sacc = part[e];
+    if (nr > 1) {
+      sacc = 0.f;
+#pragma unroll 1
+      for (int r2 = 0; r2 < nr; ++r2) sacc += cluster.map_shared_rank(part, r2)[e];
+    }
+    tc_epilogue_store(a, mm, nn, sacc);
+  }
+  if (a.split > 1) cluster.sync();
 
   tc_fence_before();
   __syncthreads();

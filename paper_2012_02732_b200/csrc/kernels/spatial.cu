@@ -107,59 +107,46 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
   int c = cg * VEC;
   const float* base = a.in + n * a.in_sn + c * a.in_sc;
   const int ih0 = p * a.sh - a.ph, iw0 = q * a.sw - a.pw;
+  // Branch-free taps: every load is issued unconditionally from a clamped
+  // (always valid) address and out-of-range values are masked with selects,
+  // so the unrolled loop keeps all tap loads in flight at once instead of one
+  // memory round trip per tap (ncu: 45.8K cycles for a 7x7 with branches).
   T acc = splat(0.f, T{});
-  if (KIND == 0) {
+  int cnt = 0;
+  if (KIND == 1 && a.mode == 0) acc = splat(-INFINITY, T{});
 #pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      int ih = ih0 + r;
-      if (ih < 0 || ih >= a.H) continue;
+  for (int r = 0; r < RR; ++r) {
+    const int ih = ih0 + r;
+    const bool rok = (unsigned)ih < (unsigned)a.H;
+    const int ihc = rok ? ih : 0;
 #pragma unroll
-      for (int s = 0; s < SS; ++s) {
-        int iw = iw0 + s;
-        if (iw < 0 || iw >= a.W) continue;
-        T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
-        if (a.pre_relu) x = relu1(x);
-        T wv = V::ld(a.w + (r * a.S + s) * a.C + c);
+    for (int s = 0; s < SS; ++s) {
+      const int iw = iw0 + s;
+      const bool ok = rok && (unsigned)iw < (unsigned)a.W;
+      const int iwc = ok ? iw : 0;
+      T x = V::ld(base + ihc * a.in_sh + iwc * a.in_sw);
+      if (a.pre_relu) x = relu1(x);
+      if (KIND == 0) {
+        T wv = V::ld(a.w + (r * SS + s) * a.C + c);
+        x = ok ? x : splat(0.f, T{});
         fma_acc(acc, x, wv);
-      }
-    }
-    if (a.bias) add_to(acc, V::ld(a.bias + c));
-  } else if (a.mode == 0) {  // max
-    acc = splat(-INFINITY, T{});
-#pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      int ih = ih0 + r;
-      if (ih < 0 || ih >= a.H) continue;
-#pragma unroll
-      for (int s = 0; s < SS; ++s) {
-        int iw = iw0 + s;
-        if (iw < 0 || iw >= a.W) continue;
-        T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
-        if (a.pre_relu) x = relu1(x);
-        max_to(acc, x);
-      }
-    }
-  } else {  // avg
-    int cnt = 0;
-#pragma unroll
-    for (int r = 0; r < RR; ++r) {
-      int ih = ih0 + r;
-      if (ih < 0 || ih >= a.H) continue;
-#pragma unroll
-      for (int s = 0; s < SS; ++s) {
-        int iw = iw0 + s;
-        if (iw < 0 || iw >= a.W) continue;
-        T x = V::ld(base + ih * a.in_sh + iw * a.in_sw);
-        if (a.pre_relu) x = relu1(x);
+      } else if (a.mode == 0) {
+        if (ok) max_to(acc, x);
+      } else {
+        x = ok ? x : splat(0.f, T{});
         add_to(acc, x);
-        ++cnt;
+        cnt += ok ? 1 : 0;
       }
     }
+  }
+  if (KIND == 0) {
+    if (a.bias) add_to(acc, V::ld(a.bias + c));
+  } else if (a.mode == 1) {
     int div = cnt;
     if (a.count_pad) {  // torch: window clipped to [-pad, H + pad_bottom)
-      int hs = ih0, he = min(ih0 + a.R, a.H + a.pad_b);
-      int ws = iw0, we = min(iw0 + a.S, a.W + a.pad_r);
-      div = (he - hs) * (we - ws);
+      int he = min(ih0 + RR, a.H + a.pad_b);
+      int we = min(iw0 + SS, a.W + a.pad_r);
+      div = (he - ih0) * (we - iw0);
     }
     scale(acc, div > 0 ? 1.f / (float)div : 0.f);
   }

@@ -332,10 +332,12 @@ int sw_engine_graph_topology(sw_engine* e, int32_t slot, int64_t cap, int64_t* o
     auto it = sl.node_task.find(nodes[i]);
     out_node_task[i] = it == sl.node_task.end() ? -1 : it->second;
   }
+  // _v2: programmatic (PDL) edges carry edge data; the v1 query is "lossy"
   size_t ne = 0;
-  CU(cudaGraphGetEdges(sl.graph, nullptr, nullptr, &ne));
+  CU(cudaGraphGetEdges_v2(sl.graph, nullptr, nullptr, nullptr, &ne));
   std::vector<cudaGraphNode_t> from(ne), to(ne);
-  if (ne) CU(cudaGraphGetEdges(sl.graph, from.data(), to.data(), &ne));
+  std::vector<cudaGraphEdgeData> edata(ne);
+  if (ne) CU(cudaGraphGetEdges_v2(sl.graph, from.data(), to.data(), edata.data(), &ne));
   *out_n_edges = (int64_t)ne;
   if ((int64_t)ne > cap) return sw::fail(SW_VALUE_ERROR, "topology buffer too small");
   for (size_t i = 0; i < ne; ++i) {
