@@ -1,22 +1,26 @@
 // Dense convolution / GEMM on the 5th-generation tensor cores (tcgen05 + TMEM).
 //
 // Implicit GEMM: rows = output pixels (M = N*P*Q), columns = output channels,
-// K = R*S*C (weights [K][R][S][C]).  One CTA = 128 threads computes a
-// 128 x BN tile: the four warps gather the im2col A tile and the weight B
-// tile (128-bit loads, K-contiguous in NHWC), split every fp32 value into a
-// TF32 pair (hi = rna(x), lo = x - hi) and store both halves into shared
-// memory in the canonical K-major, no-swizzle UMMA layout (8-row x 16-byte
-// core matrices).  One elected thread issues, per 8-wide K step,
-//     D += A_hi·B_hi + A_hi·B_lo + A_lo·B_hi      (tcgen05.mma kind::tf32)
-// into a TMEM fp32 accumulator (3xTF32: ~fp32 accuracy, which the fp32
-// parity gate of rel 1e-3 needs over 50-300 layers).  Stages are
-// double buffered: tcgen05.commit arrives on the stage's mbarrier when the
-// tensor core has consumed it, so gathering tile k+1 overlaps the MMAs of
-// tile k.  The epilogue reads TMEM with tcgen05.ld (warp w owns TMEM lanes
-// 32w..32w+31 = tile rows), applies bias (folded BN) + residual + activation
-// and stores NHWC / channel-slice / NCHW output.  Split-K uses a cluster of
-// CTAs along z whose partial tiles are reduced through DSMEM, exactly like
-// the SIMT kernel (conv.cu).
+// K = R*S*C.  One CTA = 128 threads computes a 128 x BN tile over its slice of
+// K (split-K across a thread-block cluster along z, reduced through DSMEM).
+//
+// Latency-first pipeline (batch-1 layers are round-trip bound, not FLOP bound):
+//  * every K tile of the CTA's slice is requested at once with cp.async
+//    straight into the canonical K-major / no-swizzle UMMA layout (8-row x
+//    16-byte core matrices): im2col rows of NHWC activations are 16-byte
+//    chunks of 4 consecutive channels; out-of-range taps are zero-filled by
+//    cp.async, so a layer costs ~one memory round trip;
+//  * fp32 accuracy via 3xTF32: weights arrive pre-split (W_hi = tf32(W),
+//    W_lo = W - W_hi, prepared once at plan time, [K][Kpad]); activations are
+//    split in shared memory by one pass per stage (hi in place, lo beside it);
+//    one elected thread issues, per 8-wide K step,
+//        D += A_hi·B_hi + A_hi·B_lo + A_lo·B_hi   (tcgen05.mma.kind::tf32)
+//    into an fp32 TMEM accumulator; tcgen05.commit → per-stage mbarrier frees
+//    a stage for refill when the slice is longer than the stage ring;
+//  * epilogue: tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = tile rows) →
+//    smem tile → one rolled loop: bias (folded BN) + residual + activation,
+//    strided NHWC / channel-slice / NCHW store.  Code is kept compact because
+//    every CTA of a batch-1 layer starts on a cold SM.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -30,14 +34,15 @@ namespace {
 struct TcArgs {
   const float* __restrict__ in;
   float* __restrict__ out;
-  const float* __restrict__ w;
+  const float* __restrict__ w_hi;  // [K][Kpad]
+  const float* __restrict__ w_lo;  // [K][Kpad]
   const float* __restrict__ bias;
   const float* __restrict__ res;
   int N, H, W, C, P, Q, K, R, S, sh, sw, ph, pw, act, pre_relu, has_res;
-  int64_t in_sn, in_sh, in_sw, in_sc;
+  int in_sn, in_sh, in_sw, in_sc;
   int64_t out_sn, out_sh, out_sw, out_sc;
   int64_t res_sn, res_sh, res_sw, res_sc;
-  int M, Kdim, split, vec;
+  int M, Kdim, Kpad, split, vec;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -65,17 +70,12 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// SWIZZLE_NONE, K-major canonical layout: core matrix = 8 rows x 16 B;
+// SWIZZLE_NONE, K-major canonical layout (mma_sm100_desc.hpp SmemDescriptor):
 // SBO = byte stride between 8-row groups, LBO = byte stride between the two
-// 16-byte K chunks of one MMA (mma_sm100_desc.hpp SmemDescriptor bit layout).
+// 16-byte K chunks of one MMA, version = 1 (sm_100), layout type 0.
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // version = 1 (sm_100)
-  // base_offset = 0, lbo_mode = 0, layout_type (bits 61-63) = 0: SWIZZLE_NONE
-  return d;
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -104,43 +104,42 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
+__device__ __forceinline__ void cp4(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__device__ __forceinline__ void store_split(uint8_t* hi_base, uint8_t* lo_base, uint32_t off, float4 v) {
-  float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-  float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-  *reinterpret_cast<float4*>(hi_base + off) = h;
-  *reinterpret_cast<float4*>(lo_base + off) = l;
-}
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __device__ __forceinline__ void tc_epilogue_store(const TcArgs& a, int m, int n, float v) {
-  int q = m % a.Q;
-  int t = m / a.Q;
-  int pp = t % a.P;
-  int nb = t / a.P;
+  const int q = m % a.Q;
+  const int t = m / a.Q;
+  const int pp = t % a.P;
+  const int nb = t / a.P;
   v += a.bias ? a.bias[n] : 0.f;
   if (a.has_res) v += a.res[nb * a.res_sn + pp * a.res_sh + q * a.res_sw + n * a.res_sc];
   a.out[nb * a.out_sn + pp * a.out_sh + q * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
 }
 
 constexpr int TC_BM = 128;
-constexpr int TC_BK = 32;  // fp32 elements per stage (= 8 chunks of 16 B = 4 MMA K-steps)
+constexpr int TC_BK = 32;  // fp32 per stage row = 8 chunks of 16 B = 4 MMA K-steps
 constexpr int TC_THREADS = 128;
 
 template <int BN>
 struct TcSmem {
-  static constexpr int A_BYTES = TC_BM * TC_BK * 4;
+  static constexpr int A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 4;
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int STAGES = 2;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
+  static constexpr int STAGES = (BN <= 64) ? 4 : (BN == 128 ? 3 : 2);
   static constexpr int OPER = STAGES * STAGE;
-  static constexpr int PART = TC_BM * BN * 4;  // split-K partial tile (reuses operands)
+  static constexpr int PART = TC_BM * BN * 4;
   static constexpr int BODY = OPER > PART ? OPER : PART;
-  static constexpr int TOTAL = BODY + 64;      // + mbarriers + tmem slot
+  static constexpr int TOTAL = BODY + 128;  // + mbarriers + tmem slot
   static constexpr int NCOLS = BN < 32 ? 32 : BN;
 };
 
@@ -149,9 +148,11 @@ struct TcSmem {
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   using L = TcSmem<BN>;
+  constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::BODY);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::BODY + 32);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::BODY + 8 * S);
+  const uint32_t sbase = smem_u32(smem);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -162,12 +163,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   const int ktiles = (a.Kdim + TC_BK - 1) / TC_BK;
   const int per = (ktiles + a.split - 1) / a.split;
   const int kt0 = blockIdx.z * per;
-  const int kt1 = min(ktiles, kt0 + per);
-  const int iters = max(0, kt1 - kt0);
+  const int iters = max(0, min(ktiles, kt0 + per) - kt0);
 
   if (tid == 0) {
-    mbar_init(smem_u32(&mbar[0]), 1);
-    mbar_init(smem_u32(&mbar[1]), 1);
+    for (int s = 0; s < S; ++s) mbar_init(smem_u32(&mbar[s]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -180,132 +179,107 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_trigger();
-  pdl_wait();
 
   // Loader mapping: thread owns 16-byte K chunk (tid % 8) of rows tid/8 + 16*i.
   const int chunk = tid & 7;
   const int row0 = tid >> 3;
-  constexpr int A_ROWS = TC_BM / 16;  // 8 rows per thread
+  constexpr int A_ROWS = TC_BM / 16;
   constexpr int B_ROWS = BN / 16;
-  int64_t a_base[A_ROWS];
-  int a_ih[A_ROWS], a_iw[A_ROWS];
-  bool a_ok[A_ROWS];
+  int a_base[A_ROWS], a_ih[A_ROWS], a_iw[A_ROWS];
 #pragma unroll
   for (int i = 0; i < A_ROWS; ++i) {
-    int m = m0 + row0 + 16 * i;
-    a_ok[i] = m < a.M;
-    int mm = a_ok[i] ? m : 0;
-    int q = mm % a.Q;
-    int t = mm / a.Q;
-    int p = t % a.P;
-    int nb = t / a.P;
-    a_base[i] = nb * a.in_sn;
-    a_ih[i] = p * a.sh - a.ph;
+    const int m = m0 + row0 + 16 * i;
+    const int q = m % a.Q;
+    const int t = m / a.Q;
+    a_base[i] = (t / a.P) * a.in_sn;
+    a_ih[i] = m < a.M ? (t % a.P) * a.sh - a.ph : -(1 << 28);
     a_iw[i] = q * a.sw - a.pw;
   }
 
-  // instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = 128
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                         ((uint32_t)(TC_BM >> 4) << 24);
-
-  float4 ra[A_ROWS], rb[B_ROWS];
-  auto gather = [&](int kt) {
-    const int k = kt * TC_BK + chunk * 4;
+  // cp.async of K tile `kt` (slice-relative) into stage `st`: A raw → A_hi slot,
+  // W_hi / W_lo → B slots
+  auto issue = [&](int kt, int st) {
+    const uint32_t stage = sbase + st * L::STAGE;
+    const int k = (kt0 + kt) * TC_BK + chunk * 4;
     if (a.vec) {
-      // 4 consecutive k share (r, s) because C % 4 == 0
       const bool kin = k < a.Kdim;
-      int c = 0, r = 0, s = 0;
-      if (kin) {
-        c = k % a.C;
-        int rs = k / a.C;
-        s = rs % a.S;
-        r = rs / a.S;
-      }
+      const int c = k % a.C;
+      const int rs = k / a.C;
+      const int s = rs % a.S, r = rs / a.S;
 #pragma unroll
       for (int i = 0; i < A_ROWS; ++i) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        int ih = a_ih[i] + r, iw = a_iw[i] + s;
-        if (kin && a_ok[i] && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W) {
-          v = __ldg(reinterpret_cast<const float4*>(a.in + a_base[i] + ih * a.in_sh + iw * a.in_sw + c));
-          if (a.pre_relu) {
-            v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
-          }
-        }
-        ra[i] = v;
-      }
-#pragma unroll
-      for (int i = 0; i < B_ROWS; ++i) {
-        int n = n0 + row0 + 16 * i;
-        rb[i] = (kin && n < a.K) ? __ldg(reinterpret_cast<const float4*>(a.w + (int64_t)n * a.Kdim + k))
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int rr = row0 + 16 * i;
+        const int ih = a_ih[i] + r, iw = a_iw[i] + s;
+        const bool ok = kin && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
+        cp16(stage + chunk * (TC_BM * 16) + (rr >> 3) * 128 + (rr & 7) * 16,
+             a.in + (ok ? a_base[i] + ih * a.in_sh + iw * a.in_sw + c : 0), ok);
       }
     } else {
-      // generic strides / C % 4 != 0 (first layer): rolled to keep code small
 #pragma unroll 1
       for (int i = 0; i < A_ROWS; ++i) {
-        float e[4];
+        const int rr = row0 + 16 * i;
 #pragma unroll 1
         for (int j = 0; j < 4; ++j) {
           const int kk = k + j;
           const int c = kk % a.C;
           const int rs = kk / a.C;
           const int ih = a_ih[i] + rs / a.S, iw = a_iw[i] + rs % a.S;
-          const bool ok = kk < a.Kdim && a_ok[i] && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
-          float v = __ldg(a.in + (ok ? a_base[i] + ih * a.in_sh + iw * a.in_sw + c * a.in_sc : 0));
-          if (a.pre_relu) v = fmaxf(v, 0.f);
-          e[j] = ok ? v : 0.f;
+          const bool ok = kk < a.Kdim && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
+          cp4(stage + chunk * (TC_BM * 16) + (rr >> 3) * 128 + (rr & 7) * 16 + 4 * j,
+              a.in + (ok ? a_base[i] + ih * a.in_sh + iw * a.in_sw + c * a.in_sc : 0), ok);
         }
-        ra[i] = make_float4(e[0], e[1], e[2], e[3]);
-      }
-#pragma unroll 1
-      for (int i = 0; i < B_ROWS; ++i) {
-        const int n = n0 + row0 + 16 * i;
-        float e[4];
-#pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
-          const int kk = k + j;
-          const bool ok = kk < a.Kdim && n < a.K;
-          const float v = __ldg(a.w + (ok ? (int64_t)n * a.Kdim + kk : 0));
-          e[j] = ok ? v : 0.f;
-        }
-        rb[i] = make_float4(e[0], e[1], e[2], e[3]);
       }
     }
-  };
-  // canonical offsets: chunk j of row r at j*(ROWS*16) + (r/8)*128 + (r%8)*16
-  auto deposit = [&](int stage) {
-    uint8_t* st = smem + stage * L::STAGE;
-    uint8_t* a_hi = st;
-    uint8_t* a_lo = st + L::A_BYTES;
-    uint8_t* b_hi = st + 2 * L::A_BYTES;
-    uint8_t* b_lo = b_hi + L::B_BYTES;
-#pragma unroll
-    for (int i = 0; i < A_ROWS; ++i) {
-      int r = row0 + 16 * i;
-      uint32_t off = chunk * (TC_BM * 16) + (r >> 3) * 128 + (r & 7) * 16;
-      store_split(a_hi, a_lo, off, ra[i]);
-    }
+    const uint32_t b_hi = stage + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
 #pragma unroll
     for (int i = 0; i < B_ROWS; ++i) {
-      int r = row0 + 16 * i;
-      uint32_t off = chunk * (BN * 16) + (r >> 3) * 128 + (r & 7) * 16;
-      store_split(b_hi, b_lo, off, rb[i]);
+      const int rr = row0 + 16 * i;
+      const int n = n0 + rr;
+      const bool ok = n < a.K;
+      const size_t off = ok ? (size_t)n * a.Kpad + k : 0;
+      const uint32_t d = chunk * (BN * 16) + (rr >> 3) * 128 + (rr & 7) * 16;
+      cp16(b_hi + d, a.w_hi + off, ok);
+      cp16(b_lo + d, a.w_lo + off, ok);
     }
   };
 
+  // instruction descriptor: D f32, A/B tf32, both K-major, N = BN, M = 128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                         ((uint32_t)(TC_BM >> 4) << 24);
+
+  pdl_trigger();
+  pdl_wait();
+#pragma unroll 1
+  for (int st = 0; st < S; ++st) {
+    if (st < iters) issue(st, st);
+    cp_commit();
+  }
+#pragma unroll 1
   for (int it = 0; it < iters; ++it) {
-    const int stage = it & 1;
-    gather(kt0 + it);
-    if (it >= 2) mbar_wait(smem_u32(&mbar[stage]), ((it - 2) >> 1) & 1);
-    deposit(stage);
+    const int st = it % S;
+    cp_wait<S - 1>();
+    __syncthreads();
+    // split the activation tile: hi = tf32(x) in place, lo = x - hi beside it
+    {
+      float4* hi = reinterpret_cast<float4*>(smem + st * L::STAGE);
+      float4* lo = reinterpret_cast<float4*>(smem + st * L::STAGE + L::A_BYTES);
+#pragma unroll 2
+      for (int i = tid; i < L::A_BYTES / 16; i += TC_THREADS) {
+        float4 x = hi[i];
+        if (a.pre_relu) {
+          x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+        }
+        const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+        hi[i] = h;
+        lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      }
+    }
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      const uint32_t st = smem_u32(smem + stage * L::STAGE);
-      const uint32_t a_hi = st, a_lo = st + L::A_BYTES;
-      const uint32_t b_hi = st + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
+      const uint32_t a_hi = sbase + st * L::STAGE, a_lo = a_hi + L::A_BYTES;
+      const uint32_t b_hi = a_hi + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
       constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
 #pragma unroll
       for (int ks = 0; ks < TC_BK / 8; ++ks) {
@@ -317,22 +291,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
         mma_tf32(tmem, ah, bl, idesc, 1u);
         mma_tf32(tmem, al, bh, idesc, 1u);
       }
-      mma_commit(smem_u32(&mbar[stage]));
+      mma_commit(smem_u32(&mbar[st]));
     }
+    if (it + S < iters) {  // refill this stage once the tensor core has consumed it
+      mbar_wait(smem_u32(&mbar[st]), (it / S) & 1);
+      issue(it + S, st);
+    }
+    cp_commit();
   }
   if (iters > 0) {
     const int last = iters - 1;
-    mbar_wait(smem_u32(&mbar[last & 1]), (last >> 1) & 1);
+    mbar_wait(smem_u32(&mbar[last % S]), (last / S) & 1);
   }
   tc_fence_after();
 
-  const int row = warp * 32 + lane;  // TMEM lane == tile row
-  const int m = m0 + row;
-  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
-
   // TMEM → smem tile (rows = TMEM lanes) → one rolled epilogue loop, shared
-  // with the split-K DSMEM reduction; keeps the kernel's code footprint small
-  float* part = reinterpret_cast<float*>(smem);  // [128][BN]; operand smem is free now
+  // with the split-K DSMEM reduction
+  const int row = warp * 32 + lane;
+  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  float* part = reinterpret_cast<float*>(smem);  // [128][BN]; operands are dead now
   __syncthreads();
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -347,7 +324,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     for (int j = 0; j < 16; j += 4)
       *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
-  (void)m;
   int e0 = 0, e1 = TC_BM * BN, nr = 1;
   cg::cluster_group cluster = cg::this_cluster();
   if (a.split > 1) {
@@ -386,7 +362,8 @@ static TcArgs tc_args(const sw_op_desc& op) {
   TcArgs a;
   a.in = reinterpret_cast<const float*>(op.ptrs[PT_IN]);
   a.out = reinterpret_cast<float*>(op.ptrs[PT_OUT]);
-  a.w = reinterpret_cast<const float*>(op.ptrs[PT_W]);
+  a.w_hi = reinterpret_cast<const float*>(op.ptrs[PT_W_TC_HI]);
+  a.w_lo = reinterpret_cast<const float*>(op.ptrs[PT_W_TC_LO]);
   a.bias = reinterpret_cast<const float*>(op.ptrs[PT_BIAS]);
   a.res = reinterpret_cast<const float*>(op.ptrs[PT_RES]);
   a.N = (int)p[SP_N]; a.H = (int)p[SP_H]; a.W = (int)p[SP_W]; a.C = (int)p[SP_C];
@@ -395,31 +372,18 @@ static TcArgs tc_args(const sw_op_desc& op) {
   a.sh = (int)p[SP_STRIDE_H]; a.sw = (int)p[SP_STRIDE_W];
   a.ph = (int)p[SP_PAD_H]; a.pw = (int)p[SP_PAD_W];
   a.act = (int)p[SP_ACT]; a.pre_relu = (int)p[SP_PRE_RELU]; a.has_res = (int)p[SP_HAS_RES];
-  a.in_sn = p[SP_IN_SN]; a.in_sh = p[SP_IN_SH]; a.in_sw = p[SP_IN_SW]; a.in_sc = p[SP_IN_SC];
+  a.in_sn = (int)p[SP_IN_SN]; a.in_sh = (int)p[SP_IN_SH]; a.in_sw = (int)p[SP_IN_SW]; a.in_sc = (int)p[SP_IN_SC];
   a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
   a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
   a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
   a.res_sc = p[SP_RES_SC] ? p[SP_RES_SC] : 1;
   a.M = a.N * a.P * a.Q;
   a.Kdim = a.R * a.S * a.C;
+  a.Kpad = (int)p[SP_KPAD];
   a.split = p[SP_SPLIT_K] > 1 ? (int)p[SP_SPLIT_K] : 1;
-  const bool aligned = ((op.ptrs[PT_IN] & 15) == 0) && ((op.ptrs[PT_W] & 15) == 0);
   a.vec = (a.C % 4 == 0) && a.in_sc == 1 && (a.in_sn % 4 == 0) && (a.in_sh % 4 == 0) && (a.in_sw % 4 == 0) &&
-          aligned;
+          ((op.ptrs[PT_IN] & 15) == 0);
   return a;
-}
-
-template <int BN>
-static int launch_tc(const TcArgs& a, cudaStream_t st) {
-  using L = TcSmem<BN>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return (int)e;
-    configured = true;
-  }
-  dim3 grid((unsigned)cdiv(a.M, TC_BM), (unsigned)cdiv(a.K, BN), (unsigned)a.split);
-  return (int)launch_k(conv_tc_kernel<BN>, grid, dim3(TC_THREADS), (size_t)L::TOTAL, st, (unsigned)a.split, a);
 }
 
 // variant = N tile (32, 64, 128, 256); SP_SPLIT_K = cluster split along K.
@@ -427,12 +391,27 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
   TcArgs a = tc_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a.M == 0 || a.K == 0) return 0;
+  if (!a.w_hi || !a.w_lo || a.Kpad < a.Kdim || a.Kpad % TC_BK) return (int)cudaErrorInvalidValue;
+  dim3 grid((unsigned)cdiv(a.M, TC_BM), 1, (unsigned)a.split);
   switch (op.variant) {
-    case 32: return launch_tc<32>(a, st);
-    case 64: return launch_tc<64>(a, st);
-    case 128: return launch_tc<128>(a, st);
-    case 256: return launch_tc<256>(a, st);
-    default: return (int)cudaErrorInvalidValue;
+    case 32:
+      grid.y = (unsigned)cdiv(a.K, 32);
+      return (int)launch_k(conv_tc_kernel<32>, grid, dim3(TC_THREADS), (size_t)TcSmem<32>::TOTAL, st,
+                           (unsigned)a.split, a);
+    case 64:
+      grid.y = (unsigned)cdiv(a.K, 64);
+      return (int)launch_k(conv_tc_kernel<64>, grid, dim3(TC_THREADS), (size_t)TcSmem<64>::TOTAL, st,
+                           (unsigned)a.split, a);
+    case 128:
+      grid.y = (unsigned)cdiv(a.K, 128);
+      return (int)launch_k(conv_tc_kernel<128>, grid, dim3(TC_THREADS), (size_t)TcSmem<128>::TOTAL, st,
+                           (unsigned)a.split, a);
+    case 256:
+      grid.y = (unsigned)cdiv(a.K, 256);
+      return (int)launch_k(conv_tc_kernel<256>, grid, dim3(TC_THREADS), (size_t)TcSmem<256>::TOTAL, st,
+                           (unsigned)a.split, a);
+    default:
+      return (int)cudaErrorInvalidValue;
   }
 }
 

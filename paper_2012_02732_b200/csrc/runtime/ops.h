@@ -45,10 +45,12 @@ enum SpatialParam : int {
   SP_PAD_BOTTOM, SP_PAD_RIGHT,         // avg count_include_pad window clamp
   SP_SPLIT_K,                          // K_CONV: split-K cluster size (1 = none)
   SP_OUT_SC,                           // output channel stride (1 = NHWC, H*W = NCHW output)
-  SP_RES_SC                            // residual channel stride (0 → 1)
+  SP_RES_SC,                           // residual channel stride (0 → 1)
+  SP_KPAD                              // K_CONV_TC: row stride of the pre-split weights
 };
-// ptrs: 0 in, 1 out, 2 weight, 3 bias, 4 residual, 5 workspace
-enum SpatialPtr : int { PT_IN = 0, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS };
+// ptrs: 0 in, 1 out, 2 weight [K][R][S][C], 3 bias, 4 residual, 5 workspace,
+// 6/7 tcgen05 weights pre-split into TF32 hi / lo, [K][Kpad]
+enum SpatialPtr : int { PT_IN = 0, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS, PT_W_TC_HI, PT_W_TC_LO };
 
 // K_ELTWISE / K_GLOBAL_POOL params
 enum EwParam : int {

@@ -44,8 +44,9 @@ EW_ADD, EW_MUL, EW_AFFINE, EW_COPY = 0, 1, 2, 3
 (SP_N, SP_H, SP_W, SP_C, SP_P, SP_Q, SP_K, SP_R, SP_S, SP_STRIDE_H, SP_STRIDE_W, SP_PAD_H,
  SP_PAD_W, SP_ACT, SP_PRE_RELU, SP_IN_SN, SP_IN_SH, SP_IN_SW, SP_IN_SC, SP_OUT_SN, SP_OUT_SH,
  SP_OUT_SW, SP_RES_SN, SP_RES_SH, SP_RES_SW, SP_HAS_RES, SP_POOL_MODE, SP_COUNT_PAD,
- SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC) = range(33)
-PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS = range(6)
+ SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC, SP_KPAD) = range(34)
+PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS, PT_W_TC_HI, PT_W_TC_LO = range(8)
+TC_BK = 32  # K tile of the tcgen05 conv; its pre-split weights are padded to a multiple
 (EW_N, EW_H, EW_W, EW_C, EW_OP, EW_ACT, EW_A_SN, EW_A_SH, EW_A_SW, EW_A_SC, EW_B_SN, EW_B_SH,
  EW_B_SW, EW_B_SC, EW_C_SN, EW_C_SH, EW_C_SW, EW_C_SC, EW_O_SN, EW_O_SH, EW_O_SW, EW_O_SC,
  EW_NIN, EW_PRE_RELU) = range(24)
@@ -144,6 +145,15 @@ def _pack_weights(prog: Program):
         if t.kind == "conv":
             w = n.attrs["weight"].float().permute(0, 2, 3, 1).contiguous()  # [K][R][S][C]
             arrays[(t.tid, "w")] = w.numpy().reshape(-1)
+            # tcgen05 operand: 3xTF32 pre-split, K padded to the 32-wide K tile
+            k_out = w.shape[0]
+            kdim = w[0].numel()
+            kpad = (kdim + TC_BK - 1) // TC_BK * TC_BK
+            wp = np.zeros((k_out, kpad), dtype=np.float32)
+            wp[:, :kdim] = w.numpy().reshape(k_out, kdim)
+            hi = (wp.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+            arrays[(t.tid, "w_tc_hi")] = hi.reshape(-1)
+            arrays[(t.tid, "w_tc_lo")] = (wp - hi).astype(np.float32).reshape(-1)
             if n.attrs["bias"] is not None:
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
         elif t.kind == "dwconv":
@@ -207,8 +217,11 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 d.kind = K_CONV
                 q[PT_W] = wptr("w")
                 q[PT_BIAS] = wptr("b")
+                q[PT_W_TC_HI] = wptr("w_tc_hi")
+                q[PT_W_TC_LO] = wptr("w_tc_lo")
                 M = nb * P * Q
                 Kdim = R * S * c
+                vals[SP_KPAD] = (Kdim + TC_BK - 1) // TC_BK * TC_BK
                 if conv_impl == "tc":
                     d.kind = K_CONV_TC
                     variant, split = pick_conv_tc(M, oc, Kdim)
