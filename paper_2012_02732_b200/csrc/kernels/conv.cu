@@ -76,24 +76,23 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// BM x BN output tile, 4x4 micro-tile per thread, BK = 16, STAGES-deep
-// cp.async (LDGSTS) pipeline: the im2col gather of STAGES-1 future K tiles is
-// in flight while the current tile is multiplied, so a layer costs about one
-// memory round trip instead of one per K tile (batch-1 layers are latency-,
-// not FLOP-bound).  Out-of-range taps are zero-filled by cp.async itself.
-template <int BM, int BN, bool PRE>
-__global__ void __launch_bounds__((BM / 4) * (BN / 4))
+// BM x BN output tile computed by 256 threads with a TM x TN micro-tile each,
+// BK = 16, 4-stage cp.async (LDGSTS) pipeline.  Batch-1 layers are tiny, so
+// the variants are "wide and shallow": 8 warps per CTA and as little serial
+// work per warp as possible (ncu: a 2-warp CTA spent 4.4K dependent
+// instructions per warp at IPC 0.26).  Out-of-range taps are zero-filled by
+// cp.async; the epilogue is one smem-staged rolled loop shared with the
+// split-K DSMEM reduction, keeping the code an SM must fetch small.
+template <int BM, int BN, int TM, int TN, bool PRE>
+__global__ void __launch_bounds__(256)
 conv_simt_kernel(ConvArgs a) {
-  // Code size matters as much as FLOPs here: at batch 1 every CTA starts on
-  // a cold SM, so loops outside the FMA micro-kernel stay rolled and the
-  // epilogue is one smem-staged loop shared with the split-K reduction.
   constexpr int BK = 16;
   constexpr int STAGES = 4;
-  constexpr int NT = (BM / 4) * (BN / 4);
-  constexpr int A_PER = BM * BK / NT;
-  constexpr int B_PER = BN * BK / NT;
+  constexpr int NT = 256;
+  static_assert((BM / TM) * (BN / TN) == NT, "256 threads per CTA");
+  constexpr int A_PER = (BM * BK + NT - 1) / NT;
+  constexpr int B_PER = (BN * BK + NT - 1) / NT;
   constexpr int PAD = 4;
-  static_assert(NT % BK == 0, "kk must be fixed per thread");
   extern __shared__ __align__(16) float smem[];
   float* As = smem;                                // [STAGES][BK][BM+PAD]
   float* Bs = smem + STAGES * BK * (BM + PAD);     // [STAGES][BK][BN+PAD]
@@ -102,30 +101,26 @@ conv_simt_kernel(ConvArgs a) {
   const int m0 = blockIdx.x * BM;
   const int n0 = blockIdx.y * BN;
   const int kk = tid % BK;
-  const int row = tid / BK;  // + i * (NT / BK)
+  const int row = tid / BK;  // 0..15, + i * 16
 
-  // K range of this split (cluster rank == blockIdx.z)
   const int ksteps_total = (a.Kdim + BK - 1) / BK;
   const int per = (ksteps_total + a.split - 1) / a.split;
   const int ks_begin = blockIdx.z * per;
   const int nsteps = max(0, min(ksteps_total, ks_begin + per) - ks_begin);
 
-  // per-thread pixel decode for the A loads (fixed across K)
   int a_base[A_PER], a_ih[A_PER], a_iw[A_PER];
 #pragma unroll
   for (int i = 0; i < A_PER; ++i) {
-    int m = m0 + row + i * (NT / BK);
-    int q = m % a.Q;
-    int t = m / a.Q;
-    int p = t % a.P;
-    int nb = t / a.P;
-    a_base[i] = nb * (int)a.in_sn;
-    a_ih[i] = m < a.M ? p * a.sh - a.ph : -(1 << 28);  // out-of-range row: never valid
+    const int mm = row + i * 16;
+    const int m = m0 + mm;
+    const int q = m % a.Q;
+    const int t = m / a.Q;
+    a_base[i] = (t / a.P) * (int)a.in_sn;
+    a_ih[i] = (m < a.M && mm < BM) ? (t % a.P) * a.sh - a.ph : -(1 << 28);
     a_iw[i] = q * a.sw - a.pw;
   }
   const int in_sh = (int)a.in_sh, in_sw = (int)a.in_sw, in_sc = (int)a.in_sc;
 
-  // cp.async gather of K tile `kstep` into pipeline buffer `buf`
   auto issue = [&](int kstep, int buf) {
     const int k = kstep * BK + kk;
     const bool kin = k < a.Kdim;
@@ -137,26 +132,27 @@ conv_simt_kernel(ConvArgs a) {
     float* bs = Bs + (buf * BK + kk) * (BN + PAD) + row;
 #pragma unroll
     for (int i = 0; i < A_PER; ++i) {
+      if (row + i * 16 >= BM) break;
       const int ih = a_ih[i] + r, iw = a_iw[i] + s;
       const bool ok = kin && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
-      const float* src = a.in + (ok ? a_base[i] + ih * in_sh + iw * in_sw + c * in_sc : 0);
-      cp_async4(as + i * (NT / BK), src, ok);
+      cp_async4(as + i * 16, a.in + (ok ? a_base[i] + ih * in_sh + iw * in_sw + c * in_sc : 0), ok);
     }
 #pragma unroll
     for (int i = 0; i < B_PER; ++i) {
-      const int n = n0 + row + i * (NT / BK);
+      if (row + i * 16 >= BN) break;
+      const int n = n0 + row + i * 16;
       const bool ok = kin && n < a.K;
-      cp_async4(bs + i * (NT / BK), a.w + (ok ? (size_t)n * a.Kdim + k : 0), ok);
+      cp_async4(bs + i * 16, a.w + (ok ? (size_t)n * a.Kdim + k : 0), ok);
     }
   };
 
-  const int ty = tid / (BN / 4);
-  const int tx = tid % (BN / 4);
-  float acc[4][4];
+  const int ty = tid / (BN / TN);
+  const int tx = tid % (BN / TN);
+  float acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
   pdl_trigger();
   pdl_wait();
@@ -172,33 +168,29 @@ conv_simt_kernel(ConvArgs a) {
     const int nxt = it + STAGES - 1;
     if (nxt < nsteps) issue(ks_begin + nxt, nxt % STAGES);
     cp_async_commit();
-    const float* at = As + (it % STAGES) * BK * (BM + PAD) + ty * 4;
-    const float* bt = Bs + (it % STAGES) * BK * (BN + PAD) + tx * 4;
+    const float* at = As + (it % STAGES) * BK * (BM + PAD) + ty * TM;
+    const float* bt = Bs + (it % STAGES) * BK * (BN + PAD) + tx * TN;
 #pragma unroll 4
     for (int k2 = 0; k2 < BK; ++k2) {
-      float4 av = *reinterpret_cast<const float4*>(at + k2 * (BM + PAD));
-      float4 bv = *reinterpret_cast<const float4*>(bt + k2 * (BN + PAD));
-      if (PRE) {
-        av.x = fmaxf(av.x, 0.f); av.y = fmaxf(av.y, 0.f); av.z = fmaxf(av.z, 0.f); av.w = fmaxf(av.w, 0.f);
-      }
-      const float ai[4] = {av.x, av.y, av.z, av.w};
-      const float bj[4] = {bv.x, bv.y, bv.z, bv.w};
+      float ai[TM], bj[TN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i) ai[i] = PRE ? fmaxf(at[k2 * (BM + PAD) + i], 0.f) : at[k2 * (BM + PAD) + i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ai[i], bj[j], acc[i][j]);
+      for (int j = 0; j < TN; ++j) bj[j] = bt[k2 * (BN + PAD) + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(ai[i], bj[j], acc[i][j]);
     }
   }
   cp_async_wait<0>();
   __syncthreads();
 
-  // stage the tile in smem (reusing the operand buffers), then one rolled
-  // epilogue loop; split-K ranks of a cluster reduce through DSMEM first
-  float* part = smem;  // [BM][BN]
+  float* part = smem;  // [BM][BN], reuses the operand buffers
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    *reinterpret_cast<float4*>(&part[(ty * 4 + i) * BN + tx * 4]) =
-        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) part[(ty * TM + i) * BN + tx * TN + j] = acc[i][j];
   int e_begin = 0, e_end = BM * BN, nranks = 1;
   cg::cluster_group cluster = cg::this_cluster();
   if (a.split > 1) {
@@ -224,7 +216,6 @@ conv_simt_kernel(ConvArgs a) {
   }
   if (a.split > 1) cluster.sync();
 }
-
 
 // Small-M 1x1 conv / linear (batch-1 classifier heads, 1x1-spatial layers):
 // one warp per output channel streams its weight row once with 128-bit loads.
@@ -292,6 +283,27 @@ __global__ void __launch_bounds__(256) conv_gemv_kernel(ConvArgs a) {
   }
 }
 
+struct SimtCfg {
+  int bm, bn;
+  void (*fn[2])(ConvArgs);
+};
+
+#define SW_SIMT_CFG(BM, BN, TM, TN) \
+  { BM, BN, { conv_simt_kernel<BM, BN, TM, TN, false>, conv_simt_kernel<BM, BN, TM, TN, true> } }
+
+// variant → tile; all 256 threads.  8 = GEMV (M <= 8, 1x1).
+static const SimtCfg kSimt[] = {
+    SW_SIMT_CFG(64, 64, 4, 4),   // 0
+    SW_SIMT_CFG(32, 64, 2, 4),   // 1
+    SW_SIMT_CFG(32, 32, 2, 2),   // 2
+    SW_SIMT_CFG(128, 64, 8, 4),  // 3
+    SW_SIMT_CFG(16, 32, 1, 2),   // 4
+    SW_SIMT_CFG(16, 64, 1, 4),   // 5
+    SW_SIMT_CFG(16, 16, 1, 1),   // 6
+    SW_SIMT_CFG(64, 32, 4, 2),   // 7
+};
+constexpr int kNumSimt = sizeof(kSimt) / sizeof(kSimt[0]);
+
 static size_t simt_smem_bytes(int bm, int bn) {
   const size_t tile = 4 * 16 * (size_t)(bm + 4) + 4 * 16 * (size_t)(bn + 4);  // STAGES * BK * (B? + PAD)
   const size_t part = (size_t)bm * bn;
@@ -299,19 +311,12 @@ static size_t simt_smem_bytes(int bm, int bn) {
 }
 
 void init_simt_kernels() {
-  const int cfgs[4][2] = {{64, 64}, {32, 64}, {32, 32}, {128, 64}};
-  void (*fns[4][2])(ConvArgs) = {
-      {conv_simt_kernel<64, 64, false>, conv_simt_kernel<64, 64, true>},
-      {conv_simt_kernel<32, 64, false>, conv_simt_kernel<32, 64, true>},
-      {conv_simt_kernel<32, 32, false>, conv_simt_kernel<32, 32, true>},
-      {conv_simt_kernel<128, 64, false>, conv_simt_kernel<128, 64, true>}};
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < kNumSimt; ++i)
     for (int j = 0; j < 2; ++j)
-      cudaFuncSetAttribute(fns[i][j], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)simt_smem_bytes(cfgs[i][0], cfgs[i][1]));
+      cudaFuncSetAttribute(kSimt[i].fn[j], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)simt_smem_bytes(kSimt[i].bm, kSimt[i].bn));
 }
 
-// variant: 0 = 64x64, 1 = 32x64, 2 = 32x32, 3 = 128x64, 8 = gemv (M <= 8, 1x1)
 int launch_conv(const sw_op_desc& op, void* stream) {
   ConvArgs a = conv_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -321,25 +326,11 @@ int launch_conv(const sw_op_desc& op, void* stream) {
     int blocks = (int)cdiv((int64_t)a.K * 32, 256);
     return (int)launch_k(conv_gemv_kernel<8>, dim3(blocks), dim3(256), 0, st, 1, a);
   }
-  int bm = 64, bn = 64;
-  switch (op.variant) {
-    case 1: bm = 32; bn = 64; break;
-    case 2: bm = 32; bn = 32; break;
-    case 3: bm = 128; bn = 64; break;
-    default: break;
-  }
-  dim3 grid((unsigned)cdiv(a.M, bm), (unsigned)cdiv(a.K, bn), (unsigned)a.split);
-  int threads = (bm / 4) * (bn / 4);
-  void (*fn)(ConvArgs) = nullptr;
-  const bool pre = a.pre_relu != 0;
-  switch (op.variant) {
-    case 1: fn = pre ? conv_simt_kernel<32, 64, true> : conv_simt_kernel<32, 64, false>; break;
-    case 2: fn = pre ? conv_simt_kernel<32, 32, true> : conv_simt_kernel<32, 32, false>; break;
-    case 3: fn = pre ? conv_simt_kernel<128, 64, true> : conv_simt_kernel<128, 64, false>; break;
-    default: fn = pre ? conv_simt_kernel<64, 64, true> : conv_simt_kernel<64, 64, false>; break;
-  }
-  const size_t smem = simt_smem_bytes(bm, bn);
-  return (int)launch_k(fn, grid, dim3(threads), smem, st, (unsigned)a.split, a);
+  if (op.variant < 0 || op.variant >= kNumSimt) return (int)cudaErrorInvalidValue;
+  const SimtCfg& c = kSimt[op.variant];
+  dim3 grid((unsigned)cdiv(a.M, c.bm), (unsigned)cdiv(a.K, c.bn), (unsigned)a.split);
+  return (int)launch_k(c.fn[a.pre_relu ? 1 : 0], grid, dim3(256), simt_smem_bytes(c.bm, c.bn), st,
+                       (unsigned)a.split, a);
 }
 
 }  // namespace sw

@@ -21,6 +21,7 @@ enum KernelKind : int32_t {
   K_GLOBAL_POOL = 5, // global average pool over H x W
   K_CONV_TC = 6,     // dense conv / GEMM on tcgen05 tensor cores (3xTF32)
   K_CONCAT = 7,      // unfused channel concat of up to 7 dense NHWC inputs
+  K_SEPCONV = 8,     // fused depthwise k x k → pointwise 1x1
 };
 // K_CONCAT params: 0 N, 1 H, 2 W, 3 n_in, 4 C_total, 5 out channel stride,
 // 6 out pixel stride, 8.. C_i; ptrs 0..6 inputs, 7 output.
@@ -46,8 +47,13 @@ enum SpatialParam : int {
   SP_SPLIT_K,                          // K_CONV: split-K cluster size (1 = none)
   SP_OUT_SC,                           // output channel stride (1 = NHWC, H*W = NCHW output)
   SP_RES_SC,                           // residual channel stride (0 → 1)
-  SP_KPAD                              // K_CONV_TC: row stride of the pre-split weights
+  SP_KPAD,                             // K_CONV_TC: row stride of the pre-split weights
+  SP_DW_ACT                            // K_SEPCONV: activation between depthwise and pointwise
 };
+// K_SEPCONV: PT_W / PT_BIAS = pointwise [K][C] / [K]; PT_WS = depthwise
+// weights [R][S][C]; PT_DW_BIAS = depthwise bias [C]; spatial params describe
+// the depthwise geometry, SP_K the pointwise output channels.
+constexpr int PT_DW_BIAS = 6;
 // ptrs: 0 in, 1 out, 2 weight [K][R][S][C], 3 bias, 4 residual, 5 workspace,
 // 6/7 tcgen05 weights pre-split into TF32 hi / lo, [K][Kpad]
 enum SpatialPtr : int { PT_IN = 0, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS, PT_W_TC_HI, PT_W_TC_LO };
@@ -75,5 +81,7 @@ int launch_global_pool(const sw_op_desc& op, void* stream);
 int launch_concat(const sw_op_desc& op, void* stream);
 void init_tc_kernels();
 void init_simt_kernels();
+int launch_sepconv(const sw_op_desc& op, void* stream);
+void init_sep_kernels();
 
 }  // namespace sw

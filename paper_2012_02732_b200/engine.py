@@ -44,8 +44,10 @@ EW_ADD, EW_MUL, EW_AFFINE, EW_COPY = 0, 1, 2, 3
 (SP_N, SP_H, SP_W, SP_C, SP_P, SP_Q, SP_K, SP_R, SP_S, SP_STRIDE_H, SP_STRIDE_W, SP_PAD_H,
  SP_PAD_W, SP_ACT, SP_PRE_RELU, SP_IN_SN, SP_IN_SH, SP_IN_SW, SP_IN_SC, SP_OUT_SN, SP_OUT_SH,
  SP_OUT_SW, SP_RES_SN, SP_RES_SH, SP_RES_SW, SP_HAS_RES, SP_POOL_MODE, SP_COUNT_PAD,
- SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC, SP_KPAD) = range(34)
+ SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC, SP_KPAD, SP_DW_ACT) = range(35)
 PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS, PT_W_TC_HI, PT_W_TC_LO = range(8)
+PT_DW_BIAS = 6  # K_SEPCONV
+K_SEPCONV = 8
 TC_BK = 32  # K tile of the tcgen05 conv; its pre-split weights are padded to a multiple
 (EW_N, EW_H, EW_W, EW_C, EW_OP, EW_ACT, EW_A_SN, EW_A_SH, EW_A_SW, EW_A_SC, EW_B_SN, EW_B_SH,
  EW_B_SW, EW_B_SC, EW_C_SN, EW_C_SH, EW_C_SW, EW_C_SC, EW_O_SN, EW_O_SH, EW_O_SW, EW_O_SC,
@@ -64,15 +66,23 @@ def pick_conv_variant(M: int, K: int, Kdim: int, R: int, S: int, pad, stride) ->
     """(variant, split_k) for the SIMT implicit-GEMM conv (csrc/kernels/conv.cu)."""
     if M <= 8 and R == 1 and S == 1 and tuple(pad) == (0, 0):
         return 8, 1
-    for v, bm, bn in ((3, 128, 64), (0, 64, 64), (1, 32, 64)):
+    for v in (3, 0, 1, 2):
+        bm, bn = SIMT_TILES[v]
         if math.ceil(M / bm) * math.ceil(K / bn) >= NUM_SMS:
             return v, 1
-    ctas = math.ceil(M / 32) * math.ceil(K / 32)
+    v = 4 if M < 64 else 2
+    bm, bn = SIMT_TILES[v]
+    ctas = math.ceil(M / bm) * math.ceil(K / bn)
     ksteps = math.ceil(Kdim / 16)
     split = 1
     while split < 8 and ctas * split * 2 <= 2 * NUM_SMS and ksteps // (split * 2) >= 4:
         split *= 2
-    return 2, split
+    return v, split
+
+
+# csrc/kernels/conv.cu kSimt[]: variant → (BM, BN); every variant runs 256 threads
+SIMT_TILES = {0: (64, 64), 1: (32, 64), 2: (32, 32), 3: (128, 64), 4: (16, 32), 5: (16, 64),
+              6: (16, 16), 7: (64, 32)}
 
 
 def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
@@ -94,12 +104,14 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
     if M <= 8 and R == 1 and S == 1 and tuple(pad) == (0, 0):
         out.append((K_CONV, 8, 1))
     ksteps = math.ceil(Kdim / 16)
-    for v, bm, bn in ((3, 128, 64), (0, 64, 64), (1, 32, 64), (2, 32, 32)):
+    for v, (bm, bn) in SIMT_TILES.items():
         ctas = math.ceil(M / bm) * math.ceil(K / bn)
+        if bm > 2 * max(M, 16) or bn > 2 * max(K, 16):
+            continue  # tile mostly padding
+        if ctas > 16 * NUM_SMS and bm * bn < 2048:
+            continue  # far too many tiny CTAs
         for split in (1, 2, 4, 8):
             if split > 1 and (ksteps // split < 2 or ctas * split > 4 * NUM_SMS):
-                continue
-            if split == 1 and ctas > 64 * NUM_SMS and v == 2:
                 continue
             out.append((K_CONV, v, split))
     ktiles = math.ceil(Kdim / 32)
@@ -161,6 +173,15 @@ def _pack_weights(prog: Program):
             arrays[(t.tid, "w")] = w.numpy().reshape(-1)
             if n.attrs["bias"] is not None:
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
+        elif t.kind == "sepconv":
+            pw = n.attrs["weight"].float().reshape(n.attrs["weight"].shape[0], -1)  # [K][C]
+            arrays[(t.tid, "w")] = pw.contiguous().numpy().reshape(-1)
+            if n.attrs["bias"] is not None:
+                arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
+            dw = n.attrs["dw_weight"].float()[:, 0].permute(1, 2, 0).contiguous()  # [R][S][C]
+            arrays[(t.tid, "dw")] = dw.numpy().reshape(-1)
+            if n.attrs["dw_bias"] is not None:
+                arrays[(t.tid, "dwb")] = n.attrs["dw_bias"].float().numpy().reshape(-1)
         elif t.kind == "affine":
             arrays[(t.tid, "scale")] = n.attrs["scale"].float().numpy().reshape(-1)
             arrays[(t.tid, "shift")] = n.attrs["shift"].float().numpy().reshape(-1)
@@ -176,7 +197,7 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
         p = d.params
         q = d.ptrs
         wptr = lambda key: weight_base + weight_offsets[(t.tid, key)] if (t.tid, key) in weight_offsets else 0  # noqa: E731
-        if t.kind in ("conv", "dwconv", "pool"):
+        if t.kind in ("conv", "dwconv", "pool", "sepconv"):
             n = t.node
             x = t.inputs[0]
             st_in = x.st
@@ -213,6 +234,13 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 d.kind = K_DWCONV
                 q[PT_W] = wptr("w")
                 q[PT_BIAS] = wptr("b")
+            elif t.kind == "sepconv":
+                d.kind = K_SEPCONV
+                q[PT_W] = wptr("w")
+                q[PT_BIAS] = wptr("b")
+                q[PT_WS] = wptr("dw")
+                q[PT_DW_BIAS] = wptr("dwb")
+                vals[SP_DW_ACT] = n.attrs["dw_act"]
             else:
                 d.kind = K_CONV
                 q[PT_W] = wptr("w")
@@ -311,6 +339,12 @@ def task_cost(t: Task) -> tuple[float, float]:
         R, S = t.node.attrs["k"]
         flops = 2.0 * out_elems * R * S
         wbytes = (o.c * R * S + o.c) * 4
+    elif t.kind == "sepconv":
+        R, S = t.node.attrs["k"]
+        c = t.inputs[0].c
+        pix = o.st.n * o.st.h * o.st.w
+        flops = 2.0 * pix * c * R * S + 2.0 * pix * c * o.c
+        wbytes = (c * R * S + c + o.c * c + o.c) * 4
     elif t.kind == "pool":
         R, S = t.node.attrs["k"]
         flops = 1.0 * out_elems * R * S

@@ -411,13 +411,49 @@ def _pre_relu(nodes):
     return keep
 
 
-def optimize(nodes: list[INode]) -> list[INode]:
+def _fuse_separable(nodes):
+    """depthwise → pointwise 1x1 (single consumer) becomes ONE 'sepconv' task.
+
+    NASNet's sep-convs and MobileNetV2's dw → project both have this shape
+    after BN/act folding; the depthwise tile then lives only in shared memory
+    and the graph loses a node (csrc/kernels/sepconv.cu).
+    """
+    users = _users(nodes)
+    drop = set()
+    for n in nodes:
+        if n.kind != "conv" or n.attrs.get("linear"):
+            continue
+        d = n.inputs[0]
+        if d.kind != "dwconv" or len(users[id(d)]) != 1 or d.residual is not None:
+            continue
+        if tuple(n.attrs["k"]) != (1, 1) or tuple(n.attrs["stride"]) != (1, 1) or \
+                tuple(n.attrs["pad"]) != (0, 0):
+            continue
+        dw_act = d.act
+        if n.pre_relu:
+            if dw_act not in (ACT_NONE, ACT_RELU):
+                continue
+            dw_act = ACT_RELU
+        n.attrs = {"weight": n.attrs["weight"], "bias": n.attrs["bias"],
+                   "dw_weight": d.attrs["weight"], "dw_bias": d.attrs["bias"],
+                   "stride": d.attrs["stride"], "pad": d.attrs["pad"], "k": d.attrs["k"],
+                   "dw_act": dw_act}
+        n.kind = "sepconv"
+        n.pre_relu = d.pre_relu
+        n.inputs = [d.inputs[0]]
+        drop.add(id(d))
+    return [n for n in nodes if id(n) not in drop]
+
+
+def optimize(nodes: list[INode], fuse_separable: bool = True) -> list[INode]:
     out_node = nodes[-1]
     nodes = _drop_identities(nodes)
     nodes = _fold_bn(nodes)
     nodes = _fold_residual_adds(nodes)
     nodes = _fold_acts(nodes, out_node)
     nodes = _pre_relu(nodes)
+    if fuse_separable:
+        nodes = _fuse_separable(nodes)
     return nodes
 
 
@@ -629,10 +665,11 @@ def to_compgraph(prog: Program, durations=None) -> CompGraph:
     return g
 
 
-def build_program(model: nn.Module, example: torch.Tensor, fuse: bool = True) -> Program:
+def build_program(model: nn.Module, example: torch.Tensor, fuse: bool = True,
+                  fuse_separable: bool = True) -> Program:
     nodes = trace_model(model, example)
     if fuse:
-        nodes = optimize(nodes)
+        nodes = optimize(nodes, fuse_separable=fuse_separable)
     else:
         nodes = _drop_identities(nodes)
         for n in nodes:

@@ -84,7 +84,7 @@ def _window(x, ph, pw, P, Q, R, S, sh, sw, fill):
 def run_op(mem: HostMemory, d):
     p = list(d.params)
     q = list(d.ptrs)
-    if d.kind in (E.K_CONV, E.K_DWCONV, E.K_POOL):
+    if d.kind in (E.K_CONV, E.K_DWCONV, E.K_POOL, E.K_SEPCONV):
         Nb, H, W, Cc, P, Q, K, R, S = (p[E.SP_N], p[E.SP_H], p[E.SP_W], p[E.SP_C], p[E.SP_P],
                                        p[E.SP_Q], p[E.SP_K], p[E.SP_R], p[E.SP_S])
         sh, sw, ph, pw = p[E.SP_STRIDE_H], p[E.SP_STRIDE_W], p[E.SP_PAD_H], p[E.SP_PAD_W]
@@ -97,6 +97,20 @@ def run_op(mem: HostMemory, d):
             w = w.view(K, R, S, Cc).permute(0, 3, 1, 2)
             xw, _ = _window(x, ph, pw, P, Q, R, S, sh, sw, 0.0)
             y = F.conv2d(xw.double(), w.double(), stride=(sh, sw)).float()
+            if q[E.PT_BIAS]:
+                b = torch.from_numpy(mem.buf[mem.idx(q[E.PT_BIAS]):mem.idx(q[E.PT_BIAS]) + K].copy())
+                y = y + b.view(1, -1, 1, 1)
+        elif d.kind == E.K_SEPCONV:
+            wdw = torch.from_numpy(mem.buf[mem.idx(q[E.PT_WS]):mem.idx(q[E.PT_WS]) + R * S * Cc].copy())
+            wdw = wdw.view(R, S, Cc).permute(2, 0, 1)[:, None]
+            xw, _ = _window(x, ph, pw, P, Q, R, S, sh, sw, 0.0)
+            dwo = F.conv2d(xw.double(), wdw.double(), stride=(sh, sw), groups=Cc)
+            if q[E.PT_DW_BIAS]:
+                bdw = torch.from_numpy(mem.buf[mem.idx(q[E.PT_DW_BIAS]):mem.idx(q[E.PT_DW_BIAS]) + Cc].copy())
+                dwo = dwo + bdw.double().view(1, -1, 1, 1)
+            dwo = _act(dwo.float(), p[E.SP_DW_ACT])
+            wpw = torch.from_numpy(mem.buf[mem.idx(q[E.PT_W]):mem.idx(q[E.PT_W]) + K * Cc].copy()).view(K, Cc)
+            y = F.conv2d(dwo.double(), wpw.double()[:, :, None, None]).float()
             if q[E.PT_BIAS]:
                 b = torch.from_numpy(mem.buf[mem.idx(q[E.PT_BIAS]):mem.idx(q[E.PT_BIAS]) + K].copy())
                 y = y + b.view(1, -1, 1, 1)

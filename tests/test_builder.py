@@ -71,7 +71,7 @@ def test_fusion_shrinks_nasnet(programs):
     assert len(fused.tasks) < 0.5 * len(raw.tasks)
     kinds = fused.stats()
     # BN, ReLU, add and concat tasks all disappear into kernel epilogues/prologues
-    assert set(kinds) <= {"conv", "dwconv", "pool", "gpool", "copy"}
+    assert set(kinds) <= {"conv", "sepconv", "dwconv", "pool", "gpool", "copy"}
     assert kinds.get("copy", 0) == 0
 
 
