@@ -87,7 +87,7 @@ template <int BM, int BN, int TM, int TN, bool PRE>
 __global__ void __launch_bounds__(256)
 conv_simt_kernel(ConvArgs a) {
   constexpr int BK = 16;
-  constexpr int STAGES = 4;
+  constexpr int STAGES = 8;  // deep ring: a batch-1 K slice is in flight at once
   constexpr int NT = 256;
   static_assert((BM / TM) * (BN / TN) == NT, "256 threads per CTA");
   constexpr int A_PER = (BM * BK + NT - 1) / NT;
@@ -202,7 +202,7 @@ conv_simt_kernel(ConvArgs a) {
   } else {
     __syncthreads();
   }
-#pragma unroll 1
+#pragma unroll 4
   for (int e = e_begin + tid; e < e_end; e += NT) {
     const int m = m0 + e / BN, n = n0 + e % BN;
     if (m >= a.M || n >= a.K) continue;
@@ -305,7 +305,7 @@ static const SimtCfg kSimt[] = {
 constexpr int kNumSimt = sizeof(kSimt) / sizeof(kSimt[0]);
 
 static size_t simt_smem_bytes(int bm, int bn) {
-  const size_t tile = 4 * 16 * (size_t)(bm + 4) + 4 * 16 * (size_t)(bn + 4);  // STAGES * BK * (B? + PAD)
+  const size_t tile = 8 * 16 * (size_t)(bm + 4) + 8 * 16 * (size_t)(bn + 4);  // STAGES * BK * (B? + PAD)
   const size_t part = (size_t)bm * bn;
   return 4 * (tile > part ? tile : part);
 }

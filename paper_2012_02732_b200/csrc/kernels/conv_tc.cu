@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   } else {
     __syncthreads();
   }
-#pragma unroll 1
+#pragma unroll 4
   for (int e = e0 + tid; e < e1; e += TC_THREADS) {
     const int mm = m0 + e / BN, nn = n0 + e % BN;
     if (mm >= a.M || nn >= a.K) continue;

@@ -9,8 +9,8 @@
 //   1. cp.async prefetch of the first pointwise-weight chunk;
 //   2. depthwise for all C_in channels of the 16 pixels into smem D[c][px]
 //      (branch-free unrolled taps, 128-bit NHWC loads when C % 4 == 0);
-//   3. pointwise GEMM D^T x W over C_in in 16-channel chunks (cp.async
-//      double-buffered weights), 1x2 micro-tile per thread;
+//   3. pointwise GEMM D^T x W over C_in (all weight chunks requested by
+//      cp.async at kernel start, before the PDL wait), 1x2 micro-tile;
 //   4. smem-staged rolled epilogue (bias, residual, activation, strided store).
 #include "common.cuh"
 
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   extern __shared__ __align__(16) float smem[];
   const int Cp = (a.C + SEP_BK - 1) / SEP_BK * SEP_BK;  // D rows padded to the K chunk
   float* D = smem;                                      // [Cp][SEP_BM]
-  float* Bs = smem + Cp * SEP_BM;                       // [2][SEP_BK][SEP_BN]
+  float* Bs = smem + Cp * SEP_BM;                       // [Cp][SEP_BN]: every weight chunk
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * SEP_BM;
   const int n0 = blockIdx.y * SEP_BN;
@@ -71,7 +71,11 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
     }
     cp_commit();
   };
-  load_b(0, 0);  // weights are constant: prefetch before waiting on the producer
+  // weights are constant: request every chunk before waiting on the producer,
+  // so the whole pointwise operand is one round trip hidden behind the depthwise
+  const int chunks = Cp / SEP_BK;
+#pragma unroll 1
+  for (int ch = 0; ch < chunks; ++ch) load_b(ch, ch);
   pdl_trigger();
   pdl_wait();
 
@@ -143,17 +147,11 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   const int ty = tid / (SEP_BN / 2);  // 0..15 → output row (pixel) ty
   const int tx = tid % (SEP_BN / 2);  // 0..15 → cols tx*2, tx*2+1
   float o0 = 0.f, o1 = 0.f;
-  const int chunks = Cp / SEP_BK;
+  cp_wait<0>();
+  __syncthreads();  // D complete and all weight chunks landed
 #pragma unroll 1
   for (int ch = 0; ch < chunks; ++ch) {
-    if (ch + 1 < chunks) {
-      load_b(ch + 1, (ch + 1) & 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();  // D complete (first pass) and chunk ch landed for everyone
-    const float* bt = Bs + (ch & 1) * SEP_BK * SEP_BN + tx * 2;
+    const float* bt = Bs + ch * SEP_BK * SEP_BN + tx * 2;
     const float* at = D + ch * SEP_BK * SEP_BM + ty;
 #pragma unroll 4
     for (int k = 0; k < SEP_BK; ++k) {
@@ -162,15 +160,15 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
       o0 = fmaf(av, bv.x, o0);
       o1 = fmaf(av, bv.y, o1);
     }
-    __syncthreads();  // buffer (ch & 1) free for chunk ch + 2
   }
+  __syncthreads();
 
   // ---- epilogue (tile through smem, rolled, coalesced along channels) ----
-  float* part = Bs;  // [SEP_BM][SEP_BN] fits in the 2 x 16 x 32 weight buffers
+  float* part = Bs;  // [SEP_BM][SEP_BN] fits in the weight buffer (>= 16 x 32)
   part[ty * SEP_BN + tx * 2] = o0;
   part[ty * SEP_BN + tx * 2 + 1] = o1;
   __syncthreads();
-#pragma unroll 1
+#pragma unroll 2
   for (int e = tid; e < SEP_BM * SEP_BN; e += SEP_THREADS) {
     const int m = m0 + e / SEP_BN, n = n0 + e % SEP_BN;
     if (m >= a.M || n >= a.K) continue;
@@ -213,7 +211,7 @@ static SepArgs sep_args(const sw_op_desc& op) {
 
 size_t sepconv_smem_bytes(int C) {
   const int cp = (C + SEP_BK - 1) / SEP_BK * SEP_BK;
-  return 4 * ((size_t)cp * SEP_BM + 2 * SEP_BK * SEP_BN);
+  return 4 * ((size_t)cp * SEP_BM + (size_t)cp * SEP_BN);
 }
 
 template <bool VEC>

@@ -366,7 +366,7 @@ class Engine:
     """Nimble-style AoT engine around a static ``nn.Module`` (eval mode, fp32)."""
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
-                 device: int = 0, conv_impl: str = "auto", pdl: bool = True):
+                 device: int = 0, conv_impl: str = "auto", pdl: bool = False):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -377,6 +377,7 @@ class Engine:
         self.conv_impl = conv_impl
         self.pdl = pdl
         self.tuning = {}
+        self.tuning_log = {}
         self._h = None
         self.prepared = False
 
@@ -490,6 +491,9 @@ class Engine:
                 trial.variant = variant
                 trial.params[SP_SPLIT_K] = split
                 rc = lib.sw_engine_time_op(self._h, C.byref(trial), reps, C.byref(us))
+                self.tuning_log.setdefault(t.tid, []).append(
+                    (kind, variant, split, us.value if rc == 0 else None,
+                     None if rc == 0 else lib.sw_last_error().decode()))
                 if rc != 0:
                     continue
                 if best is None or us.value < best[0]:

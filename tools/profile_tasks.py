@@ -71,6 +71,14 @@ def main():
           f"single {r_single.makespan/1000:.1f} us critical path "
           f"{sw.critical_path_time(g2)/1000:.1f} us")
     print("tuning picks:", {k: v for k, v in list(eng.tuning.items())[:5]}, "...")
+    for r in sorted(rows, key=lambda r: -r["us"])[:4]:
+        log = eng.tuning_log.get(r["tid"], [])
+        print(f"  candidates of task {r['tid']} ({r['name']}):")
+        for kind, var, split, us, err in sorted(log, key=lambda c: (c[3] is None, c[3] or 0))[:12]:
+            print(f"     kind={kind} variant={var} split={split} " + (f"{us:.2f}us" if us is not None else f"FAILED {err}"))
+        fails = [c for c in log if c[3] is None]
+        if fails:
+            print(f"     ... {len(fails)} failed, e.g. {fails[0]}")
     # the critical path itself (longest measured-duration chain)
     preds = {t.tid: sorted(t.deps) for t in eng.program.tasks}
     best, arg = {}, {}
