@@ -31,6 +31,7 @@ struct ConvArgs {
   int64_t out_sn, out_sh, out_sw, out_sc;
   int64_t res_sn, res_sh, res_sw, res_sc;
   int M, Kdim, split;
+  Epi epi;
 };
 
 static ConvArgs conv_args(const sw_op_desc& op) {
@@ -55,6 +56,10 @@ static ConvArgs conv_args(const sw_op_desc& op) {
   a.M = a.N * a.P * a.Q;
   a.Kdim = a.R * a.S * a.C;
   a.split = p[SP_SPLIT_K] > 1 ? (int)p[SP_SPLIT_K] : 1;
+  a.epi = Epi{a.bias, a.res, a.out, a.M, a.K, a.P, a.Q, a.act, a.has_res, 0,
+              a.out_sn, a.out_sh, a.out_sw, a.out_sc, a.res_sn, a.res_sh, a.res_sw, a.res_sc};
+  a.epi.vec = epi_vec_ok(op.ptrs[PT_OUT], a.out_sn, a.out_sh, a.out_sw, a.out_sc, op.ptrs[PT_BIAS],
+                         a.has_res != 0, op.ptrs[PT_RES], a.res_sn, a.res_sh, a.res_sw, a.res_sc) ? 1 : 0;
   return a;
 }
 
@@ -191,30 +196,8 @@ conv_simt_kernel(ConvArgs a) {
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) part[(ty * TM + i) * BN + tx * TN + j] = acc[i][j];
-  int e_begin = 0, e_end = BM * BN, nranks = 1;
   cg::cluster_group cluster = cg::this_cluster();
-  if (a.split > 1) {
-    cluster.sync();
-    nranks = (int)cluster.num_blocks();
-    const int chunk = (BM * BN + nranks - 1) / nranks;
-    e_begin = (int)cluster.block_rank() * chunk;
-    e_end = min(BM * BN, e_begin + chunk);
-  } else {
-    __syncthreads();
-  }
-#pragma unroll 4
-  for (int e = e_begin + tid; e < e_end; e += NT) {
-    const int m = m0 + e / BN, n = n0 + e % BN;
-    if (m >= a.M || n >= a.K) continue;
-    float v = part[e];
-    if (nranks > 1) {
-      v = 0.f;
-#pragma unroll 1
-      for (int r = 0; r < nranks; ++r) v += cluster.map_shared_rank(part, r)[e];
-    }
-    conv_epilogue_store(a, m, n, v);
-  }
-  if (a.split > 1) cluster.sync();
+  tile_epilogue<BM, BN, NT>(a.epi, part, m0, n0, a.split, cluster);
 }
 
 // Small-M 1x1 conv / linear (batch-1 classifier heads, 1x1-spatial layers):

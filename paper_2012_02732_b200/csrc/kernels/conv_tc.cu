@@ -43,6 +43,7 @@ struct TcArgs {
   int64_t out_sn, out_sh, out_sw, out_sc;
   int64_t res_sn, res_sh, res_sw, res_sc;
   int M, Kdim, Kpad, split, vec;
+  Epi epi;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
     const int st = it % S;
-    cp_wait<S - 1>();
+    cp_wait<S - 2>();  // tile `it` landed (refills run one iteration behind)
     __syncthreads();
     // split the activation tile: hi = tf32(x) in place, lo = x - hi beside it
     {
@@ -293,9 +294,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
       }
       mma_commit(smem_u32(&mbar[st]));
     }
-    if (it + S < iters) {  // refill this stage once the tensor core has consumed it
-      mbar_wait(smem_u32(&mbar[st]), (it / S) & 1);
-      issue(it + S, st);
+    // refill the stage of the PREVIOUS tile (its MMAs have had a whole
+    // iteration to drain) with tile it-1+S; the tensor pipe stays busy
+    if (it >= 1 && it - 1 + S < iters) {
+      const int ps = (it - 1) % S;
+      mbar_wait(smem_u32(&mbar[ps]), ((it - 1) / S) & 1);
+      issue(it - 1 + S, ps);
     }
     cp_commit();
   }
@@ -324,30 +328,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     for (int j = 0; j < 16; j += 4)
       *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
-  int e0 = 0, e1 = TC_BM * BN, nr = 1;
   cg::cluster_group cluster = cg::this_cluster();
-  if (a.split > 1) {
-    cluster.sync();
-    nr = (int)cluster.num_blocks();
-    const int chunk_e = (TC_BM * BN + nr - 1) / nr;
-    e0 = (int)cluster.block_rank() * chunk_e;
-    e1 = min(TC_BM * BN, e0 + chunk_e);
-  } else {
-    __syncthreads();
-  }
-#pragma unroll 4
-  for (int e = e0 + tid; e < e1; e += TC_THREADS) {
-    const int mm = m0 + e / BN, nn = n0 + e % BN;
-    if (mm >= a.M || nn >= a.K) continue;
-    float sacc = part[e];
-    if (nr > 1) {
-      sacc = 0.f;
-#pragma unroll 1
-      for (int r2 = 0; r2 < nr; ++r2) sacc += cluster.map_shared_rank(part, r2)[e];
-    }
-    tc_epilogue_store(a, mm, nn, sacc);
-  }
-  if (a.split > 1) cluster.sync();
+  tile_epilogue<TC_BM, BN, TC_THREADS>(a.epi, part, m0, n0, a.split, cluster);
 
   tc_fence_before();
   __syncthreads();
@@ -383,6 +365,10 @@ static TcArgs tc_args(const sw_op_desc& op) {
   a.split = p[SP_SPLIT_K] > 1 ? (int)p[SP_SPLIT_K] : 1;
   a.vec = (a.C % 4 == 0) && a.in_sc == 1 && (a.in_sn % 4 == 0) && (a.in_sh % 4 == 0) && (a.in_sw % 4 == 0) &&
           ((op.ptrs[PT_IN] & 15) == 0);
+  a.epi = Epi{a.bias, a.res, a.out, a.M, a.K, a.P, a.Q, a.act, a.has_res, 0,
+              a.out_sn, a.out_sh, a.out_sw, a.out_sc, a.res_sn, a.res_sh, a.res_sw, a.res_sc};
+  a.epi.vec = epi_vec_ok(op.ptrs[PT_OUT], a.out_sn, a.out_sh, a.out_sw, a.out_sc, op.ptrs[PT_BIAS],
+                         a.has_res != 0, op.ptrs[PT_RES], a.res_sn, a.res_sh, a.res_sw, a.res_sc) ? 1 : 0;
   return a;
 }
 
