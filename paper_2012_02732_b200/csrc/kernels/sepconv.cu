@@ -5,22 +5,26 @@
 // the graph executor issues roughly one kernel node per microsecond
 // (tools/microbench.cu), so node count is latency.
 //
-// CTA = 256 threads, tile = 16 output pixels x 32 output channels:
-//   1. cp.async prefetch of the first pointwise-weight chunk;
-//   2. depthwise for all C_in channels of the 16 pixels into smem D[c][px]
-//      (branch-free unrolled taps, 128-bit NHWC loads when C % 4 == 0);
-//   3. pointwise GEMM D^T x W over C_in (all weight chunks requested by
-//      cp.async at kernel start, before the PDL wait), 1x2 micro-tile;
-//   4. smem-staged rolled epilogue (bias, residual, activation, strided store).
+// CTA = 256 threads, tile = BM output pixels x BN output channels (variants
+// autotuned at prepare; a small BN means more CTAs but recomputes the
+// depthwise tile per column block, a large BN the opposite):
+//   1. cp.async of ALL pointwise weight rows the tile needs and of the whole
+//      depthwise filter, issued before the PDL wait (constants);
+//   2. depthwise for all C_in channels of the BM pixels into smem D[c][px]
+//      (branch-free unrolled taps, 128-bit NHWC loads, filter from smem);
+//   3. pointwise GEMM D^T x W, TM x TN micro-tile per thread;
+//   4. shared float4 tile epilogue (bias, residual, activation, strided store).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sw {
 
 namespace {
 
-constexpr int SEP_BM = 16;
-constexpr int SEP_BN = 32;
-constexpr int SEP_BK = 16;
+constexpr int SEP_BK = 16;  // channel padding granule
 constexpr int SEP_THREADS = 256;
 
 struct SepArgs {
@@ -33,57 +37,70 @@ struct SepArgs {
   const float* __restrict__ res;
   int N, H, W, C, P, Q, K, R, S, sh, sw, ph, pw, act, dw_act, pre_relu, has_res, M, vec;
   int in_sn, in_sh, in_sw, in_sc;
-  int64_t out_sn, out_sh, out_sw, out_sc;
-  int64_t res_sn, res_sh, res_sw, res_sc;
+  Epi epi;
 };
 
 __device__ __forceinline__ void cp4(float* dst, const float* src, bool ok) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
 }
+__device__ __forceinline__ void cp16(float* dst, const float* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 }  // namespace
 
-template <int KS, bool VEC>
+template <int KS, bool VEC, int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
+  static_assert((BM / TM) * (BN / TN) == SEP_THREADS, "256 threads");
   extern __shared__ __align__(16) float smem[];
-  const int Cp = (a.C + SEP_BK - 1) / SEP_BK * SEP_BK;  // D rows padded to the K chunk
-  float* D = smem;                                      // [Cp][SEP_BM]
-  float* Bs = smem + Cp * SEP_BM;                       // [Cp][SEP_BN]: every weight chunk
-  const int tid = threadIdx.x;
-  const int m0 = blockIdx.x * SEP_BM;
-  const int n0 = blockIdx.y * SEP_BN;
+  const int Cp = (a.C + SEP_BK - 1) / SEP_BK * SEP_BK;
   const int RR = KS ? KS : a.R;
   const int SS = KS ? KS : a.S;
+  float* D = smem;                  // [Cp][BM]
+  float* Bs = D + Cp * BM;          // [Cp][BN]
+  float* Wd = Bs + Cp * BN;         // [RR*SS][Cp]
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
 
-  // pointwise weight chunk loader: thread → (k row, n col) pairs of a 16x32 chunk
-  auto load_b = [&](int chunk, int buf) {
-#pragma unroll
-    for (int i = 0; i < (SEP_BK * SEP_BN) / SEP_THREADS; ++i) {
-      const int e = tid + i * SEP_THREADS;
-      const int kk = e % SEP_BK, nn = e / SEP_BK;
-      const int c = chunk * SEP_BK + kk, n = n0 + nn;
-      const bool ok = c < a.C && n < a.K;
-      cp4(&Bs[(buf * SEP_BK + kk) * SEP_BN + nn], a.w_pw + (ok ? (size_t)n * a.C + c : 0), ok);
-    }
-    cp_commit();
-  };
-  // weights are constant: request every chunk before waiting on the producer,
-  // so the whole pointwise operand is one round trip hidden behind the depthwise
-  const int chunks = Cp / SEP_BK;
+  // constants first: every pointwise row the tile needs + the depthwise filter
 #pragma unroll 1
-  for (int ch = 0; ch < chunks; ++ch) load_b(ch, ch);
+  for (int e = tid; e < Cp * BN; e += SEP_THREADS) {
+    const int c = e % Cp, nn = e / Cp;
+    const int n = n0 + nn;
+    const bool ok = c < a.C && n < a.K;
+    cp4(&Bs[c * BN + nn], a.w_pw + (ok ? (size_t)n * a.C + c : 0), ok);
+  }
+  if (VEC) {
+#pragma unroll 1
+    for (int e = tid; e < RR * SS * (Cp / 4); e += SEP_THREADS) {
+      const int cg4 = e % (Cp / 4), tap = e / (Cp / 4);
+      const bool ok = cg4 * 4 < a.C;
+      cp16(&Wd[tap * Cp + cg4 * 4], a.w_dw + (ok ? tap * a.C + cg4 * 4 : 0), ok);
+    }
+  } else {
+#pragma unroll 1
+    for (int e = tid; e < RR * SS * Cp; e += SEP_THREADS) {
+      const int c = e % Cp, tap = e / Cp;
+      const bool ok = c < a.C;
+      cp4(&Wd[tap * Cp + c], a.w_dw + (ok ? tap * a.C + c : 0), ok);
+    }
+  }
+  cp_commit();
   pdl_trigger();
   pdl_wait();
+  cp_wait_all();
+  __syncthreads();
 
-  // ---- depthwise into D[c][px] (zero for padded rows / pixels past M) ----
+  // ---- depthwise into D[c][px] (zero for padded channels / pixels past M) ----
   constexpr int V = VEC ? 4 : 1;
   const int cgroups = Cp / V;
 #pragma unroll 1
-  for (int e = tid; e < SEP_BM * cgroups; e += SEP_THREADS) {
+  for (int e = tid; e < BM * cgroups; e += SEP_THREADS) {
     const int cg = e % cgroups;
     const int px = e / cgroups;
     const int c = cg * V;
@@ -112,10 +129,10 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
               const int iw = iw0 + ss;
               const bool ok = rok && (unsigned)iw < (unsigned)a.W;
               const float* src = base + (ok ? ih * a.in_sh + iw * a.in_sw : 0);
-              const float* wsrc = a.w_dw + (rr * SS + ss) * a.C + c;
+              const float* wsrc = &Wd[(rr * SS + ss) * Cp + c];
               if constexpr (VEC) {
                 float4 x = __ldg(reinterpret_cast<const float4*>(src));
-                const float4 w = __ldg(reinterpret_cast<const float4*>(wsrc));
+                const float4 w = *reinterpret_cast<const float4*>(wsrc);
                 if (a.pre_relu) {
                   x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
                 }
@@ -127,58 +144,51 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
               } else {
                 float x = __ldg(src);
                 if (a.pre_relu) x = fmaxf(x, 0.f);
-                acc[0] = fmaf(ok ? x : 0.f, __ldg(wsrc), acc[0]);
+                acc[0] = fmaf(ok ? x : 0.f, *wsrc, acc[0]);
               }
             }
           }
         }
       }
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        float v = acc[j] + (a.b_dw ? a.b_dw[c + j] : 0.f);
-        acc[j] = apply_act(v, a.dw_act);
-      }
+      for (int j = 0; j < V; ++j) acc[j] = apply_act(acc[j] + (a.b_dw ? a.b_dw[c + j] : 0.f), a.dw_act);
     }
 #pragma unroll
-    for (int j = 0; j < V; ++j) D[(c + j) * SEP_BM + px] = acc[j];
+    for (int j = 0; j < V; ++j) D[(c + j) * BM + px] = acc[j];
   }
+  __syncthreads();
 
   // ---- pointwise GEMM: out[px][n] = sum_c D[c][px] * W[n][c] ----
-  const int ty = tid / (SEP_BN / 2);  // 0..15 → output row (pixel) ty
-  const int tx = tid % (SEP_BN / 2);  // 0..15 → cols tx*2, tx*2+1
-  float o0 = 0.f, o1 = 0.f;
-  cp_wait<0>();
-  __syncthreads();  // D complete and all weight chunks landed
-#pragma unroll 1
-  for (int ch = 0; ch < chunks; ++ch) {
-    const float* bt = Bs + ch * SEP_BK * SEP_BN + tx * 2;
-    const float* at = D + ch * SEP_BK * SEP_BM + ty;
+  const int ty = tid / (BN / TN);
+  const int tx = tid % (BN / TN);
+  float o[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) o[i][j] = 0.f;
+  const float* at = D + ty * TM;
+  const float* bt = Bs + tx * TN;
 #pragma unroll 4
-    for (int k = 0; k < SEP_BK; ++k) {
-      const float av = at[k * SEP_BM];
-      const float2 bv = *reinterpret_cast<const float2*>(bt + k * SEP_BN);
-      o0 = fmaf(av, bv.x, o0);
-      o1 = fmaf(av, bv.y, o1);
-    }
+  for (int k = 0; k < Cp; ++k) {
+    float av[TM], bv[TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) av[i] = at[k * BM + i];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) bv[j] = bt[k * BN + j];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) o[i][j] = fmaf(av[i], bv[j], o[i][j]);
   }
-  __syncthreads();
+  __syncthreads();  // D / Bs reads done; reuse D as the output tile
 
-  // ---- epilogue (tile through smem, rolled, coalesced along channels) ----
-  float* part = Bs;  // [SEP_BM][SEP_BN] fits in the weight buffer (>= 16 x 32)
-  part[ty * SEP_BN + tx * 2] = o0;
-  part[ty * SEP_BN + tx * 2 + 1] = o1;
-  __syncthreads();
-#pragma unroll 2
-  for (int e = tid; e < SEP_BM * SEP_BN; e += SEP_THREADS) {
-    const int m = m0 + e / SEP_BN, n = n0 + e % SEP_BN;
-    if (m >= a.M || n >= a.K) continue;
-    const int q = m % a.Q;
-    const int t = m / a.Q;
-    const int pp = t % a.P, nb = t / a.P;
-    float v = part[e] + (a.b_pw ? a.b_pw[n] : 0.f);
-    if (a.has_res) v += a.res[nb * a.res_sn + pp * a.res_sh + q * a.res_sw + n * a.res_sc];
-    a.out[nb * a.out_sn + pp * a.out_sh + q * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
-  }
+  float* part = D;  // [BM][BN] ≤ Cp*BM + Cp*BN floats
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) part[(ty * TM + i) * BN + tx * TN + j] = o[i][j];
+  cg::cluster_group cluster = cg::this_cluster();
+  tile_epilogue<BM, BN, SEP_THREADS>(a.epi, part, m0, n0, 1, cluster);
 }
 
 static SepArgs sep_args(const sw_op_desc& op) {
@@ -199,28 +209,53 @@ static SepArgs sep_args(const sw_op_desc& op) {
   a.act = (int)p[SP_ACT]; a.dw_act = (int)p[SP_DW_ACT];
   a.pre_relu = (int)p[SP_PRE_RELU]; a.has_res = (int)p[SP_HAS_RES];
   a.in_sn = (int)p[SP_IN_SN]; a.in_sh = (int)p[SP_IN_SH]; a.in_sw = (int)p[SP_IN_SW]; a.in_sc = (int)p[SP_IN_SC];
-  a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
-  a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
-  a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
-  a.res_sc = p[SP_RES_SC] ? p[SP_RES_SC] : 1;
   a.M = a.N * a.P * a.Q;
   a.vec = (a.C % 4 == 0) && a.in_sc == 1 && a.in_sn % 4 == 0 && a.in_sh % 4 == 0 && a.in_sw % 4 == 0 &&
           aligned16(op.ptrs[PT_IN]) && aligned16(op.ptrs[PT_WS]);
+  const int64_t osn = p[SP_OUT_SN], osh = p[SP_OUT_SH], osw = p[SP_OUT_SW], osc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
+  const int64_t rsn = p[SP_RES_SN], rsh = p[SP_RES_SH], rsw = p[SP_RES_SW], rsc = p[SP_RES_SC] ? p[SP_RES_SC] : 1;
+  a.epi = Epi{a.b_pw, a.res, a.out, a.M, a.K, a.P, a.Q, a.act, a.has_res, 0, osn, osh, osw, osc, rsn, rsh, rsw, rsc};
+  a.epi.vec = epi_vec_ok(op.ptrs[PT_OUT], osn, osh, osw, osc, op.ptrs[PT_BIAS], a.has_res != 0, op.ptrs[PT_RES],
+                         rsn, rsh, rsw, rsc) ? 1 : 0;
   return a;
 }
 
-size_t sepconv_smem_bytes(int C) {
-  const int cp = (C + SEP_BK - 1) / SEP_BK * SEP_BK;
-  return 4 * ((size_t)cp * SEP_BM + (size_t)cp * SEP_BN);
+namespace {
+struct SepCfg {
+  int bm, bn;
+};
+// variant → tile (all 256 threads)
+constexpr SepCfg kSep[] = {{16, 32}, {8, 64}, {16, 64}, {32, 32}, {8, 32}, {32, 64}};
+constexpr int kNumSep = sizeof(kSep) / sizeof(kSep[0]);
+constexpr int kSepSmemMax = 227 * 1024;
+}  // namespace
+
+static size_t sep_smem(int C, int R, int S, int bm, int bn) {
+  const size_t cp = (size_t)(C + SEP_BK - 1) / SEP_BK * SEP_BK;
+  const size_t body = cp * bm + cp * bn + (size_t)R * S * cp;
+  const size_t part = (size_t)bm * bn;  // epilogue tile reuses the same buffer
+  return 4 * (body > part ? body : part);
+}
+
+template <int KS, bool VEC>
+static cudaError_t launch_sep_v(int v, const SepArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  switch (v) {
+    case 1: return launch_k(sepconv_kernel<KS, VEC, 8, 64, 1, 2>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 2: return launch_k(sepconv_kernel<KS, VEC, 16, 64, 1, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 3: return launch_k(sepconv_kernel<KS, VEC, 32, 32, 2, 2>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 4: return launch_k(sepconv_kernel<KS, VEC, 8, 32, 1, 1>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 5: return launch_k(sepconv_kernel<KS, VEC, 32, 64, 2, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    default: return launch_k(sepconv_kernel<KS, VEC, 16, 32, 1, 2>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+  }
 }
 
 template <bool VEC>
-static int launch_sep_ks(const SepArgs& a, int ks, dim3 grid, size_t smem, cudaStream_t st) {
+static cudaError_t launch_sep_ks(int ks, int v, const SepArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   switch (ks) {
-    case 3: return (int)launch_k(sepconv_kernel<3, VEC>, grid, dim3(SEP_THREADS), smem, st, 1, a);
-    case 5: return (int)launch_k(sepconv_kernel<5, VEC>, grid, dim3(SEP_THREADS), smem, st, 1, a);
-    case 7: return (int)launch_k(sepconv_kernel<7, VEC>, grid, dim3(SEP_THREADS), smem, st, 1, a);
-    default: return (int)launch_k(sepconv_kernel<0, VEC>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 3: return launch_sep_v<3, VEC>(v, a, grid, smem, st);
+    case 5: return launch_sep_v<5, VEC>(v, a, grid, smem, st);
+    case 7: return launch_sep_v<7, VEC>(v, a, grid, smem, st);
+    default: return launch_sep_v<0, VEC>(v, a, grid, smem, st);
   }
 }
 
@@ -228,19 +263,27 @@ int launch_sepconv(const sw_op_desc& op, void* stream) {
   SepArgs a = sep_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a.M == 0 || a.K == 0) return 0;
-  const size_t smem = sepconv_smem_bytes(a.C);
-  if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
-  dim3 grid((unsigned)cdiv(a.M, SEP_BM), (unsigned)cdiv(a.K, SEP_BN));
+  const int v = (op.variant >= 0 && op.variant < kNumSep) ? op.variant : 0;
+  const size_t smem = sep_smem(a.C, a.R, a.S, kSep[v].bm, kSep[v].bn);
+  if (smem > (size_t)kSepSmemMax) return (int)cudaErrorInvalidValue;  // the autotuner skips it
+  dim3 grid((unsigned)cdiv(a.M, kSep[v].bm), (unsigned)cdiv(a.K, kSep[v].bn));
   const int ks = (a.R == a.S && (a.R == 3 || a.R == 5 || a.R == 7)) ? a.R : 0;
-  return a.vec ? launch_sep_ks<true>(a, ks, grid, smem, st) : launch_sep_ks<false>(a, ks, grid, smem, st);
+  return (int)(a.vec ? launch_sep_ks<true>(ks, v, a, grid, smem, st) : launch_sep_ks<false>(ks, v, a, grid, smem, st));
+}
+
+template <int KS, bool VEC>
+static void init_sep_ks() {
+  cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 16, 32, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 8, 64, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 16, 64, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 32, 32, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 8, 32, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 32, 64, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
 }
 
 void init_sep_kernels() {
-  const int maxb = 227 * 1024;
-  void (*fns[])(SepArgs) = {sepconv_kernel<3, true>, sepconv_kernel<5, true>, sepconv_kernel<7, true>,
-                            sepconv_kernel<0, true>, sepconv_kernel<3, false>, sepconv_kernel<5, false>,
-                            sepconv_kernel<7, false>, sepconv_kernel<0, false>};
-  for (auto f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
+  init_sep_ks<3, true>(); init_sep_ks<5, true>(); init_sep_ks<7, true>(); init_sep_ks<0, true>();
+  init_sep_ks<3, false>(); init_sep_ks<5, false>(); init_sep_ks<7, false>(); init_sep_ks<0, false>();
 }
 
 }  // namespace sw

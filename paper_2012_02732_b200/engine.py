@@ -80,6 +80,9 @@ def pick_conv_variant(M: int, K: int, Kdim: int, R: int, S: int, pad, stride) ->
     return v, split
 
 
+# csrc/kernels/sepconv.cu kSep[]: variant → (BM pixels, BN channels), 256 threads
+SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (32, 64)}
+
 # csrc/kernels/conv.cu kSimt[]: variant → (BM, BN); every variant runs 256 threads
 SIMT_TILES = {0: (64, 64), 1: (32, 64), 2: (32, 32), 3: (128, 64), 4: (16, 32), 5: (16, 64),
               6: (16, 16), 7: (64, 32)}
@@ -475,7 +478,7 @@ class Engine:
         lib = N.lib()
         us = C.c_double()
         for t in self.program.tasks:
-            if t.kind != "conv":
+            if t.kind not in ("conv", "sepconv"):
                 continue
             d = self.ops[t.tid]
             p = d.params
@@ -485,8 +488,11 @@ class Engine:
             best = None
             trial = N.OpDesc()
             C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
-            for kind, variant, split in conv_candidates(M, K, Kdim, p[SP_R], p[SP_S],
-                                                         (p[SP_PAD_H], p[SP_PAD_W])):
+            if t.kind == "sepconv":
+                cands = [(K_SEPCONV, v, 1) for v in range(len(SEP_TILES))]
+            else:
+                cands = conv_candidates(M, K, Kdim, p[SP_R], p[SP_S], (p[SP_PAD_H], p[SP_PAD_W]))
+            for kind, variant, split in cands:
                 trial.kind = kind
                 trial.variant = variant
                 trial.params[SP_SPLIT_K] = split

@@ -123,6 +123,30 @@ def test_depthwise(c, k, s, p, h):
     close(y, ref)
 
 
+@pytest.mark.parametrize("variant", range(6))
+@pytest.mark.parametrize("c,k,s,h", [(44, 5, 1, 14), (11, 7, 2, 23), (176, 3, 1, 7)])
+def test_sepconv_tile_variants(variant, c, k, s, h):
+    """Every fused depthwise→pointwise tile variant, forced (vector and scalar paths)."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_SEPCONV, SLOT_MULTI
+    torch.manual_seed(3)
+    m = DW(c, k, s, k // 2).eval()
+    x = torch.randn(1, c, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    d = eng.ops[0]
+    assert d.kind == K_SEPCONV and len(eng.program.tasks) == 1
+    d.variant = variant
+    N.check(N.lib().sw_engine_set_ops(eng._h, 1, eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 class Pools(nn.Module):
     def __init__(self):
         super().__init__()
