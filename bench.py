@@ -195,7 +195,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(dev)
     model, shape = build_model(args.config)
     x = example_input(shape, batch=args.batch, seed=1 + rank)
-    eng = Engine(model, multi_stream=True, device=local).prepare(x)
+    eng = Engine(model, multi_stream=True, device=local,
+                 tuning_cache=args.tuning_cache).prepare(x)
     # correctness gate before timing (cheap at batch 1)
     y = eng(x)
     parity = None
@@ -371,6 +372,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--tuning-cache", default=None,
+                    help="reuse kernel picks (e.g. for an ncu launch list of this command)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

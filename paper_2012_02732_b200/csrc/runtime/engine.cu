@@ -350,38 +350,45 @@ int sw_engine_graph_topology(sw_engine* e, int32_t slot, int64_t cap, int64_t* o
 }
 
 int sw_engine_profile_ops(sw_engine* e, int64_t n, const int64_t* order, int32_t reps, double* out_us) {
-  if (reps < 1) reps = 1;
-  CU(cudaStreamSynchronize(e->launch));
+  // each task timed as a graph-captured chain (see sw_engine_time_op)
   for (int64_t i = 0; i < n; ++i) {
-    int64_t t = order[i];
-    CU(cudaEventRecord(e->t0, e->launch));
-    for (int r = 0; r < reps; ++r) {
-      int rc = launch_task(e->ops[t], e->launch);
-      if (rc) return rc;
-    }
-    CU(cudaEventRecord(e->t1, e->launch));
-    CU(cudaEventSynchronize(e->t1));
-    float ms = 0.f;
-    CU(cudaEventElapsedTime(&ms, e->t0, e->t1));
-    out_us[i] = (double)ms * 1000.0 / reps;
+    int rc = sw_engine_time_op(e, &e->ops[order[i]], reps, &out_us[i]);
+    if (rc) return rc;
   }
   return SW_OK;
 }
 
+// Candidates are timed as a chain of `reps` dependent launches inside a
+// captured CUDA graph — the way they will run — so microsecond kernels are not
+// masked by the host's stream-launch rate (~4 µs per cudaLaunchKernelEx).
 int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* out_us) {
   if (reps < 1) reps = 1;
   CU(cudaStreamSynchronize(e->launch));
-  int rc = launch_task(*op, e->launch);
+  int rc = launch_task(*op, e->launch);  // validates the launch outside capture
   if (rc) return rc;
-  CU(cudaEventRecord(e->t0, e->launch));
-  for (int r = 0; r < reps; ++r) {
-    rc = launch_task(*op, e->launch);
-    if (rc) return rc;
+  CU(cudaStreamSynchronize(e->launch));
+  cudaGraph_t g = nullptr;
+  CU(cudaStreamBeginCapture(e->launch, cudaStreamCaptureModeThreadLocal));
+  for (int r = 0; r < reps && rc == 0; ++r) rc = launch_task(*op, e->launch);
+  cudaError_t ce = cudaStreamEndCapture(e->launch, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
   }
-  CU(cudaEventRecord(e->t1, e->launch));
-  CU(cudaEventSynchronize(e->t1));
+  if (ce != cudaSuccess) return cuda_fail(ce, "time_op capture");
+  cudaGraphExec_t ex = nullptr;
+  ce = cudaGraphInstantiateWithFlags(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return cuda_fail(ce, "time_op instantiate");
+  ce = cudaGraphLaunch(ex, e->launch);  // warm (code + data into caches)
+  if (ce == cudaSuccess) ce = cudaEventRecord(e->t0, e->launch);
+  if (ce == cudaSuccess) ce = cudaGraphLaunch(ex, e->launch);
+  if (ce == cudaSuccess) ce = cudaEventRecord(e->t1, e->launch);
+  if (ce == cudaSuccess) ce = cudaEventSynchronize(e->t1);
   float ms = 0.f;
-  CU(cudaEventElapsedTime(&ms, e->t0, e->t1));
+  if (ce == cudaSuccess) ce = cudaEventElapsedTime(&ms, e->t0, e->t1);
+  cudaGraphExecDestroy(ex);
+  if (ce != cudaSuccess) return cuda_fail(ce, "time_op replay");
   *out_us = (double)ms * 1000.0 / reps;
   return SW_OK;
 }

@@ -19,12 +19,13 @@ def main():
     ap.add_argument("--conv-impl", default="simt")
     ap.add_argument("--replays", type=int, default=1)
     ap.add_argument("--eager", type=int, default=1)
+    ap.add_argument("--tuning-cache", default=None)
     a = ap.parse_args()
     from paper_2012_02732_b200.engine import Engine
     from paper_2012_02732_b200.networks import build_model, example_input
     model, shape = build_model(a.config)
     x = example_input(shape, batch=a.batch)
-    eng = Engine(model, conv_impl=a.conv_impl).prepare(x)
+    eng = Engine(model, conv_impl=a.conv_impl, tuning_cache=a.tuning_cache).prepare(x)
     eng.load_input_device(x)
     for _ in range(a.eager):
         eng.run_eager(python_loop=False)
