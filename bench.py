@@ -299,6 +299,10 @@ def run_ours(args, world, rank, local):
     achieved = dd["bytes"] / (dd["us"] * 1e-6) / 1e9
     roof_sum = eng.roofline_sum_us(hbm, bf16)
 
+    extra = None
+    if rank == 0 and world == 1 and not args.skip_extra:
+        extra = other_configs(args, dev, hbm, bf16, flush, stream)
+
     line = None
     if rank == 0:
         cpu = None
@@ -357,9 +361,72 @@ def run_ours(args, world, rank, local):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if extra is not None:
+            line["other_configs"] = extra
         print(json.dumps(line))
     eng.close()
     return line
+
+
+def other_configs(args, dev, hbm, bf16, flush, stream):
+    """The remaining BASELINE configs, same engine and timing discipline:
+    latency (µs) of multi-stream AoT replay, single-stream AoT replay and the
+    eager launch loop for the 8-op cell / ResNet-50 / Inception-v3 at batch 1,
+    and NASNet-A mobile images/s at batch 256 (one replica)."""
+    import torch
+    from paper_2012_02732_b200.engine import Engine
+    from paper_2012_02732_b200.networks import build_model, example_input
+
+    out = {}
+    plan = [("cell", 1), ("resnet50", 1), ("inception_v3", 1), ("nasnet_mobile", args.big_batch)]
+    steps = max(10, min(args.steps, 50))
+    for name, batch in plan:
+        t0 = time.perf_counter()
+        model, shape = build_model(name)
+        x = example_input(shape, batch=batch)
+        eng = Engine(model, device=dev.index or 0).prepare(x)
+        eng.load_input_device(x)
+
+        def timed(multi):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(steps)]
+            with torch.cuda.stream(stream):
+                for a, b in ev:
+                    flush.zero_()
+                    a.record(stream)
+                    eng.replay(multi=multi)
+                    b.record(stream)
+            torch.cuda.synchronize(dev)
+            return sum(a.elapsed_time(b) for a, b in ev) / steps * 1e3
+
+        # the engine has its own launch stream; time on it
+        import ctypes as C
+        from paper_2012_02732_b200 import _native as N
+        sh = C.c_uint64()
+        N.check(N.lib().sw_engine_stream(eng._h, C.byref(sh)))
+        stream = torch.cuda.ExternalStream(sh.value, device=dev)
+        for _ in range(3):
+            eng.replay(multi=True)
+            eng.replay(multi=False)
+        torch.cuda.synchronize(dev)
+        multi_us = timed(True)
+        single_us = timed(False)
+        t = time.perf_counter()
+        for _ in range(3):
+            eng.run_eager()
+        eng.synchronize()
+        eager_us = (time.perf_counter() - t) / 3 * 1e6
+        roof = eng.roofline_sum_us(hbm, bf16)
+        out[f"{name}_bs{batch}"] = {
+            "multi_stream_aot_us": round(multi_us, 2), "single_stream_aot_us": round(single_us, 2),
+            "eager_non_aot_us": round(eager_us, 2),
+            "images_per_s": round(batch / (multi_us * 1e-6), 2),
+            "multi_over_single": round(single_us / multi_us, 4),
+            "tasks": len(eng.program.tasks), "streams": eng.assignment.num_streams,
+            "syncs": len(eng.plan), "roofline_sum_us": round(roof, 3),
+            "prepare_s": round(time.perf_counter() - t0, 2)}
+        eng.close()
+    return out
 
 
 def main():
@@ -372,6 +439,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-extra", action="store_true", help="skip the other BASELINE configs")
+    ap.add_argument("--big-batch", type=int, default=256, help="NASNet images/s batch (one replica)")
     ap.add_argument("--tuning-cache", default=None,
                     help="reuse kernel picks (e.g. for an ncu launch list of this command)")
     args = ap.parse_args()

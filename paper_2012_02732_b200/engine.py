@@ -369,7 +369,7 @@ class Engine:
     """Nimble-style AoT engine around a static ``nn.Module`` (eval mode, fp32)."""
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
-                 device: int = 0, conv_impl: str = "auto", pdl: bool = False,
+                 device: int = 0, conv_impl: str = "auto", pdl: bool = True,
                  tuning_cache: str | None = None):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
@@ -460,6 +460,7 @@ class Engine:
         t3 = time.perf_counter()
         if self.conv_impl == "auto":
             self.d_in.copy_(ex.reshape(-1).to(dev))
+            self._signature = self._tuning_signature()  # before tuning rewrites the ops
             if not self._load_tuning():
                 self._autotune()
                 self._save_tuning()
@@ -494,7 +495,7 @@ class Engine:
             return False
         with open(self.tuning_cache) as fh:
             doc = json.load(fh)
-        if doc.get("signature") != self._tuning_signature():
+        if doc.get("signature") != self._signature:
             return False
         for tid, kind, variant, split in doc["picks"]:
             d = self.ops[tid]
@@ -509,7 +510,7 @@ class Engine:
             return
         picks = [[tid, b[1], b[2], b[3]] for tid, b in sorted(self.tuning.items())]
         with open(self.tuning_cache, "w") as fh:
-            json.dump({"signature": self._tuning_signature(), "picks": picks}, fh)
+            json.dump({"signature": self._signature, "picks": picks}, fh)
 
     def _autotune(self, reps: int = 5):
         """Time every conv task's candidate kernels in isolation; keep the fastest."""
