@@ -294,9 +294,27 @@ def run_ours(args, world, rank, local):
         d["flops"] += f_
         d["bytes"] += b_
         d["n"] += 1
+    # simulator in the loop: the reference replay semantics
+    # fed with the measured per-task durations (ns), zero submission overhead
+    import paper_2012_02732_b200 as swpkg
+    g0 = eng.graph
+    gd = swpkg.CompGraph.build(
+        [swpkg.TaskNode(n.id, max(1, int(round(per_task[n.id] * 1000))), 1, n.label, n.mem)
+         for n in g0.nodes], g0.edges)
+    fd, pd = swpkg.assign_streams(gd)
+    sim_multi = swpkg.simulate(swpkg.pre_run(gd, fd, pd), gd, swpkg.SimConfig()).makespan / 1000
+    sim_single = sum(per_task)
+    crit = swpkg.critical_path_time(gd) / 1000
     dom = max(fam, key=lambda k: fam[k]["us"])
     dd = fam[dom]
     achieved = dd["bytes"] / (dd["us"] * 1e-6) / 1e9
+    # DRAM bytes per launch of this family from the committed ncu --set full
+    # capture (profiles/traffic.json, written by tools/ncu_summary.py --traffic)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(dom)
     roof_sum = eng.roofline_sum_us(hbm, bf16)
 
     extra = None
@@ -341,10 +359,14 @@ def run_ours(args, world, rank, local):
             "host_overhead": {"launch_us_per_iter": round(host_us, 3),
                               "gpu_us_per_iter": round(gpu_us, 3),
                               "fraction_of_gpu_time": round(host_us / gpu_us, 5)},
+            "simulated_from_measured": {"multi_stream_us": round(sim_multi, 2),
+                                        "single_stream_us": round(sim_single, 2),
+                                        "critical_path_us": round(crit, 2)},
             "roofline_sum_us": round(roof_sum, 3),
             "latency_over_roofline_sum": round(ms * 1e3 / roof_sum, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 5), "traffic": None,
+                         "frac": round(achieved / hbm, 5), "traffic": traffic,
+                         "algorithmic_bytes_per_launch": round(dd["bytes"] / dd["n"], 1),
                          "kernel": f"{dom} family ({dd['n']} launches, "
                                    f"{dd['us'] / n_tasks:.2f} µs avg/task)",
                          "peak_source": peak_src},

@@ -8,7 +8,7 @@
 // CTA = 256 threads, tile = BM output pixels x BN output channels (variants
 // autotuned at prepare; a small BN means more CTAs but recomputes the
 // depthwise tile per column block, a large BN the opposite):
-//   1. cp.async of ALL pointwise weight rows the tile needs and of the whole
+//   1. cp.async of the pointwise weights (stored [C][K]) the tile needs and of the whole
 //      depthwise filter, issued before the PDL wait (constants);
 //   2. depthwise for all C_in channels of the BM pixels into smem D[c][px]
 //      (branch-free unrolled taps, 128-bit NHWC loads, filter from smem);
@@ -35,7 +35,7 @@ struct SepArgs {
   const float* __restrict__ w_dw;   // [R][S][C]
   const float* __restrict__ b_dw;   // [C] or null
   const float* __restrict__ res;
-  int N, H, W, C, P, Q, K, R, S, sh, sw, ph, pw, act, dw_act, pre_relu, has_res, M, vec;
+  int N, H, W, C, P, Q, K, R, S, sh, sw, ph, pw, act, dw_act, pre_relu, has_res, M, vec, wvec;
   int in_sn, in_sh, in_sw, in_sc;
   Epi epi;
 };
@@ -60,20 +60,31 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   const int Cp = (a.C + SEP_BK - 1) / SEP_BK * SEP_BK;
   const int RR = KS ? KS : a.R;
   const int SS = KS ? KS : a.S;
-  float* D = smem;                  // [Cp][BM]
-  float* Bs = D + Cp * BM;          // [Cp][BN]
+  float* D = smem;                  // [BM][Cp]   depthwise tile, channels contiguous
+  float* Bs = D + Cp * BM;          // [Cp][BN]   pointwise weights, columns contiguous
   float* Wd = Bs + Cp * BN;         // [RR*SS][Cp]
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * BM;
   const int n0 = blockIdx.y * BN;
 
-  // constants first: every pointwise row the tile needs + the depthwise filter
+  // constants first: the tile's pointwise columns (weights stored transposed,
+  // [C][K], so the fill is coalesced and bank-conflict free) + the filter
+  if (a.wvec) {
 #pragma unroll 1
-  for (int e = tid; e < Cp * BN; e += SEP_THREADS) {
-    const int c = e % Cp, nn = e / Cp;
-    const int n = n0 + nn;
-    const bool ok = c < a.C && n < a.K;
-    cp4(&Bs[c * BN + nn], a.w_pw + (ok ? (size_t)n * a.C + c : 0), ok);
+    for (int e = tid; e < Cp * (BN / 4); e += SEP_THREADS) {
+      const int n4 = e % (BN / 4), c = e / (BN / 4);
+      const int n = n0 + n4 * 4;
+      const bool ok = c < a.C && n < a.K;  // K % 4 == 0: a group is all in or all out
+      cp16(&Bs[c * BN + n4 * 4], a.w_pw + (ok ? (size_t)c * a.K + n : 0), ok);
+    }
+  } else {
+#pragma unroll 1
+    for (int e = tid; e < Cp * BN; e += SEP_THREADS) {
+      const int nn = e % BN, c = e / BN;
+      const int n = n0 + nn;
+      const bool ok = c < a.C && n < a.K;
+      cp4(&Bs[c * BN + nn], a.w_pw + (ok ? (size_t)c * a.K + n : 0), ok);
+    }
   }
   if (VEC) {
 #pragma unroll 1
@@ -96,7 +107,7 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   cp_wait_all();
   __syncthreads();
 
-  // ---- depthwise into D[c][px] (zero for padded channels / pixels past M) ----
+  // ---- depthwise into D[px][c] (zero for padded channels / pixels past M) ----
   constexpr int V = VEC ? 4 : 1;
   const int cgroups = Cp / V;
 #pragma unroll 1
@@ -153,8 +164,11 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[j] = apply_act(acc[j] + (a.b_dw ? a.b_dw[c + j] : 0.f), a.dw_act);
     }
-#pragma unroll
-    for (int j = 0; j < V; ++j) D[(c + j) * BM + px] = acc[j];
+    if constexpr (VEC) {
+      *reinterpret_cast<float4*>(&D[px * Cp + c]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+      D[px * Cp + c] = acc[0];
+    }
   }
   __syncthreads();
 
@@ -166,13 +180,13 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) o[i][j] = 0.f;
-  const float* at = D + ty * TM;
+  const float* at = D + ty * TM * Cp;
   const float* bt = Bs + tx * TN;
 #pragma unroll 4
   for (int k = 0; k < Cp; ++k) {
     float av[TM], bv[TN];
 #pragma unroll
-    for (int i = 0; i < TM; ++i) av[i] = at[k * BM + i];
+    for (int i = 0; i < TM; ++i) av[i] = at[i * Cp + k];
 #pragma unroll
     for (int j = 0; j < TN; ++j) bv[j] = bt[k * BN + j];
 #pragma unroll
@@ -212,6 +226,7 @@ static SepArgs sep_args(const sw_op_desc& op) {
   a.M = a.N * a.P * a.Q;
   a.vec = (a.C % 4 == 0) && a.in_sc == 1 && a.in_sn % 4 == 0 && a.in_sh % 4 == 0 && a.in_sw % 4 == 0 &&
           aligned16(op.ptrs[PT_IN]) && aligned16(op.ptrs[PT_WS]);
+  a.wvec = (a.K % 4 == 0) && aligned16(op.ptrs[PT_W]);
   const int64_t osn = p[SP_OUT_SN], osh = p[SP_OUT_SH], osw = p[SP_OUT_SW], osc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
   const int64_t rsn = p[SP_RES_SN], rsh = p[SP_RES_SH], rsw = p[SP_RES_SW], rsc = p[SP_RES_SC] ? p[SP_RES_SC] : 1;
   a.epi = Epi{a.b_pw, a.res, a.out, a.M, a.K, a.P, a.Q, a.act, a.has_res, 0, osn, osh, osw, osc, rsn, rsh, rsw, rsc};

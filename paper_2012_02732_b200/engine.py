@@ -178,7 +178,7 @@ def _pack_weights(prog: Program):
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
         elif t.kind == "sepconv":
             pw = n.attrs["weight"].float().reshape(n.attrs["weight"].shape[0], -1)  # [K][C]
-            arrays[(t.tid, "w")] = pw.contiguous().numpy().reshape(-1)
+            arrays[(t.tid, "w")] = pw.t().contiguous().numpy().reshape(-1)  # stored [C][K]
             if n.attrs["bias"] is not None:
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
             dw = n.attrs["dw_weight"].float()[:, 0].permute(1, 2, 0).contiguous()  # [R][S][C]

@@ -109,7 +109,7 @@ def run_op(mem: HostMemory, d):
                 bdw = torch.from_numpy(mem.buf[mem.idx(q[E.PT_DW_BIAS]):mem.idx(q[E.PT_DW_BIAS]) + Cc].copy())
                 dwo = dwo + bdw.double().view(1, -1, 1, 1)
             dwo = _act(dwo.float(), p[E.SP_DW_ACT])
-            wpw = torch.from_numpy(mem.buf[mem.idx(q[E.PT_W]):mem.idx(q[E.PT_W]) + K * Cc].copy()).view(K, Cc)
+            wpw = torch.from_numpy(mem.buf[mem.idx(q[E.PT_W]):mem.idx(q[E.PT_W]) + K * Cc].copy()).view(Cc, K).t()
             y = F.conv2d(dwo.double(), wpw.double()[:, :, None, None]).float()
             if q[E.PT_BIAS]:
                 b = torch.from_numpy(mem.buf[mem.idx(q[E.PT_BIAS]):mem.idx(q[E.PT_BIAS]) + K].copy())

@@ -105,7 +105,41 @@ def summarize_launches(path: str) -> str:
     return "\n".join(out) + "\n"
 
 
+FAMILY = {"sepconv_kernel": "sepconv", "conv_simt_kernel": "conv", "conv_tc_kernel": "conv",
+          "conv_gemv_kernel": "conv", "spatial_kernel<0": "dwconv", "spatial_kernel<1": "pool",
+          "global_pool": "gpool", "ew_": "eltwise"}
+
+
+def traffic_json(path: str) -> dict:
+    """Mean DRAM bytes (read + write) per launch, by engine task family."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    acc = defaultdict(list)
+    for row in rows[2:]:
+        if len(row) < len(hdr):
+            continue
+        name = row[hdr.index("Kernel Name")]
+        fam = next((f for k, f in FAMILY.items() if k in name), None)
+        if fam is None:
+            continue
+        b = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v = _num(row[hdr.index(key)]) or 0.0
+            b += v * _UNIT.get(units[hdr.index(key)], 1.0)
+        acc[fam].append(b)
+    return {f: sum(v) / len(v) for f, v in acc.items()}
+
+
 def main():
+    if sys.argv[1] == "--traffic":
+        import json
+        d = traffic_json(sys.argv[2])
+        with open(sys.argv[3], "w") as fh:
+            json.dump(d, fh, indent=1)
+        print(d)
+        return
     if sys.argv[1] == "--launches":
         text = summarize_launches(sys.argv[2])
         dst = sys.argv[3]
