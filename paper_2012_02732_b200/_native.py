@@ -15,7 +15,9 @@ import numpy as np
 
 from .errors import ExtensionMissing, from_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsw_b200.so")
+# SW_B200_LIB selects the diagnostic build (libsw_b200_probe.so) for tools/
+LIB_PATH = os.environ.get("SW_B200_LIB") or \
+    os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsw_b200.so")
 
 i64 = C.c_int64
 i32 = C.c_int32

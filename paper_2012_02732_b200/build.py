@@ -59,7 +59,12 @@ def _run(cmd, log):
         raise RuntimeError(f"build step failed: {' '.join(cmd[:6])} ...")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, probe: bool = False) -> str:
+    """Build libsw_b200.so; ``probe=True`` builds the diagnostic variant
+    libsw_b200_probe.so (-DSW_PROBE: kernel phase stamps, tools/phase_probe.py)."""
+    BUILD = os.path.join(ROOT, "build", "probe") if probe else os.path.join(ROOT, "build")
+    LIB = os.path.join(PKG, "libsw_b200_probe.so") if probe else globals()["LIB"]
+    extra = ["-DSW_PROBE"] if probe else []
     os.makedirs(BUILD, exist_ok=True)
     newest_header = max(os.path.getmtime(h) for h in headers())
     objs = []
@@ -74,9 +79,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if not stale:
             continue
         if src.endswith(".cu"):
-            cmd = [NVCC, *NVCC_FLAGS, "-c", src, "-o", obj]
+            cmd = [NVCC, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         else:
-            cmd = ["g++", *CXX_FLAGS, "-c", src, "-o", obj]
+            cmd = ["g++", *CXX_FLAGS, *extra, "-c", src, "-o", obj]
         jobs.append(cmd)
     # compile in parallel
     procs = []
@@ -107,8 +112,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--probe", action="store_true", help="diagnostic build with kernel phase stamps")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, probe=a.probe))
 
 
 if __name__ == "__main__":

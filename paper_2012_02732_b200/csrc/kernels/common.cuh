@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "../runtime/ops.h"
+#include "probe.cuh"
 
 namespace sw {
 

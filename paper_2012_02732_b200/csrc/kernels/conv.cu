@@ -126,7 +126,9 @@ conv_simt_kernel(ConvArgs a) {
   }
   const int in_sh = (int)a.in_sh, in_sw = (int)a.in_sw, in_sc = (int)a.in_sc;
 
-  auto issue = [&](int kstep, int buf) {
+  // A (activations) and B (weights) halves of one ring stage; the weights of
+  // the prologue stages are constants and go out before the PDL wait.
+  auto issue_a = [&](int kstep, int buf) {
     const int k = kstep * BK + kk;
     const bool kin = k < a.Kdim;
     const int c = k % a.C;
@@ -134,7 +136,6 @@ conv_simt_kernel(ConvArgs a) {
     const int s = rs % a.S;
     const int r = rs / a.S;
     float* as = As + (buf * BK + kk) * (BM + PAD) + row;
-    float* bs = Bs + (buf * BK + kk) * (BN + PAD) + row;
 #pragma unroll
     for (int i = 0; i < A_PER; ++i) {
       if (row + i * 16 >= BM) break;
@@ -142,6 +143,11 @@ conv_simt_kernel(ConvArgs a) {
       const bool ok = kin && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
       cp_async4(as + i * 16, a.in + (ok ? a_base[i] + ih * in_sh + iw * in_sw + c * in_sc : 0), ok);
     }
+  };
+  auto issue_b = [&](int kstep, int buf) {
+    const int k = kstep * BK + kk;
+    const bool kin = k < a.Kdim;
+    float* bs = Bs + (buf * BK + kk) * (BN + PAD) + row;
 #pragma unroll
     for (int i = 0; i < B_PER; ++i) {
       if (row + i * 16 >= BN) break;
@@ -159,19 +165,29 @@ conv_simt_kernel(ConvArgs a) {
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
+  probe_begin();
+#pragma unroll 1
+  for (int st = 0; st < STAGES - 1; ++st)
+    if (st < nsteps) issue_b(ks_begin + st, st);  // joins commit group 0
   pdl_trigger();
+  probe_pt(1);
   pdl_wait();
+  probe_pt(2);
 #pragma unroll 1
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nsteps) issue(ks_begin + st, st);
+    if (st < nsteps) issue_a(ks_begin + st, st);
     cp_async_commit();
   }
 #pragma unroll 1
   for (int it = 0; it < nsteps; ++it) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();  // tile `it` landed for everyone; buffer (it-1)%STAGES is free
+    if (it == 0) probe_pt(3);
     const int nxt = it + STAGES - 1;
-    if (nxt < nsteps) issue(ks_begin + nxt, nxt % STAGES);
+    if (nxt < nsteps) {
+      issue_a(ks_begin + nxt, nxt % STAGES);
+      issue_b(ks_begin + nxt, nxt % STAGES);
+    }
     cp_async_commit();
     const float* at = As + (it % STAGES) * BK * (BM + PAD) + ty * TM;
     const float* bt = Bs + (it % STAGES) * BK * (BN + PAD) + tx * TN;
@@ -190,6 +206,7 @@ conv_simt_kernel(ConvArgs a) {
   }
   cp_async_wait<0>();
   __syncthreads();
+  probe_pt(4);
 
   float* part = smem;  // [BM][BN], reuses the operand buffers
 #pragma unroll
@@ -198,6 +215,7 @@ conv_simt_kernel(ConvArgs a) {
     for (int j = 0; j < TN; ++j) part[(ty * TM + i) * BN + tx * TN + j] = acc[i][j];
   cg::cluster_group cluster = cg::this_cluster();
   tile_epilogue<BM, BN, NT>(a.epi, part, m0, n0, a.split, cluster);
+  probe_end();
 }
 
 // Small-M 1x1 conv / linear (batch-1 classifier heads, 1x1-spatial layers):

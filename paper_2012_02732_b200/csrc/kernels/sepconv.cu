@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * BM;
   const int n0 = blockIdx.y * BN;
+  probe_begin();
 
   // constants first: the tile's pointwise columns (weights stored transposed,
   // [C][K], so the fill is coalesced and bank-conflict free) + the filter
@@ -103,9 +105,12 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   }
   cp_commit();
   pdl_trigger();
+  probe_pt(1);
   pdl_wait();
+  probe_pt(2);
   cp_wait_all();
   __syncthreads();
+  probe_pt(3);
 
   // ---- depthwise into D[px][c] (zero for padded channels / pixels past M) ----
   constexpr int V = VEC ? 4 : 1;
@@ -171,6 +176,7 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
     }
   }
   __syncthreads();
+  probe_pt(4);
 
   // ---- pointwise GEMM: out[px][n] = sum_c D[c][px] * W[n][c] ----
   const int ty = tid / (BN / TN);
@@ -195,6 +201,7 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
       for (int j = 0; j < TN; ++j) o[i][j] = fmaf(av[i], bv[j], o[i][j]);
   }
   __syncthreads();  // D / Bs reads done; reuse D as the output tile
+  probe_pt(5);
 
   float* part = D;  // [BM][BN] ≤ Cp*BM + Cp*BN floats
 #pragma unroll
@@ -203,6 +210,175 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
     for (int j = 0; j < TN; ++j) part[(ty * TM + i) * BN + tx * TN + j] = o[i][j];
   cg::cluster_group cluster = cg::this_cluster();
   tile_epilogue<BM, BN, SEP_THREADS>(a.epi, part, m0, n0, 1, cluster);
+  probe_end();
+}
+
+// ---------------------------------------------------------------------------
+// TMA variant.  One CTA = BM output pixels of ONE output row x BN output
+// channels.  Everything it reads arrives by TMA / bulk copies that complete on
+// two mbarriers, issued by one thread:
+//   constants (before the PDL wait): pointwise weight slab [C][BN] (2-D tensor
+//     map over the transposed weights), depthwise filter [KS*KS][C] and both
+//     biases (1-D bulk copies);
+//   activations (after the wait): the input patch [KS][PCW][C] of the row
+//     (4-D tensor map over NHWC with per-dim strides, so concat slices and
+//     padding — out-of-bounds rows / columns are zero-filled by TMA — need no
+//     address math) and the residual tile [BM][BN].
+// The patch arrives in one memory round trip (the cp.async / ldg variants
+// above keep only a few of the 25-49 taps in flight: ~5 µs of a 7x7).
+// Depthwise from smem → D[c][px]; pointwise GEMM split over the 8 warps along
+// C (16 independent FMAs per lane per channel instead of a 176-long chain);
+// the warp partials are summed in the epilogue with bias, residual and act.
+// ---------------------------------------------------------------------------
+struct SepTmaGeo {
+  int PCW;     // patch columns = (BM - 1) * stride + KS
+  int CB;      // channels per patch chunk (≤ 256) and chunks
+  int NCH;
+  int CBW;     // weight rows per box (≤ 256) and boxes
+  int NCW;
+  int QT;      // column tiles per output row
+  int o_bs, o_wd, o_bdw, o_bpw, o_x, o_d, o_r, o_bar;  // smem offsets (floats)
+  uint32_t bytes_const, bytes_act;
+};
+
+template <int KS, int BM, int BN>
+__global__ void __launch_bounds__(SEP_THREADS)
+sepconv_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tw,
+                   const __grid_constant__ CUtensorMap tres, SepArgs a, SepTmaGeo g) {
+  static_assert(BN % 32 == 0 && BM % 4 == 0, "tile");
+  constexpr int JN = BN / 32;  // columns per lane
+  extern __shared__ __align__(128) float smem[];
+  float* Bs = smem + g.o_bs;
+  float* Wd = smem + g.o_wd;
+  float* bdw = smem + g.o_bdw;
+  float* bpw = smem + g.o_bpw;
+  float* Xs = smem + g.o_x;
+  float* D = smem + g.o_d;
+  float* Rs = smem + g.o_r;
+  float* Pt = Xs;  // warp partials reuse the patch once the depthwise is done
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + g.o_bar);
+  const uint32_t bar_c = su32(&bars[0]), bar_a = su32(&bars[1]);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qt = blockIdx.x % g.QT;
+  const int rowi = blockIdx.x / g.QT;  // nb * P + p
+  const int p = rowi % a.P, nb = rowi / a.P;
+  const int q0 = qt * BM;
+  const int n0 = blockIdx.y * BN;
+  const int C = a.C;
+  probe_begin();
+
+  if (tid == 0) {
+    prefetch_tmap(&tin);
+    prefetch_tmap(&tw);
+    mbar_init1(bar_c);
+    mbar_init1(bar_a);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_cta();
+    mbar_expect_tx(bar_c, g.bytes_const + (a.b_pw ? (uint32_t)(min(BN, a.K - n0) * 4) : 0u));
+#pragma unroll 1
+    for (int j = 0; j < g.NCW; ++j) tma_load_2d(su32(Bs + j * g.CBW * BN), &tw, n0, j * g.CBW, bar_c);
+    bulk_g2s(su32(Wd), a.w_dw, (uint32_t)(KS * KS * C * 4), bar_c);
+    if (a.b_dw) bulk_g2s(su32(bdw), a.b_dw, (uint32_t)(C * 4), bar_c);
+    if (a.b_pw) bulk_g2s(su32(bpw), a.b_pw + n0, (uint32_t)(min(BN, a.K - n0) * 4), bar_c);
+  }
+  pdl_trigger();
+  probe_pt(1);
+  pdl_wait();
+  probe_pt(2);
+  if (tid == 0) {
+    mbar_expect_tx(bar_a, g.bytes_act);
+    const int iw0 = q0 * a.sw - a.pw, ih0 = p * a.sh - a.ph;
+#pragma unroll 1
+    for (int j = 0; j < g.NCH; ++j) tma_load_4d(su32(Xs + j * KS * g.PCW * g.CB), &tin, j * g.CB, iw0, ih0, nb, bar_a);
+    if (a.has_res) tma_load_4d(su32(Rs), &tres, n0, q0, p, nb, bar_a);
+  }
+  __syncthreads();  // barrier inits visible before anyone polls them
+  mbar_wait_parity(bar_c, 0);
+  mbar_wait_parity(bar_a, 0);
+  probe_pt(3);
+
+  // ---- depthwise: D[c][px] ----
+  const int C4 = C >> 2;
+#pragma unroll 1
+  for (int e = tid; e < BM * C4; e += SEP_THREADS) {
+    const int cg = e % C4, px = e / C4;
+    const int c = cg * 4;
+    const int ch = c / g.CB, cc = c - ch * g.CB;
+    const float* xb = Xs + (ch * KS * g.PCW + px * a.sw) * g.CB + cc;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < KS; ++r) {
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) {
+        float4 x = *reinterpret_cast<const float4*>(xb + (r * g.PCW + s2) * g.CB);
+        const float4 w = *reinterpret_cast<const float4*>(Wd + (r * KS + s2) * C + c);
+        if (a.pre_relu) {
+          x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+        }
+        acc.x = fmaf(x.x, w.x, acc.x);
+        acc.y = fmaf(x.y, w.y, acc.y);
+        acc.z = fmaf(x.z, w.z, acc.z);
+        acc.w = fmaf(x.w, w.w, acc.w);
+      }
+    }
+    if (a.b_dw) acc = f4add(acc, *reinterpret_cast<const float4*>(bdw + c));
+    D[(c + 0) * BM + px] = apply_act(acc.x, a.dw_act);
+    D[(c + 1) * BM + px] = apply_act(acc.y, a.dw_act);
+    D[(c + 2) * BM + px] = apply_act(acc.z, a.dw_act);
+    D[(c + 3) * BM + px] = apply_act(acc.w, a.dw_act);
+  }
+  __syncthreads();
+  probe_pt(4);
+
+  // ---- pointwise: warp w sums channels [w*C/8, (w+1)*C/8) for the whole tile ----
+  float o[BM][JN];
+#pragma unroll
+  for (int i = 0; i < BM; ++i)
+#pragma unroll
+    for (int j = 0; j < JN; ++j) o[i][j] = 0.f;
+  const int k0 = warp * C / 8, k1 = (warp + 1) * C / 8;
+#pragma unroll 2
+  for (int k = k0; k < k1; ++k) {
+    float dv[BM];
+#pragma unroll
+    for (int i = 0; i < BM; i += 4) {
+      const float4 t = *reinterpret_cast<const float4*>(D + k * BM + i);
+      dv[i] = t.x; dv[i + 1] = t.y; dv[i + 2] = t.z; dv[i + 3] = t.w;
+    }
+    float bv[JN];
+#pragma unroll
+    for (int j = 0; j < JN; ++j) bv[j] = Bs[k * BN + lane + 32 * j];
+#pragma unroll
+    for (int i = 0; i < BM; ++i)
+#pragma unroll
+      for (int j = 0; j < JN; ++j) o[i][j] = fmaf(dv[i], bv[j], o[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < BM; ++i)
+#pragma unroll
+    for (int j = 0; j < JN; ++j) Pt[(warp * BM + i) * BN + lane + 32 * j] = o[i][j];
+  __syncthreads();
+  probe_pt(5);
+
+  // ---- epilogue: sum the 8 warp partials, bias, residual, act, float4 store ----
+  constexpr int GPR = BN / 4;
+#pragma unroll 1
+  for (int gi = tid; gi < BM * GPR; gi += SEP_THREADS) {
+    const int px = gi / GPR, nn = (gi % GPR) * 4;
+    const int q = q0 + px, n = n0 + nn;
+    float4 t[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t[w] = *reinterpret_cast<const float4*>(Pt + (w * BM + px) * BN + nn);
+    float4 v = t[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v = f4add(v, t[w]);
+    if (a.b_pw) v = f4add(v, *reinterpret_cast<const float4*>(bpw + nn));
+    if (a.has_res) v = f4add(v, *reinterpret_cast<const float4*>(Rs + px * BN + nn));
+    if (q < a.Q && n < a.K)
+      *reinterpret_cast<float4*>(a.out + nb * a.epi.out_sn + p * a.epi.out_sh + q * a.epi.out_sw + n) =
+          act4(v, a.act);
+  }
+  probe_end();
 }
 
 static SepArgs sep_args(const sw_op_desc& op) {
@@ -274,10 +450,102 @@ static cudaError_t launch_sep_ks(int ks, int v, const SepArgs& a, dim3 grid, siz
   }
 }
 
+// ---- TMA variants (6..): tile (BM, BN) ----
+namespace {
+constexpr SepCfg kSepTma[] = {{4, 32}, {8, 32}, {8, 64}, {16, 32}, {16, 64}};
+constexpr int kNumSepTma = sizeof(kSepTma) / sizeof(kSepTma[0]);
+}  // namespace
+
+static int round32(int x) { return (x + 31) / 32 * 32; }
+
+// smem plan of the TMA kernel; false if the op cannot use it
+static bool sep_tma_geo(const SepArgs& a, const sw_op_desc& op, int bm, int bn, SepTmaGeo* g, size_t* smem) {
+  const int ks = a.R;
+  if (a.R != a.S || (ks != 3 && ks != 5 && ks != 7)) return false;
+  if (!a.vec || a.in_sc != 1 || !a.wvec || !a.epi.vec) return false;
+  if (a.has_res && (op.params[SP_RES_SC] > 1 || (op.ptrs[PT_RES] & 15))) return false;
+  if ((op.ptrs[PT_WS] & 15) || (op.ptrs[PT_DW_BIAS] & 15) || (op.ptrs[PT_BIAS] & 15)) return false;
+  g->PCW = (bm - 1) * a.sw + ks;
+  if (g->PCW > 256) return false;
+  g->CB = a.C <= 256 ? a.C : 256;
+  g->NCH = (a.C + g->CB - 1) / g->CB;
+  g->CBW = a.C <= 256 ? a.C : 256;
+  g->NCW = (a.C + g->CBW - 1) / g->CBW;
+  g->QT = (a.Q + bm - 1) / bm;
+  const int bs = g->NCW * g->CBW * bn;
+  const int patch = g->NCH * ks * g->PCW * g->CB;
+  int o = 0;
+  g->o_bs = o; o += round32(bs);
+  g->o_wd = o; o += round32(ks * ks * a.C);
+  g->o_bdw = o; o += round32(a.C);
+  g->o_bpw = o; o += round32(bn);
+  g->o_x = o; o += round32(patch > 8 * bm * bn ? patch : 8 * bm * bn);
+  g->o_d = o; o += round32(a.C * bm);
+  g->o_r = o; o += round32(bm * bn);
+  g->o_bar = o; o += 32;
+  *smem = (size_t)o * 4;
+  if (*smem > (size_t)kSepSmemMax) return false;
+  // weight boxes are always BN wide (out-of-range columns zero-filled); the
+  // pointwise bias slice is added per CTA in the kernel
+  g->bytes_const = (uint32_t)(bs + ks * ks * a.C + (a.b_dw ? a.C : 0)) * 4;
+  g->bytes_act = (uint32_t)(patch + (a.has_res ? bm * bn : 0)) * 4;
+  return true;
+}
+
+template <int KS, int BM, int BN>
+static cudaError_t launch_sep_tma_t(const SepArgs& a, const sw_op_desc& op, cudaStream_t st) {
+  SepTmaGeo g;
+  size_t smem = 0;
+  if (!sep_tma_geo(a, op, BM, BN, &g, &smem)) return cudaErrorInvalidValue;
+  CUtensorMap tin, tw, tres;
+  {
+    const uint64_t dims[4] = {(uint64_t)a.C, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.N};
+    const uint64_t str[3] = {(uint64_t)a.in_sw * 4, (uint64_t)a.in_sh * 4, (uint64_t)a.in_sn * 4};
+    const uint32_t box[4] = {(uint32_t)g.CB, (uint32_t)g.PCW, (uint32_t)KS, 1};
+    if (!encode_tmap_f32(&tin, a.in, 4, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.C};
+    const uint64_t str[1] = {(uint64_t)a.K * 4};
+    const uint32_t box[2] = {(uint32_t)BN, (uint32_t)g.CBW};
+    if (!encode_tmap_f32(&tw, a.w_pw, 2, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  if (a.has_res) {
+    const uint64_t dims[4] = {(uint64_t)a.K, (uint64_t)a.Q, (uint64_t)a.P, (uint64_t)a.N};
+    const uint64_t str[3] = {(uint64_t)a.epi.res_sw * 4, (uint64_t)a.epi.res_sh * 4, (uint64_t)a.epi.res_sn * 4};
+    const uint32_t box[4] = {(uint32_t)BN, (uint32_t)BM, 1, 1};
+    if (!encode_tmap_f32(&tres, a.res, 4, dims, str, box)) return cudaErrorInvalidValue;
+  } else {
+    tres = tw;  // unused
+  }
+  dim3 grid((unsigned)(a.N * a.P * g.QT), (unsigned)cdiv(a.K, BN));
+  return launch_k(sepconv_tma_kernel<KS, BM, BN>, grid, dim3(SEP_THREADS), smem, st, 1, tin, tw, tres, a, g);
+}
+
+template <int KS>
+static cudaError_t launch_sep_tma_ks(int v, const SepArgs& a, const sw_op_desc& op, cudaStream_t st) {
+  switch (v) {
+    case 0: return launch_sep_tma_t<KS, 4, 32>(a, op, st);
+    case 1: return launch_sep_tma_t<KS, 8, 32>(a, op, st);
+    case 2: return launch_sep_tma_t<KS, 8, 64>(a, op, st);
+    case 3: return launch_sep_tma_t<KS, 16, 32>(a, op, st);
+    default: return launch_sep_tma_t<KS, 16, 64>(a, op, st);
+  }
+}
+
 int launch_sepconv(const sw_op_desc& op, void* stream) {
   SepArgs a = sep_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a.M == 0 || a.K == 0) return 0;
+  if (op.variant >= kNumSep && op.variant < kNumSep + kNumSepTma) {
+    const int v = op.variant - kNumSep;
+    switch (a.R == a.S ? a.R : 0) {
+      case 3: return (int)launch_sep_tma_ks<3>(v, a, op, st);
+      case 5: return (int)launch_sep_tma_ks<5>(v, a, op, st);
+      case 7: return (int)launch_sep_tma_ks<7>(v, a, op, st);
+      default: return (int)cudaErrorInvalidValue;
+    }
+  }
   const int v = (op.variant >= 0 && op.variant < kNumSep) ? op.variant : 0;
   const size_t smem = sep_smem(a.C, a.R, a.S, kSep[v].bm, kSep[v].bn);
   if (smem > (size_t)kSepSmemMax) return (int)cudaErrorInvalidValue;  // the autotuner skips it
@@ -296,7 +564,17 @@ static void init_sep_ks() {
   cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 32, 64, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
 }
 
+template <int KS>
+static void init_sep_tma_ks() {
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 4, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+}
+
 void init_sep_kernels() {
+  init_sep_tma_ks<3>(); init_sep_tma_ks<5>(); init_sep_tma_ks<7>();
   init_sep_ks<3, true>(); init_sep_ks<5, true>(); init_sep_ks<7, true>(); init_sep_ks<0, true>();
   init_sep_ks<3, false>(); init_sep_ks<5, false>(); init_sep_ks<7, false>(); init_sep_ks<0, false>();
 }

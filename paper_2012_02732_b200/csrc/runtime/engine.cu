@@ -24,6 +24,46 @@
 #include "../planner/planner.h"
 #include "ops.h"
 
+#ifdef SW_PROBE
+#include "../kernels/probe.cuh"
+
+namespace sw {
+static std::vector<ProbeFn>& probe_registry() {
+  static std::vector<ProbeFn> r;
+  return r;
+}
+int probe_register(ProbeFn fn) {
+  probe_registry().push_back(fn);
+  return 0;
+}
+}  // namespace sw
+
+// Diagnostic build only (not in include/): zero every kernel TU's probe
+// buffer / read back the one that saw launches as 64 uint64:
+// [0,16) phase points, [16,32) first-CTA start per launch, [32,48) last-CTA
+// end per launch, [48] CTAs started, [49] CTAs finished.
+extern "C" int sw_probe_reset() {
+  for (auto fn : sw::probe_registry()) fn(nullptr, true);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
+extern "C" int sw_probe_read(uint64_t* out) {
+  for (int i = 0; i < 64; ++i) out[i] = 0;
+  for (auto fn : sw::probe_registry()) {
+    sw::ProbeBuf b;
+    fn(&b, false);
+    if (b.started == 0) continue;
+    for (int i = 0; i < 16; ++i) {
+      out[i] = b.pt[i];
+      out[16 + i] = b.start[i];
+      out[32 + i] = b.end[i];
+    }
+    out[48] = b.started;
+    out[49] = b.finished;
+  }
+  return 0;
+}
+#endif
+
 namespace sw {
 thread_local bool g_launch_pdl = false;
 }
@@ -369,7 +409,9 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
   CU(cudaStreamSynchronize(e->launch));
   cudaGraph_t g = nullptr;
   CU(cudaStreamBeginCapture(e->launch, cudaStreamCaptureModeThreadLocal));
+  sw::g_launch_pdl = (e->flags & SW_ENGINE_PDL) != 0;  // same edges as the replayed graph
   for (int r = 0; r < reps && rc == 0; ++r) rc = launch_task(*op, e->launch);
+  sw::g_launch_pdl = false;
   cudaError_t ce = cudaStreamEndCapture(e->launch, &g);
   if (rc) {
     if (g) cudaGraphDestroy(g);

@@ -81,7 +81,10 @@ def pick_conv_variant(M: int, K: int, Kdim: int, R: int, S: int, pad, stride) ->
 
 
 # csrc/kernels/sepconv.cu kSep[]: variant → (BM pixels, BN channels), 256 threads
-SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (32, 64)}
+SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (32, 64),
+             # TMA-staged kernel (one output row per CTA): BM pixels x BN channels
+             6: (4, 32), 7: (8, 32), 8: (8, 64), 9: (16, 32), 10: (16, 64)}
+SEP_TMA_FIRST = 6
 
 # csrc/kernels/conv.cu kSimt[]: variant → (BM, BN); every variant runs 256 threads
 SIMT_TILES = {0: (64, 64), 1: (32, 64), 2: (32, 32), 3: (128, 64), 4: (16, 32), 5: (16, 64),
@@ -457,6 +460,7 @@ class Engine:
         N.check(lib.sw_engine_set_io(h, self.h_in.data_ptr(), self.d_in.data_ptr(),
                                      self.h_in.numel() * 4, self.h_out.data_ptr(),
                                      self.d_out_ptr, self.out_bytes))
+        N.check(lib.sw_engine_set_flags(h, 1 if self.pdl else 0))  # tuning sees the graph's PDL edges
         t3 = time.perf_counter()
         if self.conv_impl == "auto":
             self.d_in.copy_(ex.reshape(-1).to(dev))
@@ -466,7 +470,6 @@ class Engine:
                 self._save_tuning()
         self.plan_seconds["autotune"] = time.perf_counter() - t3
         N.check(lib.sw_engine_set_ops(h, len(prog.tasks), self.ops))
-        N.check(lib.sw_engine_set_flags(h, 1 if self.pdl else 0))
         t3 = time.perf_counter()
         self._capture(SLOT_MULTI_IO, ts, True)
         self._capture(SLOT_SINGLE_IO, ts_single, True)

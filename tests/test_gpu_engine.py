@@ -147,6 +147,55 @@ def test_sepconv_tile_variants(variant, c, k, s, h):
     eng.close()
 
 
+class SepBlock(nn.Module):
+    """relu → dw (+BN) → pw (+BN) [+ residual], then a pool so the fused
+    sepconv writes an NHWC intermediate (the TMA variants' layout)."""
+
+    def __init__(self, c, k, s, res):
+        super().__init__()
+        self.res = res and s == 1
+        self.c0 = nn.Conv2d(c, c, 1)  # NHWC producer for the sepconv input and residual
+        self.dw = nn.Conv2d(c, c, k, s, k // 2, groups=c, bias=False)
+        self.b1 = nn.BatchNorm2d(c)
+        self.pw = nn.Conv2d(c, c, 1, bias=False)
+        self.b2 = nn.BatchNorm2d(c)
+        self.pool = nn.AvgPool2d(3, 1, 1, count_include_pad=False)
+
+    def forward(self, x):
+        x = self.c0(x)
+        y = self.b2(self.pw(self.b1(self.dw(torch.relu(x)))))
+        if self.res:
+            y = y + x
+        return self.pool(y)
+
+
+@pytest.mark.parametrize("variant", range(6, 11))
+@pytest.mark.parametrize("c,k,s,h,res", [(44, 5, 1, 14, True), (176, 3, 1, 7, True), (88, 7, 2, 14, False),
+                                         (44, 3, 2, 28, False), (32, 7, 1, 9, True)])
+def test_sepconv_tma_variants(variant, c, k, s, h, res):
+    """TMA-staged fused sepconv (patch / weights / residual by tensor maps), forced."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_SEPCONV, SLOT_MULTI
+    from paper_2012_02732_b200.networks import randomize_bn
+    torch.manual_seed(5)
+    m = SepBlock(c, k, s, res).eval()
+    randomize_bn(m, seed=2)
+    x = torch.randn(1, c, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    idx = [i for i, d in enumerate(eng.ops) if d.kind == K_SEPCONV]
+    assert len(idx) == 1
+    eng.ops[idx[0]].variant = variant
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.ops), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 class Pools(nn.Module):
     def __init__(self):
         super().__init__()
