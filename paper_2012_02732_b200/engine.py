@@ -86,6 +86,9 @@ SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (
              6: (4, 32), 7: (8, 32), 8: (8, 64), 9: (16, 32), 10: (16, 64)}
 SEP_TMA_FIRST = 6
 
+# csrc/kernels/conv1x1.cu: TMA-staged pointwise conv, conv variant → (BM, BN)
+PW_TILES = {16: (8, 32), 17: (16, 32), 18: (32, 32), 19: (16, 64), 20: (32, 64), 21: (64, 32)}
+
 # csrc/kernels/conv.cu kSimt[]: variant → (BM, BN); every variant runs 256 threads
 SIMT_TILES = {0: (64, 64), 1: (32, 64), 2: (32, 32), 3: (128, 64), 4: (16, 32), 5: (16, 64),
               6: (16, 16), 7: (64, 32)}
@@ -120,6 +123,18 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
             if split > 1 and (ksteps // split < 2 or ctas * split > 4 * NUM_SMS):
                 continue
             out.append((K_CONV, v, split))
+    if R == 1 and S == 1 and tuple(pad) == (0, 0):
+        # TMA pointwise kernel (conv1x1.cu); the kernel refuses strided / odd layouts
+        for v, (bm, bn) in PW_TILES.items():
+            if bm > 2 * max(M, 8) or bn > 2 * max(K, 32):
+                continue
+            ctas = math.ceil(M / bm) * math.ceil(K / bn)
+            for split in (1, 2, 4, 8):
+                if math.ceil(Kdim / split) > 252 or ctas * split > 4 * NUM_SMS:
+                    continue
+                if split > 1 and Kdim // split < 16:
+                    continue
+                out.append((K_CONV, v, split))
     ktiles = math.ceil(Kdim / 32)
     kcap = 32
     while kcap < K:

@@ -196,6 +196,57 @@ def test_sepconv_tma_variants(variant, c, k, s, h, res):
     eng.close()
 
 
+class PwBlock(nn.Module):
+    """1x1 convs reading a zero-copy concat buffer (whole and one channel
+    slice), with a residual and pre-ReLU, feeding NHWC consumers."""
+
+    def __init__(self, cin=16, c1=120, c2=80, cout=96):
+        super().__init__()
+        self.a = nn.Conv2d(cin, c1, 3, 1, 1)
+        self.b = nn.Conv2d(cin, c2, 1)
+        self.r = nn.Conv2d(cin, cout, 1)
+        self.pw = nn.Conv2d(c1 + c2, cout, 1)
+        self.pw2 = nn.Conv2d(c1, cout, 1, bias=False)
+        self.pool = nn.AvgPool2d(3, 1, 1, count_include_pad=False)
+
+    def forward(self, x):
+        a, b, r = self.a(x), self.b(x), self.r(x)
+        h = torch.cat([a, b], 1)
+        y = self.pw(torch.relu(h)) + r
+        z = self.pw2(a)
+        return self.pool(torch.cat([y, z], 1))
+
+
+@pytest.mark.parametrize("variant", range(16, 22))
+@pytest.mark.parametrize("split", [1, 2, 4, 8])
+@pytest.mark.parametrize("hw", [7, 13])
+def test_pointwise_tma_variants(variant, split, hw):
+    """TMA pointwise conv (conv1x1.cu), every tile x DSMEM split-K cluster, forced."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV, SP_SPLIT_K, SLOT_MULTI
+    torch.manual_seed(7)
+    m = PwBlock().eval()
+    x = torch.randn(1, 16, hw, hw)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    names = [t.name for t in eng.program.tasks]
+    forced = 0
+    for i, t in enumerate(eng.program.tasks):
+        if t.name.split(".")[0] in ("pw", "pw2") and eng.ops[i].kind == K_CONV:
+            eng.ops[i].variant = variant
+            eng.ops[i].params[SP_SPLIT_K] = split
+            forced += 1
+    assert forced == 2, names
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.ops), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 class Pools(nn.Module):
     def __init__(self):
         super().__init__()
