@@ -246,6 +246,9 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
 /* Engine flags for subsequent captures / eager launches:
  * SW_ENGINE_PDL = programmatic dependent launch on same-stream kernel edges. */
 #define SW_ENGINE_PDL 1u
+/* Diagnostic: capture an empty kernel per task (same topology, same PDL
+ * protocol) — the replay then measures the graph's issue / dependency floor. */
+#define SW_ENGINE_NULL_KERNELS 2u
 int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
 #ifdef __cplusplus

@@ -25,7 +25,8 @@ namespace sw {
 
 struct PwGeo {
   int Kc;
-  int o_a, o_b, o_bias, o_res, o_t, o_bar;
+  int o_a, o_b, o_bias, o_res, o_t, o_rcv, o_bar;
+  int chunk;  // float4 groups of the tile each cluster rank finishes
   uint32_t bytes_b, bytes_act;
 };
 
@@ -42,9 +43,14 @@ pw_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
   float* Pt = smem;          // [8][BM][BN] warp partials (reuse A / B after the GEMM)
   float* bias_s = smem + g.o_bias;
   float* Rs = smem + g.o_res;  // [BM][BN]
-  float* T = smem + g.o_t;     // [BM][BN] this CTA's K-slice partial (read by the cluster)
+  float* T = smem + g.o_t;     // [BM][BN] this CTA's K-slice partial
+  float* Rcv = smem + g.o_rcv;  // [split][chunk*4] partials pushed by the peers for my slice
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + g.o_bar);
-  const uint32_t bar_c = su32(&bars[0]), bar_a = su32(&bars[1]);
+  const uint32_t bar_c = su32(&bars[0]), bar_a = su32(&bars[1]), bar_r = su32(&bars[2]);
+  const int split = (int)gridDim.z;
+  const int me = split > 1 ? (int)cluster_rank() : 0;
+  constexpr int G = BM * GPR;  // float4 groups in the tile
+  const int my_g0 = min(G, me * g.chunk), my_g1 = min(G, my_g0 + g.chunk);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int c0 = blockIdx.z * g.Kc;
@@ -56,13 +62,17 @@ pw_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
     prefetch_tmap(&tb);
     mbar_init1(bar_c);
     mbar_init1(bar_a);
+    mbar_init1(bar_r);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async_cta();
+    // the peers push (split-1) partial slices of my_g1-my_g0 groups into Rcv
+    if (split > 1) mbar_expect_tx(bar_r, (uint32_t)((split - 1) * (my_g1 - my_g0) * 16));
     const uint32_t bias_bytes = a.bias ? (uint32_t)(min(BN, a.K - n0) * 4) : 0u;
     mbar_expect_tx(bar_c, g.bytes_b + bias_bytes);
     tma_load_2d(su32(Bs), &tb, c0, n0, bar_c);
     if (a.bias) bulk_g2s(su32(bias_s), a.bias + n0, bias_bytes, bar_c);
   }
+  if (split > 1) cluster_arrive_relaxed();  // my barriers are initialised (waited on before pushing)
   pdl_trigger();
   probe_pt(1);
   pdl_wait();
@@ -75,6 +85,16 @@ pw_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
   __syncthreads();  // barrier inits visible before anyone polls them
   mbar_wait_parity(bar_c, 0);
   mbar_wait_parity(bar_a, 0);
+  if (a.pre_relu) {  // shared ReLU once over the A tile, not per use
+    float4* a4 = reinterpret_cast<float4*>(As);
+#pragma unroll 1
+    for (int i = tid; i < BM * Kc / 4; i += 256) {
+      float4 v = a4[i];
+      v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+      a4[i] = v;
+    }
+    __syncthreads();
+  }
   probe_pt(3);
 
   float o[BM][JN];
@@ -91,10 +111,7 @@ pw_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
     for (int j = 0; j < JN; ++j) b[j] = *reinterpret_cast<const float4*>(Bs + (lane + 32 * j) * Kc + 4 * kg);
 #pragma unroll
     for (int i = 0; i < BM; ++i) {
-      float4 av = *reinterpret_cast<const float4*>(As + i * Kc + 4 * kg);
-      if (a.pre_relu) {
-        av.x = fmaxf(av.x, 0.f); av.y = fmaxf(av.y, 0.f); av.z = fmaxf(av.z, 0.f); av.w = fmaxf(av.w, 0.f);
-      }
+      const float4 av = *reinterpret_cast<const float4*>(As + i * Kc + 4 * kg);
 #pragma unroll
       for (int j = 0; j < JN; ++j) {
         o[i][j] = fmaf(av.x, b[j].x, o[i][j]);
@@ -121,36 +138,45 @@ pw_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
     for (int w = 1; w < 8; ++w) v = f4add(v, t[w]);
     reinterpret_cast<float4*>(T)[gi] = v;
   }
+  probe_pt(5);
 
-  // cluster reduction over the K slices + epilogue
-  cg::cluster_group cluster = cg::this_cluster();
-  const int split = (int)gridDim.z;
-  int g0 = 0, g1 = BM * GPR;
+  // split-K reduction: push each peer its slice of my partial tile straight
+  // into its shared memory (bulk DSMEM copies completing on its mbarrier) —
+  // no cluster-wide barrier (a cg cluster.sync() costs a GPU-scope membar)
   if (split > 1) {
-    cluster.sync();
-    const int chunk = (g1 + split - 1) / split;
-    g0 = (int)cluster.block_rank() * chunk;
-    g1 = min(g1, g0 + chunk);
+    fence_proxy_async_cta();  // my T writes → visible to the bulk-copy (async) proxy
+    __syncthreads();
+    cluster_wait();  // every peer initialised its barriers
+    if (tid == 0) {
+#pragma unroll 1
+      for (int r = 0; r < split; ++r) {
+        if (r == me) continue;
+        const int r0 = min(G, r * g.chunk), r1 = min(G, r0 + g.chunk);
+        if (r1 <= r0) continue;
+        bulk_s2peer(mapa_rank(su32(Rcv + me * g.chunk * 4), (uint32_t)r), su32(T + r0 * 4), (uint32_t)((r1 - r0) * 16),
+                    mapa_rank(bar_r, (uint32_t)r));
+      }
+      bulk_commit();
+    }
+    mbar_wait_parity(bar_r, 0);
   } else {
     __syncthreads();
   }
+  probe_pt(6);
 #pragma unroll 1
-  for (int gi = g0 + tid; gi < g1; gi += 256) {
+  for (int gi = my_g0 + tid; gi < my_g1; gi += 256) {
     const int mm = gi / GPR, nn = (gi % GPR) * 4;
     const int m = m0 + mm, n = n0 + nn;
     if (m >= a.M || n >= a.K) continue;
-    float4 v;
-    if (split == 1) {
-      v = reinterpret_cast<const float4*>(T)[gi];
-    } else {
+    float4 v = reinterpret_cast<const float4*>(T)[gi];
+    if (split > 1) {
       float4 t[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r)
-        if (r < split) t[r] = reinterpret_cast<const float4*>(cluster.map_shared_rank(T, r))[gi];
-      v = t[0];
+        if (r < split && r != me) t[r] = reinterpret_cast<const float4*>(Rcv + r * g.chunk * 4)[gi - my_g0];
 #pragma unroll
-      for (int r = 1; r < 8; ++r)
-        if (r < split) v = f4add(v, t[r]);
+      for (int r = 0; r < 8; ++r)
+        if (r < split && r != me) v = f4add(v, t[r]);
     }
     if (a.bias) v = f4add(v, *reinterpret_cast<const float4*>(bias_s + nn));
     if (a.has_res) v = f4add(v, *reinterpret_cast<const float4*>(Rs + mm * BN + nn));
@@ -158,7 +184,8 @@ pw_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CU
     const int p = tt % a.P, nb = tt / a.P;
     *reinterpret_cast<float4*>(a.out + nb * a.out_sn + p * a.out_sh + q * a.out_sw + n) = act4(v, a.act);
   }
-  if (split > 1) cluster.sync();  // keep T alive until every rank has read it
+  probe_pt(7);
+  if (split > 1 && tid == 0) bulk_wait_read0();  // my pushes have read T before the CTA exits
   probe_end();
 }
 
@@ -193,6 +220,9 @@ static bool pw_geo(const ConvArgs& a, const sw_op_desc& op, int bm, int bn, PwGe
   g->o_bias = o; o += r32(bn);
   g->o_res = o; o += r32(bm * bn);
   g->o_t = o; o += r32(bm * bn);
+  const int groups = bm * bn / 4;
+  g->chunk = (groups + a.split - 1) / a.split;
+  g->o_rcv = o; o += a.split > 1 ? r32(a.split * g->chunk * 4) : 0;
   g->o_bar = o; o += 32;
   *smem = (size_t)o * 4;
   if (*smem > (size_t)kPwSmemMax) return false;

@@ -258,4 +258,16 @@ int launch_concat(const sw_op_desc& d, void* stream) {
   return (int)cudaGetLastError();
 }
 
+// Diagnostic (SW_ENGINE_NULL_KERNELS): an empty task with the same PDL
+// protocol, so a replay of the captured topology measures the graph's own
+// issue / dependency floor.
+__global__ void null_task_kernel() {
+  pdl_trigger();
+  pdl_wait();
+}
+
+int launch_null(void* stream) {
+  return (int)launch_k(null_task_kernel, dim3(1), dim3(32), 0, reinterpret_cast<cudaStream_t>(stream), 1);
+}
+
 }  // namespace sw

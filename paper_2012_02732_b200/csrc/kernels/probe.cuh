@@ -4,7 +4,7 @@
 //
 // Per launch: the first CTA to start stamps start[launch], the last CTA to
 // finish stamps end[launch] (launches counted modulo 16); CTA (0,0,0) also
-// stamps the phase points pt[i] of the kernel it runs (last launch wins).
+// stamps the phase points pt[i] (clock64) of the kernel it runs (last launch wins).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,8 +29,9 @@ __device__ __forceinline__ unsigned long long probe_time() {
   return t;
 }
 
+// phase points in SM clock cycles (globaltimer ticks in 256 ns steps here)
 __device__ __forceinline__ void probe_pt(int i) {
-  if (threadIdx.x == 0 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) g_probe.pt[i] = probe_time();
+  if (threadIdx.x == 0 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) g_probe.pt[i] = clock64();
 }
 
 __device__ __forceinline__ void probe_begin() {
@@ -45,13 +46,13 @@ __device__ __forceinline__ void probe_begin() {
 // call where every thread of the CTA passes, after its last store
 __device__ __forceinline__ void probe_end() {
   __syncthreads();
+  probe_pt(15);
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned n = gridDim.x * gridDim.y * gridDim.z;
     const unsigned f = atomicAdd(&g_probe.finished, 1u);
     if (f % n == n - 1) g_probe.end[(f / n) & 15] = probe_time();
   }
-  probe_pt(15);
 }
 
 // host side: every translation unit registers its own buffer

@@ -237,34 +237,43 @@ struct SepTmaGeo {
   int CBW;     // weight rows per box (≤ 256) and boxes
   int NCW;
   int QT;      // column tiles per output row
+  int CS;      // depthwise split: the column blocks of a row tile form a cluster of CS CTAs,
+  int Cs;      //   rank r computes the depthwise for channels [r*Cs, (r+1)*Cs)
   int o_bs, o_wd, o_bdw, o_bpw, o_x, o_d, o_r, o_bar;  // smem offsets (floats)
   uint32_t bytes_const, bytes_act;
 };
 
-template <int KS, int BM, int BN>
+template <int KS, int SW, int BM, int BN>
 __global__ void __launch_bounds__(SEP_THREADS)
 sepconv_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tw,
                    const __grid_constant__ CUtensorMap tres, SepArgs a, SepTmaGeo g) {
   static_assert(BN % 32 == 0 && BM % 4 == 0, "tile");
-  constexpr int JN = BN / 32;  // columns per lane
+  constexpr int JN = BN / 32;              // pointwise columns per lane
+  constexpr int PXT = 2;                   // depthwise output pixels per thread (row neighbours)
+  constexpr int SPAN = (PXT - 1) * SW + KS;  // input columns they read per filter row
   extern __shared__ __align__(128) float smem[];
   float* Bs = smem + g.o_bs;
   float* Wd = smem + g.o_wd;
   float* bdw = smem + g.o_bdw;
   float* bpw = smem + g.o_bpw;
   float* Xs = smem + g.o_x;
-  float* D = smem + g.o_d;
+  float* D = smem + g.o_d;  // [C][BM]
   float* Rs = smem + g.o_r;
   float* Pt = Xs;  // warp partials reuse the patch once the depthwise is done
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + g.o_bar);
-  const uint32_t bar_c = su32(&bars[0]), bar_a = su32(&bars[1]);
+  const uint32_t bar_c = su32(&bars[0]), bar_a = su32(&bars[1]), bar_d = su32(&bars[2]);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int qt = blockIdx.x % g.QT;
   const int rowi = blockIdx.x / g.QT;  // nb * P + p
   const int p = rowi % a.P, nb = rowi / a.P;
   const int q0 = qt * BM;
-  const int n0 = blockIdx.y * BN;
+  const int cb = blockIdx.y + blockIdx.z;  // column block (grid y, or cluster z when CS > 1)
+  const int n0 = cb * BN;
   const int C = a.C;
+  const int CS = g.CS;
+  const int me = CS > 1 ? (int)cluster_rank() : 0;
+  const int c_lo = CS > 1 ? me * g.Cs : 0;                   // this CTA's depthwise channels
+  const int c_n = CS > 1 ? max(0, min(g.Cs, C - c_lo)) : C;
   probe_begin();
 
   if (tid == 0) {
@@ -272,8 +281,11 @@ sepconv_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constan
     prefetch_tmap(&tw);
     mbar_init1(bar_c);
     mbar_init1(bar_a);
+    mbar_init1(bar_d);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async_cta();
+    // the peers push their depthwise slices into D: every channel but mine
+    if (CS > 1) mbar_expect_tx(bar_d, (uint32_t)((C - c_n) * BM * 4));
     mbar_expect_tx(bar_c, g.bytes_const + (a.b_pw ? (uint32_t)(min(BN, a.K - n0) * 4) : 0u));
 #pragma unroll 1
     for (int j = 0; j < g.NCW; ++j) tma_load_2d(su32(Bs + j * g.CBW * BN), &tw, n0, j * g.CBW, bar_c);
@@ -281,15 +293,17 @@ sepconv_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constan
     if (a.b_dw) bulk_g2s(su32(bdw), a.b_dw, (uint32_t)(C * 4), bar_c);
     if (a.b_pw) bulk_g2s(su32(bpw), a.b_pw + n0, (uint32_t)(min(BN, a.K - n0) * 4), bar_c);
   }
+  if (CS > 1) cluster_arrive_relaxed();  // my barriers are initialised (peers wait before pushing)
   pdl_trigger();
   probe_pt(1);
   pdl_wait();
   probe_pt(2);
   if (tid == 0) {
     mbar_expect_tx(bar_a, g.bytes_act);
-    const int iw0 = q0 * a.sw - a.pw, ih0 = p * a.sh - a.ph;
+    const int iw0 = q0 * SW - a.pw, ih0 = p * a.sh - a.ph;
 #pragma unroll 1
-    for (int j = 0; j < g.NCH; ++j) tma_load_4d(su32(Xs + j * KS * g.PCW * g.CB), &tin, j * g.CB, iw0, ih0, nb, bar_a);
+    for (int j = 0; j < g.NCH; ++j)
+      tma_load_4d(su32(Xs + j * KS * g.PCW * g.CB), &tin, c_lo + j * g.CB, iw0, ih0, nb, bar_a);
     if (a.has_res) tma_load_4d(su32(Rs), &tres, n0, q0, p, nb, bar_a);
   }
   __syncthreads();  // barrier inits visible before anyone polls them
@@ -297,37 +311,83 @@ sepconv_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constan
   mbar_wait_parity(bar_a, 0);
   probe_pt(3);
 
-  // ---- depthwise: D[c][px] ----
-  const int C4 = C >> 2;
+  // shared ReLU applied once over the patch (not once per tap use)
+  if (a.pre_relu) {
+    float4* x4 = reinterpret_cast<float4*>(Xs);
+    const int n4 = g.NCH * KS * g.PCW * g.CB / 4;
 #pragma unroll 1
-  for (int e = tid; e < BM * C4; e += SEP_THREADS) {
-    const int cg = e % C4, px = e / C4;
-    const int c = cg * 4;
-    const int ch = c / g.CB, cc = c - ch * g.CB;
-    const float* xb = Xs + (ch * KS * g.PCW + px * a.sw) * g.CB + cc;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = tid; i < n4; i += SEP_THREADS) {
+      float4 v = x4[i];
+      v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+      x4[i] = v;
+    }
+    __syncthreads();
+  }
+  probe_pt(8);
+
+  // ---- depthwise for channels [c_lo, c_lo + c_n): D[c][px] ----
+  // A thread owns 4 channels x PXT row neighbours: per filter row it loads the
+  // SPAN input columns and KS filter taps once and reuses them in registers
+  // (shared-memory bandwidth, not FMAs, bounds this phase).
+  const int C4 = c_n >> 2;
+  constexpr int PG = BM / PXT;
+#pragma unroll 1
+  for (int e = tid; e < PG * C4; e += SEP_THREADS) {
+    const int cg = e % C4, pg = e / C4;
+    const int cl = cg * 4;  // channel within the slice
+    const int c = c_lo + cl;
+    const int ch = cl / g.CB, cc = cl - ch * g.CB;
+    const float* xb = Xs + (ch * KS * g.PCW + pg * PXT * SW) * g.CB + cc;
+    const float* wb = Wd + c;
+    float4 acc[PXT];
+#pragma unroll
+    for (int j = 0; j < PXT; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int r = 0; r < KS; ++r) {
+      float4 xr[SPAN], wr[KS];
 #pragma unroll
-      for (int s2 = 0; s2 < KS; ++s2) {
-        float4 x = *reinterpret_cast<const float4*>(xb + (r * g.PCW + s2) * g.CB);
-        const float4 w = *reinterpret_cast<const float4*>(Wd + (r * KS + s2) * C + c);
-        if (a.pre_relu) {
-          x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+      for (int t = 0; t < SPAN; ++t) xr[t] = *reinterpret_cast<const float4*>(xb + (r * g.PCW + t) * g.CB);
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) wr[s2] = *reinterpret_cast<const float4*>(wb + (r * KS + s2) * C);
+#pragma unroll
+      for (int j = 0; j < PXT; ++j)
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) {
+          const float4 x = xr[j * SW + s2];
+          acc[j].x = fmaf(x.x, wr[s2].x, acc[j].x);
+          acc[j].y = fmaf(x.y, wr[s2].y, acc[j].y);
+          acc[j].z = fmaf(x.z, wr[s2].z, acc[j].z);
+          acc[j].w = fmaf(x.w, wr[s2].w, acc[j].w);
         }
-        acc.x = fmaf(x.x, w.x, acc.x);
-        acc.y = fmaf(x.y, w.y, acc.y);
-        acc.z = fmaf(x.z, w.z, acc.z);
-        acc.w = fmaf(x.w, w.w, acc.w);
-      }
     }
-    if (a.b_dw) acc = f4add(acc, *reinterpret_cast<const float4*>(bdw + c));
-    D[(c + 0) * BM + px] = apply_act(acc.x, a.dw_act);
-    D[(c + 1) * BM + px] = apply_act(acc.y, a.dw_act);
-    D[(c + 2) * BM + px] = apply_act(acc.z, a.dw_act);
-    D[(c + 3) * BM + px] = apply_act(acc.w, a.dw_act);
+    const float4 bd = a.b_dw ? *reinterpret_cast<const float4*>(bdw + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < PXT; ++j) {
+      const int px = pg * PXT + j;
+      D[(c + 0) * BM + px] = apply_act(acc[j].x + bd.x, a.dw_act);
+      D[(c + 1) * BM + px] = apply_act(acc[j].y + bd.y, a.dw_act);
+      D[(c + 2) * BM + px] = apply_act(acc[j].z + bd.z, a.dw_act);
+      D[(c + 3) * BM + px] = apply_act(acc[j].w + bd.w, a.dw_act);
+    }
   }
-  __syncthreads();
+  probe_pt(9);
+  if (CS > 1) {
+    // push my D slice into every peer's D (bulk DSMEM copies completing on
+    // the peer's mbarrier), then wait for theirs — no cluster-wide barrier
+    fence_proxy_async_cta();
+    __syncthreads();
+    cluster_wait();  // every peer initialised its barriers
+    if (tid == 0 && c_n > 0) {
+      const uint32_t src = su32(D + c_lo * BM);
+#pragma unroll 1
+      for (int r = 0; r < CS; ++r)
+        if (r != me) bulk_s2peer(mapa_rank(src, (uint32_t)r), src, (uint32_t)(c_n * BM * 4), mapa_rank(bar_d, (uint32_t)r));
+      bulk_commit();
+    }
+    mbar_wait_parity(bar_d, 0);
+  } else {
+    __syncthreads();
+  }
   probe_pt(4);
 
   // ---- pointwise: warp w sums channels [w*C/8, (w+1)*C/8) for the whole tile ----
@@ -378,6 +438,8 @@ sepconv_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constan
       *reinterpret_cast<float4*>(a.out + nb * a.epi.out_sn + p * a.epi.out_sh + q * a.epi.out_sw + n) =
           act4(v, a.act);
   }
+  probe_pt(6);
+  if (CS > 1 && tid == 0) bulk_wait_read0();  // my pushes have read D before the CTA exits
   probe_end();
 }
 
@@ -469,6 +531,17 @@ static bool sep_tma_geo(const SepArgs& a, const sw_op_desc& op, int bm, int bn, 
   if (g->PCW > 256) return false;
   g->CB = a.C <= 256 ? a.C : 256;
   g->NCH = (a.C + g->CB - 1) / g->CB;
+  g->CS = 1;
+  g->Cs = a.C;
+  if (op.params[SP_SPLIT_K] > 1) {  // cluster-split depthwise over the column blocks
+    const int cs = (int)cdiv(a.K, bn);
+    if (cs < 2 || cs > 8) return false;
+    g->CS = cs;
+    g->Cs = (int)cdiv(cdiv(a.C, cs), 4) * 4;
+    if (g->Cs > 256) return false;
+    g->CB = g->Cs;
+    g->NCH = 1;
+  }
   g->CBW = a.C <= 256 ? a.C : 256;
   g->NCW = (a.C + g->CBW - 1) / g->CBW;
   g->QT = (a.Q + bm - 1) / bm;
@@ -492,7 +565,7 @@ static bool sep_tma_geo(const SepArgs& a, const sw_op_desc& op, int bm, int bn, 
   return true;
 }
 
-template <int KS, int BM, int BN>
+template <int KS, int SW, int BM, int BN>
 static cudaError_t launch_sep_tma_t(const SepArgs& a, const sw_op_desc& op, cudaStream_t st) {
   SepTmaGeo g;
   size_t smem = 0;
@@ -518,19 +591,31 @@ static cudaError_t launch_sep_tma_t(const SepArgs& a, const sw_op_desc& op, cuda
   } else {
     tres = tw;  // unused
   }
+  if (g.CS > 1) {  // one cluster (along z) per row tile
+    dim3 grid((unsigned)(a.N * a.P * g.QT), 1, (unsigned)g.CS);
+    return launch_k(sepconv_tma_kernel<KS, SW, BM, BN>, grid, dim3(SEP_THREADS), smem, st, (unsigned)g.CS, tin, tw,
+                    tres, a, g);
+  }
   dim3 grid((unsigned)(a.N * a.P * g.QT), (unsigned)cdiv(a.K, BN));
-  return launch_k(sepconv_tma_kernel<KS, BM, BN>, grid, dim3(SEP_THREADS), smem, st, 1, tin, tw, tres, a, g);
+  return launch_k(sepconv_tma_kernel<KS, SW, BM, BN>, grid, dim3(SEP_THREADS), smem, st, 1, tin, tw, tres, a, g);
+}
+
+template <int KS, int SW>
+static cudaError_t launch_sep_tma_ksw(int v, const SepArgs& a, const sw_op_desc& op, cudaStream_t st) {
+  switch (v) {
+    case 0: return launch_sep_tma_t<KS, SW, 4, 32>(a, op, st);
+    case 1: return launch_sep_tma_t<KS, SW, 8, 32>(a, op, st);
+    case 2: return launch_sep_tma_t<KS, SW, 8, 64>(a, op, st);
+    case 3: return launch_sep_tma_t<KS, SW, 16, 32>(a, op, st);
+    default: return launch_sep_tma_t<KS, SW, 16, 64>(a, op, st);
+  }
 }
 
 template <int KS>
 static cudaError_t launch_sep_tma_ks(int v, const SepArgs& a, const sw_op_desc& op, cudaStream_t st) {
-  switch (v) {
-    case 0: return launch_sep_tma_t<KS, 4, 32>(a, op, st);
-    case 1: return launch_sep_tma_t<KS, 8, 32>(a, op, st);
-    case 2: return launch_sep_tma_t<KS, 8, 64>(a, op, st);
-    case 3: return launch_sep_tma_t<KS, 16, 32>(a, op, st);
-    default: return launch_sep_tma_t<KS, 16, 64>(a, op, st);
-  }
+  if (a.sw == 1) return launch_sep_tma_ksw<KS, 1>(v, a, op, st);
+  if (a.sw == 2) return launch_sep_tma_ksw<KS, 2>(v, a, op, st);
+  return cudaErrorInvalidValue;
 }
 
 int launch_sepconv(const sw_op_desc& op, void* stream) {
@@ -564,13 +649,18 @@ static void init_sep_ks() {
   cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 32, 64, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
 }
 
+template <int KS, int SW>
+static void init_sep_tma_ksw() {
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, SW, 4, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, SW, 8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, SW, 8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, SW, 16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  cudaFuncSetAttribute(sepconv_tma_kernel<KS, SW, 16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+}
 template <int KS>
 static void init_sep_tma_ks() {
-  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 4, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
-  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 8, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
-  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 8, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
-  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
-  cudaFuncSetAttribute(sepconv_tma_kernel<KS, 16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  init_sep_tma_ksw<KS, 1>();
+  init_sep_tma_ksw<KS, 2>();
 }
 
 void init_sep_kernels() {

@@ -98,7 +98,7 @@ struct sw_engine {
   std::vector<sw_op_desc> ops;
   uint64_t host_in = 0, dev_in = 0, host_out = 0, dev_out = 0;
   int64_t in_bytes = 0, out_bytes = 0;
-  uint32_t flags = 0;  // SW_ENGINE_PDL
+  uint32_t flags = 0;  // SW_ENGINE_PDL | SW_ENGINE_NULL_KERNELS
   Slot slots[kSlots];
 };
 
@@ -260,7 +260,7 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     cudaStream_t st = e->streams[s];
     if (op_kind[k] == SW_OP_LAUNCH) {
       int64_t t = op_arg[k];
-      rc = launch_task(e->ops[t], st);
+      rc = (e->flags & SW_ENGINE_NULL_KERNELS) ? (sw::launch_null(st) ? SW_CUDA_ERROR : 0) : launch_task(e->ops[t], st);
       if (rc) return abort_capture(rc);
       cudaStreamCaptureStatus status;
       const cudaGraphNode_t* deps = nullptr;

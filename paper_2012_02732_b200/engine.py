@@ -546,7 +546,10 @@ class Engine:
             trial = N.OpDesc()
             C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
             if t.kind == "sepconv":
-                cands = [(K_SEPCONV, v, 1) for v in range(len(SEP_TILES))]
+                cands = [(K_SEPCONV, v, 1) for v in SEP_TILES]
+                # TMA kernel with the depthwise split over a cluster of the column blocks
+                cands += [(K_SEPCONV, v, 2) for v, (bm, bn) in SEP_TILES.items()
+                          if v >= SEP_TMA_FIRST and 2 <= math.ceil(K / bn) <= 8]
             else:
                 cands = conv_candidates(M, K, Kdim, p[SP_R], p[SP_S], (p[SP_PAD_H], p[SP_PAD_W]))
             for kind, variant, split in cands:
@@ -572,11 +575,15 @@ class Engine:
         o = prog.output_view.st
         return (o.n, o.c, o.h, o.w) if (o.h * o.w > 1) else (o.n, o.c)
 
-    def recapture(self, pdl: bool | None = None):
-        """Re-capture every slot (e.g. after toggling programmatic dependent launch)."""
+    def recapture(self, pdl: bool | None = None, null_kernels: bool = False):
+        """Re-capture every slot (e.g. after toggling programmatic dependent launch).
+
+        ``null_kernels=True`` captures an empty kernel per task instead (same
+        topology and PDL protocol): a diagnostic replay that measures the
+        graph's own issue / dependency floor.  Recapture again to restore."""
         if pdl is not None:
             self.pdl = pdl
-            N.check(N.lib().sw_engine_set_flags(self._h, 1 if pdl else 0))
+        N.check(N.lib().sw_engine_set_flags(self._h, (1 if self.pdl else 0) | (2 if null_kernels else 0)))
         self._capture(SLOT_MULTI_IO, self.schedule, True)
         self._capture(SLOT_SINGLE_IO, self.schedule_single, True)
         self._capture(SLOT_MULTI, self.schedule, False)

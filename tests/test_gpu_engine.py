@@ -169,14 +169,21 @@ class SepBlock(nn.Module):
         return self.pool(y)
 
 
+@pytest.mark.parametrize("split", [1, 2])
 @pytest.mark.parametrize("variant", range(6, 11))
 @pytest.mark.parametrize("c,k,s,h,res", [(44, 5, 1, 14, True), (176, 3, 1, 7, True), (88, 7, 2, 14, False),
-                                         (44, 3, 2, 28, False), (32, 7, 1, 9, True)])
-def test_sepconv_tma_variants(variant, c, k, s, h, res):
-    """TMA-staged fused sepconv (patch / weights / residual by tensor maps), forced."""
+                                         (44, 3, 2, 28, False), (32, 7, 1, 9, True), (264, 3, 1, 7, False)])
+def test_sepconv_tma_variants(variant, split, c, k, s, h, res):
+    """TMA-staged fused sepconv (patch / weights / residual by tensor maps), forced;
+    split=2: the depthwise is split over a cluster of the column blocks (DSMEM gather)."""
+    import math
     from paper_2012_02732_b200 import _native as N
-    from paper_2012_02732_b200.engine import K_SEPCONV, SLOT_MULTI
+    from paper_2012_02732_b200.engine import K_SEPCONV, SEP_TILES, SLOT_MULTI, SP_SPLIT_K
     from paper_2012_02732_b200.networks import randomize_bn
+    if split == 2 and not 2 <= math.ceil(c / SEP_TILES[variant][1]) <= 8:
+        pytest.skip("cluster split needs 2..8 column blocks")
+    if c > 256 and split == 1 and SEP_TILES[variant] == (16, 64):
+        pytest.skip("exceeds 227 KB of shared memory (the kernel refuses it; the autotuner skips it)")
     torch.manual_seed(5)
     m = SepBlock(c, k, s, res).eval()
     randomize_bn(m, seed=2)
@@ -187,6 +194,7 @@ def test_sepconv_tma_variants(variant, c, k, s, h, res):
     idx = [i for i, d in enumerate(eng.ops) if d.kind == K_SEPCONV]
     assert len(idx) == 1
     eng.ops[idx[0]].variant = variant
+    eng.ops[idx[0]].params[SP_SPLIT_K] = split
     N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.ops), eng.ops))
     eng._capture(SLOT_MULTI, eng.schedule, False)
     eng.load_input_device(x)

@@ -9,7 +9,7 @@ way time_op / the autotuner time it).  Printed per task:
     one launch's end to the next one's start (negative = PDL overlap);
   * phases of CTA (0,0,0) in the last launch, µs after its start:
     1 constants issued, 2 PDL wait returned, 3 first operands in smem,
-    4 main loop / depthwise done, 5 GEMM done, 15 CTA end.
+    4 main loop / depthwise done, 5 GEMM done, 15 CTA end (clock64 → µs at --sm-mhz).
 """
 
 from __future__ import annotations
@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--limit", type=int, default=12)
     ap.add_argument("--reps", type=int, default=4)
     ap.add_argument("--tuning-cache", default=None)
+    ap.add_argument("--no-pdl", action="store_true", help="time the chains without programmatic dependent launch")
+    ap.add_argument("--sm-mhz", type=float, default=1965.0, help="SM clock for the clock64 phase stamps")
     a = ap.parse_args()
 
     import numpy as np
@@ -49,6 +51,8 @@ def main():
     model, shape = build_model(a.config)
     x = example_input(shape, batch=a.batch)
     eng = Engine(model, tuning_cache=a.tuning_cache).prepare(x)
+    if a.no_pdl:
+        N.check(lib.sw_engine_set_flags(eng._h, 0))
     per = eng.profile_tasks(reps=20)
     if a.tasks:
         tids = [int(t) for t in a.tasks.split(",")]
@@ -73,7 +77,7 @@ def main():
         spans = [(ends[i] - starts[i]) / 1e3 for i in timed]
         gaps = [(starts[j] - ends[i]) / 1e3 for i, j in zip(timed[:-1], timed[1:])]
         pts = v[:16]
-        ph = {i: (pts[i] - pts[0]) / 1e3 for i in range(1, 16) if pts[i]}
+        ph = {i: (pts[i] - pts[0]) / (a.sm_mhz * 1e-3) / 1e3 for i in range(1, 16) if pts[i]}
         print(f"task {tid:4d} {t.kind:7s} k=({d.kind},{d.variant},split {d.params[30]}) "
               f"time_op {us.value:6.2f}us  span {np.mean(spans) if spans else 0:6.2f}us "
               f"gap {np.mean(gaps) if gaps else 0:+6.2f}us  CTAs {ctas}  "

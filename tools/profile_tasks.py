@@ -58,6 +58,11 @@ def main():
     gm, hm = eng.time_replay(multi=True, iters=100)
     gs, hs = eng.time_replay(multi=False, iters=100)
     print(f"replay multi {gm:.1f} us  single {gs:.1f} us  host launch {hm:.2f} us")
+    eng.recapture(null_kernels=True)
+    fm, _ = eng.time_replay(multi=True, iters=100)
+    fs, _ = eng.time_replay(multi=False, iters=100)
+    eng.recapture()
+    print(f"graph floor (empty kernel per task, same topology): multi {fm:.1f} us  single {fs:.1f} us")
     # simulator in the loop: measured durations (ns) into the reference replay model
     g = eng.graph
     dur = {t.tid: max(1, int(round(per[t.tid] * 1000))) for t in eng.program.tasks}
