@@ -251,6 +251,17 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
 #define SW_ENGINE_NULL_KERNELS 2u
 int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
+/* ---- training step (paper_2012_02732_b200/train.py) ---- */
+/* One more captured H2D copy in the with_io slots (labels next to images). */
+int sw_engine_add_input(sw_engine* e, uint64_t host, uint64_t dev, int64_t bytes);
+/* Bind NCCL at run time (dlopen of `path`, or "libnccl.so.2" when NULL/empty). */
+int sw_nccl_load(const char* path);
+/* ncclGetUniqueId into a caller buffer of 128 bytes (rank 0 broadcasts it). */
+int sw_nccl_unique_id(char* out128);
+/* Data-parallel communicator for the engine's K_ALLREDUCE tasks, which are
+ * captured into the training graph as ncclAllReduce(avg) on their stream. */
+int sw_engine_nccl_init(sw_engine* e, int32_t nranks, int32_t rank, const char* id128);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,10 @@
 // tails→memcpy; sw_engine_graph_topology exposes it for that check.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <chrono>
+#include <cstring>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -100,7 +103,37 @@ struct sw_engine {
   int64_t in_bytes = 0, out_bytes = 0;
   uint32_t flags = 0;  // SW_ENGINE_PDL | SW_ENGINE_NULL_KERNELS
   Slot slots[kSlots];
+  // extra captured H2D copies (training: labels next to the images)
+  std::vector<uint64_t> extra_host, extra_dev;
+  std::vector<int64_t> extra_bytes;
+  void* nccl_comm = nullptr;  // ncclComm_t of the data-parallel group (K_ALLREDUCE)
+  int nccl_ranks = 0;
 };
+
+// ---------------------------------------------------------------------------
+// NCCL, bound at run time (dlopen) so the library still loads — planner only —
+// on hosts without NCCL.  Prototypes restate nccl.h (NCCL 2.28, the copy torch
+// bundles under site-packages/nvidia/nccl); enum values from that header.
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  typedef int (*GetUniqueId)(void* id);
+  typedef int (*CommInitRank)(void** comm, int nranks, const char id[128], int rank);
+  typedef int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  typedef int (*CommDestroy)(void*);
+  typedef const char* (*ErrStr)(int);
+  void* h = nullptr;
+  GetUniqueId get_unique_id = nullptr;
+  void* comm_init_rank = nullptr;  // by-value ncclUniqueId: called through a struct wrapper
+  AllReduce all_reduce = nullptr;
+  CommDestroy comm_destroy = nullptr;
+  ErrStr err = nullptr;
+};
+NcclApi g_nccl;
+struct NcclId { char internal[128]; };
+typedef int (*CommInitRankV)(void** comm, int nranks, NcclId id, int rank);
+constexpr int kNcclFloat32 = 7, kNcclSum = 0, kNcclAvg = 4;
+}  // namespace
 
 namespace {
 
@@ -114,9 +147,26 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
 
-int launch_task(const sw_op_desc& op, cudaStream_t st) {
+int launch_task(sw_engine* e, const sw_op_desc& op, cudaStream_t st) {
   int rc = 0;
   switch (op.kind) {
+    case sw::K_BN_STATS:
+    case sw::K_BN_APPLY:
+    case sw::K_BN_BWD_REDUCE:
+    case sw::K_BN_BWD_APPLY:
+    case sw::K_DW_DGRAD:
+    case sw::K_DW_WGRAD:
+    case sw::K_GEMM:
+    case sw::K_XENT:
+    case sw::K_SGD:
+    case sw::K_EW_BWD: rc = sw::launch_train(op, st); break;
+    case sw::K_ALLREDUCE: {
+      if (!e->nccl_comm || !g_nccl.all_reduce) return sw::fail(SW_CUDA_ERROR, "allreduce task without an NCCL communicator");
+      int r = g_nccl.all_reduce(reinterpret_cast<const void*>(op.ptrs[0]), reinterpret_cast<void*>(op.ptrs[0]),
+                                (size_t)op.params[0], kNcclFloat32, kNcclAvg, e->nccl_comm, st);
+      if (r != 0) return sw::fail(SW_CUDA_ERROR, std::string("ncclAllReduce: ") + (g_nccl.err ? g_nccl.err(r) : "?"));
+      return SW_OK;
+    }
     case sw::K_CONV: rc = sw::launch_conv(op, st); break;
     case sw::K_CONV_TC: rc = sw::launch_conv_tc(op, st); break;
     case sw::K_DWCONV: rc = sw::launch_dwconv(op, st); break;
@@ -188,6 +238,7 @@ int sw_engine_destroy(sw_engine* e) {
   cudaEventDestroy(e->t0);
   cudaEventDestroy(e->t1);
   cudaStreamDestroy(e->launch);
+  if (e->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(e->nccl_comm);
   delete e;
   return SW_OK;
 }
@@ -245,6 +296,11 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
                           (size_t)e->in_bytes, cudaMemcpyHostToDevice, origin);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture H2D"));
   }
+  for (size_t i = 0; with_io && i < e->extra_host.size(); ++i) {
+    err = cudaMemcpyAsync(reinterpret_cast<void*>(e->extra_dev[i]), reinterpret_cast<const void*>(e->extra_host[i]),
+                          (size_t)e->extra_bytes[i], cudaMemcpyHostToDevice, origin);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture extra H2D"));
+  }
   err = cudaEventRecord(e->fork, origin);
   if (err != cudaSuccess) return abort_capture(cuda_fail(err, "fork record"));
   for (int64_t s = 0; s < n_streams; ++s) {
@@ -260,7 +316,7 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     cudaStream_t st = e->streams[s];
     if (op_kind[k] == SW_OP_LAUNCH) {
       int64_t t = op_arg[k];
-      rc = (e->flags & SW_ENGINE_NULL_KERNELS) ? (sw::launch_null(st) ? SW_CUDA_ERROR : 0) : launch_task(e->ops[t], st);
+      rc = (e->flags & SW_ENGINE_NULL_KERNELS) ? (sw::launch_null(st) ? SW_CUDA_ERROR : 0) : launch_task(e, e->ops[t], st);
       if (rc) return abort_capture(rc);
       cudaStreamCaptureStatus status;
       const cudaGraphNode_t* deps = nullptr;
@@ -332,7 +388,7 @@ int sw_engine_time_replay(sw_engine* e, int32_t slot, int32_t iters, double* out
 int sw_engine_launch_op(sw_engine* e, int64_t index) {
   if (index < 0 || index >= (int64_t)e->ops.size()) return sw::fail(SW_VALUE_ERROR, "op index out of range");
   sw::g_launch_pdl = (e->flags & SW_ENGINE_PDL) != 0;
-  int rc = launch_task(e->ops[index], e->launch);
+  int rc = launch_task(e, e->ops[index], e->launch);
   sw::g_launch_pdl = false;
   return rc;
 }
@@ -405,13 +461,13 @@ int sw_engine_profile_ops(sw_engine* e, int64_t n, const int64_t* order, int32_t
 int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* out_us) {
   if (reps < 1) reps = 1;
   CU(cudaStreamSynchronize(e->launch));
-  int rc = launch_task(*op, e->launch);  // validates the launch outside capture
+  int rc = launch_task(e, *op, e->launch);  // validates the launch outside capture
   if (rc) return rc;
   CU(cudaStreamSynchronize(e->launch));
   cudaGraph_t g = nullptr;
   CU(cudaStreamBeginCapture(e->launch, cudaStreamCaptureModeThreadLocal));
   sw::g_launch_pdl = (e->flags & SW_ENGINE_PDL) != 0;  // same edges as the replayed graph
-  for (int r = 0; r < reps && rc == 0; ++r) rc = launch_task(*op, e->launch);
+  for (int r = 0; r < reps && rc == 0; ++r) rc = launch_task(e, *op, e->launch);
   sw::g_launch_pdl = false;
   cudaError_t ce = cudaStreamEndCapture(e->launch, &g);
   if (rc) {
@@ -433,6 +489,48 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
   cudaGraphExecDestroy(ex);
   if (ce != cudaSuccess) return cuda_fail(ce, "time_op replay");
   *out_us = (double)ms * 1000.0 / reps;
+  return SW_OK;
+}
+
+int sw_engine_add_input(sw_engine* e, uint64_t host, uint64_t dev, int64_t bytes) {
+  e->extra_host.push_back(host);
+  e->extra_dev.push_back(dev);
+  e->extra_bytes.push_back(bytes);
+  return SW_OK;
+}
+
+int sw_nccl_load(const char* path) {
+  if (g_nccl.h) return SW_OK;
+  void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return sw::fail(SW_CUDA_ERROR, std::string("dlopen NCCL: ") + dlerror());
+  g_nccl.get_unique_id = (NcclApi::GetUniqueId)dlsym(h, "ncclGetUniqueId");
+  g_nccl.comm_init_rank = dlsym(h, "ncclCommInitRank");
+  g_nccl.all_reduce = (NcclApi::AllReduce)dlsym(h, "ncclAllReduce");
+  g_nccl.comm_destroy = (NcclApi::CommDestroy)dlsym(h, "ncclCommDestroy");
+  g_nccl.err = (NcclApi::ErrStr)dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.get_unique_id || !g_nccl.comm_init_rank || !g_nccl.all_reduce || !g_nccl.comm_destroy)
+    return sw::fail(SW_CUDA_ERROR, "NCCL library lacks the expected symbols");
+  g_nccl.h = h;
+  return SW_OK;
+}
+
+int sw_nccl_unique_id(char* out128) {
+  if (!g_nccl.h) return sw::fail(SW_CUDA_ERROR, "NCCL not loaded (sw_nccl_load)");
+  int r = g_nccl.get_unique_id(out128);
+  if (r != 0) return sw::fail(SW_CUDA_ERROR, std::string("ncclGetUniqueId: ") + (g_nccl.err ? g_nccl.err(r) : "?"));
+  return SW_OK;
+}
+
+int sw_engine_nccl_init(sw_engine* e, int32_t nranks, int32_t rank, const char* id128) {
+  if (!g_nccl.h) return sw::fail(SW_CUDA_ERROR, "NCCL not loaded (sw_nccl_load)");
+  CU(cudaSetDevice(e->device));
+  NcclId id;
+  memcpy(id.internal, id128, 128);
+  void* comm = nullptr;
+  int r = reinterpret_cast<CommInitRankV>(g_nccl.comm_init_rank)(&comm, nranks, id, rank);
+  if (r != 0) return sw::fail(SW_CUDA_ERROR, std::string("ncclCommInitRank: ") + (g_nccl.err ? g_nccl.err(r) : "?"));
+  e->nccl_comm = comm;
+  e->nccl_ranks = nranks;
   return SW_OK;
 }
 

@@ -22,7 +22,71 @@ enum KernelKind : int32_t {
   K_CONV_TC = 6,     // dense conv / GEMM on tcgen05 tensor cores (3xTF32)
   K_CONCAT = 7,      // unfused channel concat of up to 7 dense NHWC inputs
   K_SEPCONV = 8,     // fused depthwise k x k → pointwise 1x1
+  // training (csrc/kernels/train.cu; paper_2012_02732_b200/train.py)
+  K_BN_STATS = 9,       // batch statistics (+ running-stat update) of an NHWC map
+  K_BN_APPLY = 10,      // normalise + affine (+ residual) + act
+  K_BN_BWD_REDUCE = 11, // dgamma / dbeta (through the activation derivative)
+  K_BN_BWD_APPLY = 12,  // dx of batch norm (+ accumulate)
+  K_DW_DGRAD = 13,      // depthwise conv input gradient (+ accumulate)
+  K_DW_WGRAD = 14,      // depthwise conv weight gradient
+  K_GEMM = 15,          // strided / implicit-im2col GEMM with deterministic split-K
+  K_XENT = 16,          // softmax cross-entropy: mean loss + dlogits
+  K_SGD = 17,           // SGD with momentum + weight decay over the flat parameters
+  K_ALLREDUCE = 18,     // NCCL average of the flat gradient buffer (engine-owned comm)
+  K_EW_BWD = 19,        // activation / broadcast-mul backward (EfficientNet SE)
 };
+
+// Batch-norm kinds (K_BN_*): params index
+enum BnParam : int {
+  BN_M = 0,      // pixels N*H*W
+  BN_C,          // channels
+  BN_HW,         // pixels per image (dOut broadcast decomposition)
+  BN_ACT,        // activation after the affine
+  BN_HAS_RES,    // APPLY: + residual (before act); BWD_APPLY: accumulate into res
+  BN_EPS,        // float bits
+  BN_MOMENTUM,   // float bits (running stats)
+  BN_GRID,       // CTAs of the reduce kinds (workspace = GRID * 2 * C doubles + ticket)
+  BN_DO_SN,      // dOut image stride
+  BN_DO_SP,      // dOut pixel stride (0 = broadcast over H*W, e.g. global-pool backward)
+  BN_DO_SCALE,   // float bits: dOut multiplier (1/HW for global-pool backward)
+  BN_LD,         // pixel stride of y / out / res
+};
+// STATS ptrs: 0 y, 1 stats out [mean C | invstd C], 2 running [mean C | var C], 7 ws
+// APPLY ptrs: 0 y, 1 stats, 2 gamma [gamma C | beta C], 3 res, 4 out
+// BWD_REDUCE ptrs: 0 dOut, 1 y, 2 stats, 3 gamma|beta, 4 dgamma|dbeta, 7 ws
+// BWD_APPLY ptrs: 0 dOut, 1 y, 2 stats, 3 gamma|beta, 4 dgamma|dbeta, 5 res, 6 out
+
+// K_DW_DGRAD / K_DW_WGRAD reuse the SpatialParam geometry (SP_N..SP_PAD_W, the
+// forward op's dims: input N,H,W,C → output P,Q); dense NHWC.
+// DGRAD ptrs: 0 dY, 1 dX out, 2 W [R][S][C], 4 res (SP_HAS_RES accumulate)
+// WGRAD ptrs: 0 dY, 1 dW out [R][S][C], 2 X, 5 ws; SP_SPLIT_K = CTAs
+// (workspace = CTAs * R*S*C floats + ticket)
+
+// K_GEMM: C[i,j] = sum_r A(i,r) B(r,j) (+ bias[j]) (+ res[i,j])
+enum GemmParam : int {
+  GM_M = 0, GM_N, GM_K,          // i < M, j < N, r < K
+  GM_A_I, GM_A_R,                // A(i,r) = A[i*a_i + r*a_r]
+  GM_B_R, GM_B_J,                // B(r,j) = B[r*b_r + j*b_j]  (GM_IM2COL = 0)
+  GM_C_I,                        // C[i*c_i + j]
+  GM_SPLIT,                      // split of r over gridDim.z (deterministic ticket reduce)
+  GM_HAS_RES,                    // accumulate: C = AB + res (res may alias C)
+  GM_IM2COL,                     // 1: B(r=pixel, j=(rr,ss,c)) gathered from a conv input
+  GM_X_N, GM_X_H, GM_X_W, GM_X_C, GM_X_P, GM_X_Q, GM_X_R, GM_X_S,
+  GM_X_STRIDE, GM_X_PAD,
+  GM_X_SN, GM_X_SH, GM_X_SW, GM_X_SC,
+};
+// ptrs: 0 A, 1 B, 2 C, 3 bias, 4 res, 5 ws (split > 1: split*tiles*64*64 floats + tiles tickets)
+
+// K_XENT params: 0 N, 1 classes, 2 logits row stride; ptrs 0 logits, 1 labels (int32),
+// 2 loss (1 float), 3 dlogits [N][classes]
+// K_SGD params: 0 n, 1 lr, 2 momentum, 3 weight decay (float bits); ptrs 0 params,
+// 1 grads, 2 momentum buffer
+// K_ALLREDUCE params: 0 count (floats); ptrs 0 buffer (in place)
+// K_EW_BWD params: 0 N, 1 HW, 2 C, 3 mode (0 act-backward: dx = dy*act'(z) [+res];
+// 1 mul-backward: dx = dy*s[n,c] [+res]; 2 mul-backward to the scale: ds[n,c] =
+// sum_hw dy*x, then act'(z_s) applied; 3 broadcast: dx = s[n,c]*scale [+res]
+// (global-pool backward)), 4 act, 5 has_res, 6 scale (float bits);
+// ptrs 0 dy, 1 z/x, 2 s, 3 res, 4 out, 5 z_s
 // K_CONCAT params: 0 N, 1 H, 2 W, 3 n_in, 4 C_total, 5 out channel stride,
 // 6 out pixel stride, 8.. C_i; ptrs 0..6 inputs, 7 output.
 
@@ -86,5 +150,6 @@ void init_simt_kernels();
 void init_pw_kernels();
 int launch_sepconv(const sw_op_desc& op, void* stream);
 void init_sep_kernels();
+int launch_train(const sw_op_desc& op, void* stream);  // K_BN_* .. K_SGD, K_EW_BWD
 
 }  // namespace sw

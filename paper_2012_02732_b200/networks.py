@@ -404,3 +404,33 @@ def build_model(name: str, seed: int = 0) -> tuple[nn.Module, tuple[int, ...]]:
 def example_input(shape, batch: int = 1, seed: int = 1) -> torch.Tensor:
     g = torch.Generator().manual_seed(seed)
     return torch.randn((batch,) + tuple(shape[1:]), generator=g)
+
+
+TRAIN_CONFIGS = ("mobilenet_v2", "efficientnet_b0")
+
+
+def build_train_model(name: str, seed: int = 0) -> nn.Module:
+    """CIFAR-10-shaped training model (BASELINE config 5): torchvision
+    MobileNetV2 / EfficientNet-B0 with 10 classes, random init, randomized BN
+    affine, train mode.  Dropout and stochastic depth are set to p = 0: their
+    RNG streams are not reproduced by the engine, and p = 0 keeps the step a
+    deterministic function of (weights, batch) for the parity gate."""
+    import torchvision.models as tvm
+    torch.manual_seed(seed)
+    if name == "mobilenet_v2":
+        model = tvm.mobilenet_v2(weights=None, num_classes=10, dropout=0.0)
+    elif name == "efficientnet_b0":
+        model = tvm.efficientnet_b0(weights=None, num_classes=10, dropout=0.0, stochastic_depth_prob=0.0)
+    else:
+        raise KeyError(name)
+    randomize_bn(model, seed)
+    return model.train()
+
+
+def train_batch(batch: int = 32, rank: int = 0, hw: int = 32):
+    """Synthetic CIFAR-10 batch: randn images, labels seeded 1000+rank."""
+    g = torch.Generator().manual_seed(1 + rank)
+    x = torch.randn((batch, 3, hw, hw), generator=g)
+    gl = torch.Generator().manual_seed(1000 + rank)
+    y = torch.randint(0, 10, (batch,), generator=gl)
+    return x, y

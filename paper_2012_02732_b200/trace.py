@@ -92,7 +92,8 @@ def _conv_node(name, conv: nn.Conv2d, x, shape, stride=None, pad=None, groups_ok
     cin = x.shape[1]
     k_out = w.shape[0]
     attrs = {"weight": w, "bias": b, "stride": stride or _pair(conv.stride),
-             "pad": pad if pad is not None else _pair(conv.padding), "k": tuple(w.shape[2:])}
+             "pad": pad if pad is not None else _pair(conv.padding), "k": tuple(w.shape[2:]),
+             "module": conv}
     if g == 1:
         kind = "conv"
     elif g == cin == k_out:
@@ -146,13 +147,14 @@ def trace_model(model: nn.Module, example: torch.Tensor) -> list[INode]:
                 node = INode(name, "conv", [x], shp(n),
                              {"weight": m.weight.detach().float()[:, :, None, None],
                               "bias": m.bias.detach().float() if m.bias is not None else None,
-                              "stride": (1, 1), "pad": (0, 0), "k": (1, 1), "linear": True})
+                              "stride": (1, 1), "pad": (0, 0), "k": (1, 1), "linear": True,
+                              "module": m})
             elif isinstance(m, nn.BatchNorm2d):
                 inv = torch.rsqrt(m.running_var.detach().double() + m.eps)
                 scale = m.weight.detach().double() * inv if m.affine else inv
                 shift = (m.bias.detach().double() if m.affine else 0) - \
                     m.running_mean.detach().double() * scale
-                node = INode(name, "bn", [x], shp(n), {"scale": scale, "shift": shift})
+                node = INode(name, "bn", [x], shp(n), {"scale": scale, "shift": shift, "module": m})
             elif isinstance(m, (nn.ReLU, nn.ReLU6, nn.SiLU, nn.Sigmoid)):
                 code = {nn.ReLU: ACT_RELU, nn.ReLU6: ACT_RELU6, nn.SiLU: ACT_SILU,
                         nn.Sigmoid: ACT_SIGMOID}[type(m)]
