@@ -320,6 +320,9 @@ def run_ours(args, world, rank, local):
     extra = None
     if rank == 0 and world == 1 and not args.skip_extra:
         extra = other_configs(args, dev, hbm, bf16, flush, stream)
+    training = None
+    if not args.skip_train and (world == 1 or args.train_dp):
+        training = train_configs(args, dev, world, rank)
 
     line = None
     if rank == 0:
@@ -385,6 +388,8 @@ def run_ours(args, world, rank, local):
             line["cpu_baseline"] = cpu
         if extra is not None:
             line["other_configs"] = extra
+        if training is not None:
+            line["training"] = training
         print(json.dumps(line))
     eng.close()
     return line
@@ -451,6 +456,90 @@ def other_configs(args, dev, hbm, bf16, flush, stream):
     return out
 
 
+def train_configs(args, dev, world=1, rank=0):
+    """BASELINE config 5: MobileNetV2 / EfficientNet-B0 CIFAR-10 training,
+    bs=32 per GPU.  One step = forward + cross-entropy + backward (+ NCCL
+    allreduce when world > 1) + SGD, captured as ONE graph.
+    Reported per net: multi-stream AoT step, single-stream AoT step, the eager
+    launch loop, images/s, e2e step() from host tensors, and the torch CPU
+    autograd step on the host cores (the CPU path)."""
+    import copy
+    import torch
+    from paper_2012_02732_b200.networks import build_train_model, train_batch
+    from paper_2012_02732_b200.train import TrainEngine
+    from oracle.numerics import cpu_threads
+
+    out = {}
+    steps = max(10, min(args.steps, 50))
+    for name in ("mobilenet_v2", "efficientnet_b0"):
+        t0 = time.perf_counter()
+        model = build_train_model(name)
+        x, y = train_batch(32, rank=rank)
+        eng = TrainEngine(copy.deepcopy(model), device=dev.index or 0, world=world, rank=rank).prepare(x, y)
+        eng.load_batch_device(x, y)
+        st = eng.stream()
+
+        def timed(multi):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(steps)]
+            with torch.cuda.stream(st):
+                for a, b in ev:
+                    a.record(st)
+                    eng.replay(multi=multi)
+                    b.record(st)
+            torch.cuda.synchronize(dev)
+            return sum(a.elapsed_time(b) for a, b in ev) / steps * 1e3
+
+        for _ in range(3):
+            eng.replay(multi=True)
+            eng.replay(multi=False)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        multi_us = reduce_max(world, timed(True), dev)
+        single_us = reduce_max(world, timed(False), dev)
+        t = time.perf_counter()
+        for _ in range(3):
+            eng.run_eager()
+        eng.synchronize()
+        eager_us = (time.perf_counter() - t) / 3 * 1e6
+        for _ in range(2):
+            eng.step(x, y)
+        t = time.perf_counter()
+        for _ in range(steps):
+            eng.step(x, y)
+        e2e_us = reduce_max(world, (time.perf_counter() - t) / steps * 1e6, dev)
+        rec = {"batch_per_gpu": 32, "gpus": world,
+               "multi_stream_aot_us": round(multi_us, 2), "single_stream_aot_us": round(single_us, 2),
+               "eager_non_aot_us": round(eager_us, 2),
+               "images_per_s": round(world * 32 / (multi_us * 1e-6), 1),
+               "e2e_images_per_s": round(world * 32 / (e2e_us * 1e-6), 1),
+               "multi_over_single": round(single_us / multi_us, 4),
+               "aot_over_eager": round(eager_us / multi_us, 4),
+               "tasks": len(eng.prog.tasks), "streams": eng.assignment.num_streams,
+               "syncs": len(eng.plan), "allreduce": eng.allreduce,
+               "params": eng.builder.param_count, "prepare_s": round(time.perf_counter() - t0, 2)}
+        eng.close()
+        if rank == 0 and world == 1 and not args.skip_cpu:
+            # the CPU path: torch fp32 autograd + SGD of the same module on the host cores
+            thr = cpu_threads()
+            torch.set_num_threads(thr)
+            m = copy.deepcopy(model)
+            opt = torch.optim.SGD(m.parameters(), lr=0.05, momentum=0.9, weight_decay=4e-5)
+            ct = []
+            for i in range(5):
+                t = time.perf_counter()
+                opt.zero_grad(set_to_none=True)
+                torch.nn.functional.cross_entropy(m(x), y).backward()
+                opt.step()
+                if i >= 1:
+                    ct.append(time.perf_counter() - t)
+            cpu_s = sum(ct) / len(ct)
+            rec["cpu_baseline"] = {"value": round(32 / cpu_s, 2), "unit": "images/s", "cores": thr,
+                                   "kind": "port", "sample": "4 torch CPU fp32 training steps, bs32"}
+        out[f"{name}_train_bs32"] = rec
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -463,6 +552,9 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-extra", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--big-batch", type=int, default=256, help="NASNet images/s batch (one replica)")
+    ap.add_argument("--skip-train", action="store_true", help="skip the training configs")
+    ap.add_argument("--train-dp", action="store_true",
+                    help="under torchrun: data-parallel training with the captured NCCL allreduce")
     ap.add_argument("--tuning-cache", default=None,
                     help="reuse kernel picks (e.g. for an ncu launch list of this command)")
     args = ap.parse_args()

@@ -1066,6 +1066,18 @@ class TrainEngine:
             out.append((m, v[:c].clone(), v[c:].clone()))
         return out
 
+    def profile_tasks(self, reps: int = 10) -> np.ndarray:
+        """Device µs per task, each timed as a graph-captured chain of `reps`
+        launches (sw_engine_profile_ops).  Tasks that accumulate in place or
+        update state (SGD, running stats) are re-run, so call this on a
+        throw-away engine or re-prepare afterwards."""
+        out = np.zeros(len(self.eager_order), dtype=np.float64)
+        N.check(N.lib().sw_engine_profile_ops(self._h, len(self.eager_order), N.ptr64(self.eager_order), reps,
+                                              out.ctypes.data_as(C.POINTER(C.c_double))))
+        res = np.zeros_like(out)
+        res[self.eager_order] = out
+        return res
+
     def time_replay(self, multi: bool = True, iters: int = 50, io: bool = False):
         slot = (SLOT_MULTI_IO if multi else SLOT_SINGLE_IO) if io else (SLOT_MULTI if multi else SLOT_SINGLE)
         gpu = C.c_double()
