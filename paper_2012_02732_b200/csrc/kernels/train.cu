@@ -90,73 +90,105 @@ struct BnArgs {
 };
 
 // MODE 0: batch statistics of y.  MODE 1: dgamma / dbeta from dOut.
+// Grid: x = row blocks (a.grid), y = channel blocks of TC channels.  Each
+// thread keeps kU independent row loads in flight (a serial dependent row loop
+// was latency-bound: 86 µs for 128x576); the last CTA of a channel block
+// reduces the row-block partials with all its threads, in a fixed order.
+constexpr int kU = 4;
+
 template <int MODE>
 __global__ void __launch_bounds__(kNT) bn_reduce_kernel(BnArgs a) {
   pdl_trigger();
   pdl_wait();
-  __shared__ float red[2][kNT];
+  __shared__ double red[2][kNT];
   __shared__ bool last;
   const int C = (int)a.C;
   const int TC = chan_tile(C);
   const int RL = kNT / TC;
   const int lane_c = threadIdx.x % TC, lane_r = threadIdx.x / TC;
-  const int64_t rows = (a.M + a.grid - 1) / a.grid;
+  const int gx = gridDim.x;
+  const int64_t rows = (a.M + gx - 1) / gx;
   const int64_t m0 = blockIdx.x * rows, m1 = min(a.M, m0 + rows);
-  double* part = a.ws + (int64_t)blockIdx.x * 2 * C;
-  for (int c0 = 0; c0 < C; c0 += TC) {
-    const int c = c0 + lane_c;
-    float s0 = 0.f, s1 = 0.f;
-    if (c < C) {
-      float mean = 0.f, istd = 0.f, g = 0.f, b = 0.f;
-      if (MODE == 1) {
-        mean = a.stats[c];
-        istd = a.stats[C + c];
-        g = a.gamma[c];
-        b = a.gamma[C + c];
+  const int c = blockIdx.y * TC + lane_c;
+  float s0 = 0.f, s1 = 0.f;
+  if (c < C) {
+    float mean = 0.f, istd = 0.f, g = 0.f, b = 0.f;
+    if (MODE == 1) {
+      mean = a.stats[c];
+      istd = a.stats[C + c];
+      g = a.gamma[c];
+      b = a.gamma[C + c];
+    }
+    for (int64_t mb = m0 + lane_r; mb < m1; mb += (int64_t)RL * kU) {
+      float v[kU], d[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t m = mb + (int64_t)u * RL;
+        v[u] = 0.f;
+        d[u] = 0.f;
+        if (m < m1) {
+          v[u] = a.y[m * a.ld + c];
+          if (MODE == 1) {
+            const int64_t n = m / a.HW, p = m - n * a.HW;
+            d[u] = a.dout[n * a.do_sn + p * a.do_sp + c];
+          }
+        }
       }
-      for (int64_t m = m0 + lane_r; m < m1; m += RL) {
-        const float v = a.y[m * a.ld + c];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
         if (MODE == 0) {
-          s0 += v;
-          s1 += v * v;
+          s0 += v[u];
+          s1 += v[u] * v[u];
         } else {
-          const float xh = (v - mean) * istd;
-          const int64_t n = m / a.HW, p = m - n * a.HW;
-          const float d = a.dout[n * a.do_sn + p * a.do_sp + c] * a.do_scale;
-          const float dz = a.act == ACT_NONE ? d : d * act_grad(g * xh + b, a.act);
+          const float xh = (v[u] - mean) * istd;
+          const float dd = d[u] * a.do_scale;
+          const float dz = a.act == ACT_NONE ? dd : dd * act_grad(g * xh + b, a.act);
           s0 += dz;
-          s1 += dz * xh;
+          s1 += dz * xh;  // rows past m1 contribute dz = 0
         }
       }
     }
-    red[0][threadIdx.x] = s0;
-    red[1][threadIdx.x] = s1;
-    __syncthreads();
-    if (lane_r == 0 && c < C) {
-      double t0 = 0.0, t1 = 0.0;
-      for (int r = 0; r < RL; ++r) {
-        t0 += (double)red[0][r * TC + lane_c];
-        t1 += (double)red[1][r * TC + lane_c];
-      }
-      part[c] = t0;
-      part[C + c] = t1;
-    }
-    __syncthreads();
   }
-  // last CTA to arrive reduces the partials in block order (deterministic)
+  red[0][threadIdx.x] = s0;
+  red[1][threadIdx.x] = s1;
+  __syncthreads();
+  if (lane_r == 0 && c < C) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int r = 0; r < RL; ++r) {
+      t0 += red[0][r * TC + lane_c];
+      t1 += red[1][r * TC + lane_c];
+    }
+    double* part = a.ws + (int64_t)blockIdx.x * 2 * C;
+    part[c] = t0;
+    part[C + c] = t1;
+  }
   __threadfence();
   __syncthreads();
-  unsigned* ticket = reinterpret_cast<unsigned*>(a.ws + (int64_t)a.grid * 2 * C);
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (unsigned)(a.grid - 1);
+  unsigned* ticket = reinterpret_cast<unsigned*>(a.ws + (int64_t)gx * 2 * C) + blockIdx.y;
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (unsigned)(gx - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int c = threadIdx.x; c < C; c += kNT) {
-    double t0 = 0.0, t1 = 0.0;
-    for (int g = 0; g < a.grid; ++g) {
-      const volatile double* pg = a.ws + (int64_t)g * 2 * C;
-      t0 += pg[c];
-      t1 += pg[C + c];
+  // all threads: lane_r strides over the row-block partials of channel c
+  double t0 = 0.0, t1 = 0.0;
+  if (c < C) {
+    const volatile double* pw = a.ws;
+#pragma unroll 4
+    for (int g = lane_r; g < gx; g += RL) {
+      t0 += pw[(int64_t)g * 2 * C + c];
+      t1 += pw[(int64_t)g * 2 * C + C + c];
+    }
+  }
+  __syncthreads();
+  red[0][threadIdx.x] = t0;
+  red[1][threadIdx.x] = t1;
+  __syncthreads();
+  if (lane_r == 0 && c < C) {
+    t0 = 0.0;
+    t1 = 0.0;
+    for (int r = 0; r < RL; ++r) {
+      t0 += red[0][r * TC + lane_c];
+      t1 += red[1][r * TC + lane_c];
     }
     if (MODE == 0) {
       const double mean = t0 / (double)a.M;
@@ -342,6 +374,9 @@ __global__ void __launch_bounds__(kNT) dw_dgrad_kernel(DwArgs a) {
 }
 
 // dW[r,s,c] = sum_{n,p,q} dY[n,p,q,c] X[n, p*sh-ph+r, q*sw-pw+s, c]
+// Grid: x = output-pixel blocks (a.grid), y = channel blocks of TC.  Each thread
+// holds KS*KS accumulators for its channel; the last CTA of a channel block
+// reduces the partials [gx][KS*KS][C] in a fixed order with all threads.
 template <int KS>
 __global__ void __launch_bounds__(kNT) dw_wgrad_kernel(DwArgs a) {
   pdl_trigger();
@@ -352,64 +387,69 @@ __global__ void __launch_bounds__(kNT) dw_wgrad_kernel(DwArgs a) {
   const int TC = chan_tile(C);
   const int RL = kNT / TC;
   const int lane_c = threadIdx.x % TC, lane_r = threadIdx.x / TC;
+  const int gx = gridDim.x;
   const int64_t M = (int64_t)a.N * a.P * a.Q;
-  const int64_t rows = (M + a.grid - 1) / a.grid;
+  const int64_t rows = (M + gx - 1) / gx;
   const int64_t m0 = blockIdx.x * rows, m1 = min(M, m0 + rows);
+  const int c = blockIdx.y * TC + lane_c;
   float* part = a.ws + (int64_t)blockIdx.x * KS * KS * C;
-  for (int c0 = 0; c0 < C; c0 += TC) {
-    const int c = c0 + lane_c;
-    float acc[KS * KS];
+  float acc[KS * KS];
 #pragma unroll
-    for (int k = 0; k < KS * KS; ++k) acc[k] = 0.f;
-    if (c < C) {
-      for (int64_t m = m0 + lane_r; m < m1; m += RL) {
-        const int q = (int)(m % a.Q);
-        const int64_t t = m / a.Q;
-        const int p = (int)(t % a.P);
-        const int n = (int)(t / a.P);
-        const float g = a.dy[m * C + c];
-        const int h0 = p * a.sh - a.ph, w0 = q * a.sw - a.pw;
+  for (int k = 0; k < KS * KS; ++k) acc[k] = 0.f;
+  if (c < C) {
+    for (int64_t m = m0 + lane_r; m < m1; m += RL) {
+      const int q = (int)(m % a.Q);
+      const int64_t t = m / a.Q;
+      const int p = (int)(t % a.P);
+      const int n = (int)(t / a.P);
+      const float g = a.dy[m * C + c];
+      const int h0 = p * a.sh - a.ph, w0 = q * a.sw - a.pw;
+      const float* xb = a.x + (int64_t)n * a.H * a.W * C + c;
 #pragma unroll
-        for (int r = 0; r < KS; ++r) {
-          const int h = h0 + r;
-          if (h < 0 || h >= a.H) continue;
+      for (int r = 0; r < KS; ++r) {
+        const int h = h0 + r;
+        const bool hv = h >= 0 && h < a.H;
 #pragma unroll
-          for (int s = 0; s < KS; ++s) {
-            const int w = w0 + s;
-            if (w < 0 || w >= a.W) continue;
-            acc[r * KS + s] += g * a.x[(((int64_t)n * a.H + h) * a.W + w) * C + c];
-          }
+        for (int s = 0; s < KS; ++s) {
+          const int w = w0 + s;
+          const bool ok = hv && w >= 0 && w < a.W;
+          const float xv = ok ? xb[((int64_t)h * a.W + w) * C] : 0.f;
+          acc[r * KS + s] += g * xv;
         }
       }
     }
-    if (RL > 1) {
+  }
+  if (RL > 1) {
 #pragma unroll
-      for (int k = 0; k < KS * KS; ++k) red[(lane_r * KS * KS + k) * TC + lane_c] = acc[k];
-      __syncthreads();
-      if (lane_r == 0 && c < C) {
-        for (int k = 0; k < KS * KS; ++k) {
-          float t = 0.f;
-          for (int r = 0; r < RL; ++r) t += red[(r * KS * KS + k) * TC + lane_c];
-          part[k * C + c] = t;
-        }
+    for (int k = 0; k < KS * KS; ++k) red[(lane_r * KS * KS + k) * TC + lane_c] = acc[k];
+    __syncthreads();
+    if (lane_r == 0 && c < C) {
+      for (int k = 0; k < KS * KS; ++k) {
+        float t = 0.f;
+        for (int r = 0; r < RL; ++r) t += red[(r * KS * KS + k) * TC + lane_c];
+        part[k * C + c] = t;
       }
-      __syncthreads();
-    } else if (c < C) {
-#pragma unroll
-      for (int k = 0; k < KS * KS; ++k) part[k * C + c] = acc[k];
     }
+  } else if (c < C) {
+#pragma unroll
+    for (int k = 0; k < KS * KS; ++k) part[k * C + c] = acc[k];
   }
   __threadfence();
   __syncthreads();
-  unsigned* ticket = reinterpret_cast<unsigned*>(a.ws + (int64_t)a.grid * KS * KS * C);
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (unsigned)(a.grid - 1);
+  unsigned* ticket = reinterpret_cast<unsigned*>(a.ws + (int64_t)gx * KS * KS * C) + blockIdx.y;
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (unsigned)(gx - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int i = threadIdx.x; i < KS * KS * C; i += kNT) {
+  const int c0 = blockIdx.y * TC;
+  const int cw = min(TC, C - c0);
+  const volatile float* pw = a.ws;
+  for (int i = threadIdx.x; i < KS * KS * cw; i += kNT) {
+    const int k = i / cw, cc = c0 + i % cw;
     double t = 0.0;
-    for (int g = 0; g < a.grid; ++g) t += (double)((const volatile float*)a.ws)[(int64_t)g * KS * KS * C + i];
-    a.out[i] = (float)t;
+#pragma unroll 4
+    for (int g = 0; g < gx; ++g) t += (double)pw[(int64_t)g * KS * KS * C + k * C + cc];
+    a.out[k * C + cc] = (float)t;
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }
@@ -461,20 +501,34 @@ __global__ void __launch_bounds__(kNT) gemm_kernel(GemmArgs g) {
   const bool b_fast_j = g.im2col || g.b_j <= g.b_r;
   const int tx = tid % 16, ty = tid / 16;  // 16 x 16 threads, 4x4 outputs each
   float acc[4][4] = {};
+  // register-staged prefetch: the next K tile's global loads are in flight
+  // while the current tile is multiplied out of shared memory
+  float ra[4], rb[4];
+  int ai[4], ak[4], bj[4], bk[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int e = tid + l * kNT;  // 0..1023 over the 64x16 tile
+    if (a_fast_i) { ai[l] = e % GBM; ak[l] = e / GBM; } else { ak[l] = e % GBK; ai[l] = e / GBK; }
+    if (b_fast_j) { bj[l] = e % GBN; bk[l] = e / GBN; } else { bk[l] = e % GBK; bj[l] = e / GBK; }
+  }
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int64_t gi = i0 + ai[l], gk = k0 + ak[l];
+      ra[l] = (gi < g.M && gk < ke) ? g.A[gi * g.a_i + gk * g.a_r] : 0.f;
+      const int64_t gj = j0 + bj[l], gk2 = k0 + bk[l];
+      rb[l] = (gj < g.N && gk2 < ke) ? gemm_b(g, gk2, gj) : 0.f;
+    }
+  };
+  if (kb < ke) fetch(kb);
   for (int64_t k0 = kb; k0 < ke; k0 += GBK) {
 #pragma unroll
     for (int l = 0; l < 4; ++l) {
-      const int e = tid + l * kNT;  // 0..1023 over the 64x16 tile
-      int ii, kk;
-      if (a_fast_i) { ii = e % GBM; kk = e / GBM; } else { kk = e % GBK; ii = e / GBK; }
-      const int64_t gi = i0 + ii, gk = k0 + kk;
-      As[kk][ii] = (gi < g.M && gk < ke) ? g.A[gi * g.a_i + gk * g.a_r] : 0.f;
-      int jj, kk2;
-      if (b_fast_j) { jj = e % GBN; kk2 = e / GBN; } else { kk2 = e % GBK; jj = e / GBK; }
-      const int64_t gj = j0 + jj, gk2 = k0 + kk2;
-      Bs[kk2][jj] = (gj < g.N && gk2 < ke) ? gemm_b(g, gk2, gj) : 0.f;
+      As[ak[l]][ai[l]] = ra[l];
+      Bs[bk[l]][bj[l]] = rb[l];
     }
     __syncthreads();
+    if (k0 + GBK < ke) fetch(k0 + GBK);
 #pragma unroll
     for (int kk = 0; kk < GBK; ++kk) {
       float av[4], bv[4];
@@ -656,7 +710,7 @@ int launch_train(const sw_op_desc& d, void* stream) {
         a.stats = reinterpret_cast<float*>(q[1]);
         a.running = reinterpret_cast<float*>(q[2]);
         a.ws = reinterpret_cast<double*>(q[7]);
-        launch_k(bn_reduce_kernel<0>, dim3(a.grid), dim3(kNT), 0, st, 1, a);
+        launch_k(bn_reduce_kernel<0>, dim3(a.grid, (unsigned)cdiv(a.C, chan_tile((int)a.C))), dim3(kNT), 0, st, 1, a);
       } else {
         a.dout = reinterpret_cast<const float*>(q[0]);
         a.y = reinterpret_cast<const float*>(q[1]);
@@ -664,7 +718,7 @@ int launch_train(const sw_op_desc& d, void* stream) {
         a.gamma = reinterpret_cast<const float*>(q[3]);
         a.dgamma = reinterpret_cast<float*>(q[4]);
         a.ws = reinterpret_cast<double*>(q[7]);
-        launch_k(bn_reduce_kernel<1>, dim3(a.grid), dim3(kNT), 0, st, 1, a);
+        launch_k(bn_reduce_kernel<1>, dim3(a.grid, (unsigned)cdiv(a.C, chan_tile((int)a.C))), dim3(kNT), 0, st, 1, a);
       }
       break;
     }
@@ -715,9 +769,9 @@ int launch_train(const sw_op_desc& d, void* stream) {
       const int TC = chan_tile(a.C), RL = kNT / TC;
       const size_t smem = RL > 1 ? (size_t)RL * a.R * a.S * TC * sizeof(float) : 0;
       if (a.R == 3)
-        launch_k(dw_wgrad_kernel<3>, dim3(a.grid), dim3(kNT), smem, st, 1, a);
+        launch_k(dw_wgrad_kernel<3>, dim3(a.grid, (unsigned)cdiv(a.C, TC)), dim3(kNT), smem, st, 1, a);
       else if (a.R == 5)
-        launch_k(dw_wgrad_kernel<5>, dim3(a.grid), dim3(kNT), smem, st, 1, a);
+        launch_k(dw_wgrad_kernel<5>, dim3(a.grid, (unsigned)cdiv(a.C, TC)), dim3(kNT), smem, st, 1, a);
       else
         return (int)cudaErrorInvalidValue;
       break;

@@ -313,8 +313,27 @@ def gemm_ws_bytes(M, Nn, split):
     return 4 * split * tiles * GEMM_TILE * GEMM_TILE + 4 * tiles
 
 
-def reduce_grid(m, rows=64):
-    return max(1, min(2 * NUM_SMS, m // rows))
+def chan_tile(c: int) -> int:
+    """csrc/kernels/train.cu chan_tile: channels per CTA of the per-channel reductions."""
+    tc = 32
+    while tc < c and tc < 256:
+        tc *= 2
+    return tc
+
+
+def reduce_grid(m: int, c: int, rows_per_thread: int) -> int:
+    """Row blocks (grid.x) of a per-channel reduction over m rows: about
+    `rows_per_thread` rows per thread, at most ~2 CTAs per SM overall."""
+    tc = chan_tile(c)
+    rl = 256 // tc
+    gy = math.ceil(c / tc)
+    gx = math.ceil(m / (rl * rows_per_thread))
+    return max(1, min(gx, max(1, 2 * NUM_SMS // gy)))
+
+
+def reduce_ws_bytes(grid: int, c: int, elem_bytes: int, per_chan: int) -> int:
+    """Partials [grid][per_chan][c] + one ticket per channel block."""
+    return elem_bytes * grid * per_chan * c + 4 * math.ceil(c / chan_tile(c)) + 16
 
 
 # ----------------------------------------------------------------------------
@@ -502,11 +521,11 @@ class _Builder:
             y = self.val[id(bn.inputs[0])]
             n, c, h, w = y.shape
             M = n * h * w
-            grid = reduce_grid(M)
+            grid = reduce_grid(M, c, 16)
             stats = P.buf(f"{bn.name}.stats", 8 * c)
             running = P.buf(f"{bn.name}.running", 8 * c)
             P.running.append((m, running))
-            ws = P.buf(f"{bn.name}.ws", 16 * grid * c + 16, zero=True)
+            ws = P.buf(f"{bn.name}.ws", reduce_ws_bytes(grid, c, 8, 2), zero=True)
             out = P.tensor(bn.name + ".out", y.shape)
             gb = self.pbuf[op["pid"]]
             eps, mom = m.eps, (m.momentum if m.momentum is not None else 0.1)
@@ -643,8 +662,8 @@ class _Builder:
             act = op["act"]
             gb = self.pbuf[op["pid"]]
             gg = self.gbuf[op["pid"]]
-            grid = reduce_grid(M)
-            ws = P.buf(f"{bn.name}.bws", 16 * grid * c + 16, zero=True)
+            grid = reduce_grid(M, c, 16)
+            ws = P.buf(f"{bn.name}.bws", reduce_ws_bytes(grid, c, 8, 2), zero=True)
             if op["res"] is not None:
                 self._contribute_alias(op["res"], op["res"].shape, gout)
             bnp = {BN_M: M, BN_C: c, BN_HW: hw, BN_ACT: act, BN_GRID: grid, BN_DO_SN: gout.sn,
@@ -793,8 +812,8 @@ class _Builder:
         wb, gw = self.pbuf[op["pid"]], self.gbuf[op["pid"]]
         M = nb * p * q
         if n.kind == "dwconv":
-            grid = reduce_grid(M, 32)
-            ws = P.buf(n.name + ".wws", 4 * grid * R * S * c + 16, zero=True)
+            grid = reduce_grid(M, c, 4)
+            ws = P.buf(n.name + ".wws", reduce_ws_bytes(grid, c, 4, R * S), zero=True)
 
             def fill_w(d, ptr):
                 _dw_params(d, xb.shape, n.shape, (R, S), st, pad)
@@ -840,9 +859,13 @@ class _Builder:
             if (R, S) != (1, 1) or tuple(st) != (1, 1) or tuple(pad) != (0, 0):
                 raise NotImplementedError("training: input gradient of a k x k / strided dense conv")
 
+            dsplit = gemm_split(M, c, kk)
+            dws = P.buf(n.name + ".dws", gemm_ws_bytes(M, c, dsplit), zero=True) if dsplit > 1 else None
+
             def emit(out, res):
-                P.task("dgrad", n.name, [gd, wb] + ([res] if res is not None else []), [out],
-                       _gemm_fill(M, c, kk, gd, kk, 1, wb, c, 1, out, c, 1, None, res=res), "bwd",
+                P.task("dgrad", n.name, [gd, wb] + ([res] if res is not None else []),
+                       [out] + ([dws] if dws is not None else []),
+                       _gemm_fill(M, c, kk, gd, kk, 1, wb, c, 1, out, c, dsplit, dws, res=res), "bwd",
                        flops=2.0 * M * c * kk)
             self._contribute(x, xb.shape, emit)
 
