@@ -301,7 +301,7 @@ def _gemm_fill(M, Nn, K, A: Buf, a_i, a_r, B: Buf, b_r, b_j, Cb: Buf, c_i, split
 def gemm_split(M, Nn, K):
     tiles = math.ceil(M / GEMM_TILE) * math.ceil(Nn / GEMM_TILE)
     split = 1
-    while tiles * split * 2 <= 2 * NUM_SMS and K // (split * 2) >= 128:
+    while split < 16 and tiles * split * 2 <= 2 * NUM_SMS and K // (split * 2) >= 128:
         split *= 2
     return split
 
@@ -315,20 +315,18 @@ def gemm_ws_bytes(M, Nn, split):
 
 def chan_tile(c: int) -> int:
     """csrc/kernels/train.cu chan_tile: channels per CTA of the per-channel reductions."""
-    tc = 32
-    while tc < c and tc < 256:
-        tc *= 2
-    return tc
+    return 32
 
 
-def reduce_grid(m: int, c: int, rows_per_thread: int) -> int:
+def reduce_grid(m: int, c: int, rows_per_thread: int, cap: int) -> int:
     """Row blocks (grid.x) of a per-channel reduction over m rows: about
-    `rows_per_thread` rows per thread, at most ~2 CTAs per SM overall."""
+    `rows_per_thread` rows per thread, ~2 CTAs per SM overall, and at most
+    `cap` partials for the last CTA to fold."""
     tc = chan_tile(c)
     rl = 256 // tc
     gy = math.ceil(c / tc)
     gx = math.ceil(m / (rl * rows_per_thread))
-    return max(1, min(gx, max(1, 2 * NUM_SMS // gy)))
+    return max(1, min(gx, cap, max(1, 2 * NUM_SMS // gy)))
 
 
 def reduce_ws_bytes(grid: int, c: int, elem_bytes: int, per_chan: int) -> int:
@@ -521,7 +519,7 @@ class _Builder:
             y = self.val[id(bn.inputs[0])]
             n, c, h, w = y.shape
             M = n * h * w
-            grid = reduce_grid(M, c, 16)
+            grid = reduce_grid(M, c, 8, 64)
             stats = P.buf(f"{bn.name}.stats", 8 * c)
             running = P.buf(f"{bn.name}.running", 8 * c)
             P.running.append((m, running))
@@ -662,7 +660,7 @@ class _Builder:
             act = op["act"]
             gb = self.pbuf[op["pid"]]
             gg = self.gbuf[op["pid"]]
-            grid = reduce_grid(M, c, 16)
+            grid = reduce_grid(M, c, 8, 64)
             ws = P.buf(f"{bn.name}.bws", reduce_ws_bytes(grid, c, 8, 2), zero=True)
             if op["res"] is not None:
                 self._contribute_alias(op["res"], op["res"].shape, gout)
@@ -812,7 +810,7 @@ class _Builder:
         wb, gw = self.pbuf[op["pid"]], self.gbuf[op["pid"]]
         M = nb * p * q
         if n.kind == "dwconv":
-            grid = reduce_grid(M, c, 4)
+            grid = reduce_grid(M, c, 4, 32 if R * S <= 9 else 16)
             ws = P.buf(n.name + ".wws", reduce_ws_bytes(grid, c, 4, R * S), zero=True)
 
             def fill_w(d, ptr):
