@@ -693,6 +693,21 @@ __global__ void __launch_bounds__(kNT) ew_bwd_kernel(EwbArgs a) {
   }
 }
 
+// 32x32 smem-tiled transpose (rows x cols → cols x rows)
+__global__ void __launch_bounds__(kNT) transpose_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                        int rows, int cols) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float t[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+  for (int i = ty; i < 32; i += 8)
+    if (r0 + i < rows && c0 + tx < cols) t[i][tx] = in[(int64_t)(r0 + i) * cols + c0 + tx];
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8)
+    if (c0 + i < cols && r0 + tx < rows) out[(int64_t)(c0 + i) * rows + r0 + tx] = t[tx][i];
+}
+
 }  // namespace
 
 int launch_train(const sw_op_desc& d, void* stream) {
@@ -842,6 +857,12 @@ int launch_train(const sw_op_desc& d, void* stream) {
       a.zs = reinterpret_cast<const float*>(q[5]);
       const int64_t work = a.mode == 2 ? a.N * a.C * 32 : a.N * a.HW * a.C;
       launch_k(ew_bwd_kernel, dim3((unsigned)cdiv(work, kNT)), dim3(kNT), 0, st, 1, a);
+      break;
+    }
+    case K_TRANSPOSE: {
+      const int rows = (int)p[0], cols = (int)p[1];
+      launch_k(transpose_kernel, dim3((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32)), dim3(kNT), 0, st, 1,
+               reinterpret_cast<const float*>(q[0]), reinterpret_cast<float*>(q[1]), rows, cols);
       break;
     }
     default: return (int)cudaErrorInvalidValue;

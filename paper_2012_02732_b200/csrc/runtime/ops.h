@@ -34,6 +34,7 @@ enum KernelKind : int32_t {
   K_SGD = 17,           // SGD with momentum + weight decay over the flat parameters
   K_ALLREDUCE = 18,     // NCCL average of the flat gradient buffer (engine-owned comm)
   K_EW_BWD = 19,        // activation / broadcast-mul backward (EfficientNet SE)
+  K_TRANSPOSE = 20,     // out[c][r] = in[r][c] (1x1 weights for the dgrad conv)
 };
 
 // Batch-norm kinds (K_BN_*): params index
@@ -82,6 +83,7 @@ enum GemmParam : int {
 // K_SGD params: 0 n, 1 lr, 2 momentum, 3 weight decay (float bits); ptrs 0 params,
 // 1 grads, 2 momentum buffer
 // K_ALLREDUCE params: 0 count (floats); ptrs 0 buffer (in place)
+// K_TRANSPOSE params: 0 rows, 1 cols; ptrs 0 in [rows][cols], 1 out [cols][rows]
 // K_EW_BWD params: 0 N, 1 HW, 2 C, 3 mode (0 act-backward: dx = dy*act'(z) [+res];
 // 1 mul-backward: dx = dy*s[n,c] [+res]; 2 mul-backward to the scale: ds[n,c] =
 // sum_hw dy*x, then act'(z_s) applied; 3 broadcast: dx = s[n,c]*scale [+res]

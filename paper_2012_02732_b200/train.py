@@ -51,7 +51,8 @@ from .engine import (EP_A, EP_B, EP_OUT, EW_A_SN, EW_ACT, EW_B_SN, EW_C, EW_H, E
                      NUM_SMS, PT_BIAS, PT_IN, PT_OUT, PT_W, SLOT_MULTI, SLOT_MULTI_IO, SLOT_SINGLE,
                      SLOT_SINGLE_IO, SP_ACT, SP_C, SP_H, SP_HAS_RES, SP_IN_SN, SP_K, SP_KPAD, SP_N,
                      SP_OUT_SC, SP_OUT_SN, SP_P, SP_PAD_H, SP_PAD_W, SP_Q, SP_R, SP_S, SP_SPLIT_K,
-                     SP_STRIDE_H, SP_STRIDE_W, SP_W, pick_conv_variant)
+                     SP_STRIDE_H, SP_STRIDE_W, SP_W, SP_RES_SN, SP_RES_SH, SP_RES_SW, SP_RES_SC, PT_RES,
+                     K_CONV_TC, conv_candidates, pick_conv_variant)
 from .errors import CudaError
 from .graph import CompGraph, TaskNode
 from .schedule import pre_run, schedule_arrays
@@ -59,7 +60,7 @@ from .trace import ACT_NONE, ACT_SIGMOID, trace_model, _drop_identities
 
 # csrc/runtime/ops.h training kinds
 (K_BN_STATS, K_BN_APPLY, K_BN_BWD_REDUCE, K_BN_BWD_APPLY, K_DW_DGRAD, K_DW_WGRAD, K_GEMM, K_XENT,
- K_SGD, K_ALLREDUCE, K_EW_BWD) = range(9, 20)
+ K_SGD, K_ALLREDUCE, K_EW_BWD, K_TRANSPOSE) = range(9, 21)
 (BN_M, BN_C, BN_HW, BN_ACT, BN_HAS_RES, BN_EPS, BN_MOMENTUM, BN_GRID, BN_DO_SN, BN_DO_SP,
  BN_DO_SCALE, BN_LD) = range(12)
 (GM_M, GM_N, GM_K, GM_A_I, GM_A_R, GM_B_R, GM_B_J, GM_C_I, GM_SPLIT, GM_HAS_RES, GM_IM2COL,
@@ -219,7 +220,8 @@ class TrainProgram:
 # op descriptors
 # ----------------------------------------------------------------------------
 
-def _spatial_fill(kind, x: Buf, out: Buf, w: Buf | None, bias: Buf | None, k, stride, pad, act=ACT_NONE):
+def _spatial_fill(kind, x: Buf, out: Buf, w: Buf | None, bias: Buf | None, k, stride, pad, act=ACT_NONE,
+                  res: Buf | None = None):
     n, c, h, wd = x.shape
     _, kk, p, q = out.shape
     R, S = k
@@ -244,6 +246,11 @@ def _spatial_fill(kind, x: Buf, out: Buf, w: Buf | None, bias: Buf | None, k, st
         d.ptrs[PT_OUT] = ptr(out)
         d.ptrs[PT_W] = ptr(w) if w is not None else 0
         d.ptrs[PT_BIAS] = ptr(bias) if bias is not None else 0
+        if res is not None:
+            rsn, rsh, rsw, rsc = res.strides()
+            for key, v in {SP_RES_SN: rsn, SP_RES_SH: rsh, SP_RES_SW: rsw, SP_RES_SC: rsc, SP_HAS_RES: 1}.items():
+                d.params[key] = int(v)
+            d.ptrs[PT_RES] = ptr(res)
     return fill
 
 
@@ -857,13 +864,23 @@ class _Builder:
             if (R, S) != (1, 1) or tuple(st) != (1, 1) or tuple(pad) != (0, 0):
                 raise NotImplementedError("training: input gradient of a k x k / strided dense conv")
 
-            dsplit = gemm_split(M, c, kk)
-            dws = P.buf(n.name + ".dws", gemm_ws_bytes(M, c, dsplit), zero=True) if dsplit > 1 else None
+            # dgrad of a 1x1 conv is a 1x1 conv of dY with the transposed weight
+            # [C][K]: the autotuned inference conv kernels (conv.cu / conv1x1.cu)
+            # run it, accumulating through their residual epilogue.  The
+            # transpose reads the weights at step start, off the critical path.
+            wt = P.tensor(n.name + ".wT", (c, kk, 1, 1))
+
+            def fill_t(d, ptr):
+                d.kind = K_TRANSPOSE
+                d.params[0], d.params[1] = kk, c
+                d.ptrs[0], d.ptrs[1] = ptr(wb), ptr(wt)
+            P.task("transpose", n.name, [wb], [wt], fill_t, "bwd")
 
             def emit(out, res):
-                P.task("dgrad", n.name, [gd, wb] + ([res] if res is not None else []),
-                       [out] + ([dws] if dws is not None else []),
-                       _gemm_fill(M, c, kk, gd, kk, 1, wb, c, 1, out, c, dsplit, dws, res=res), "bwd",
+                gview = self._view(gd, (nb, kk, p, q))
+                P.task("dgrad", n.name, [gd, wt] + ([res] if res is not None else []), [out],
+                       _spatial_fill(K_CONV, gview, self._view(out, xb.shape), wt, None, (1, 1), (1, 1), (0, 0),
+                                     res=self._view(res, xb.shape) if res is not None else None), "bwd",
                        flops=2.0 * M * c * kk)
             self._contribute(x, xb.shape, emit)
 
@@ -942,7 +959,8 @@ class TrainEngine:
 
     def __init__(self, model: nn.Module, lr: float = 0.05, momentum: float = 0.9,
                  weight_decay: float = 4e-5, multi_stream: bool = True, device: int = 0,
-                 world: int = 1, rank: int = 0, allreduce: bool | None = None, pdl: bool = False):
+                 world: int = 1, rank: int = 0, allreduce: bool | None = None, pdl: bool = False,
+                 autotune: bool = True):
         self.model = model
         self.lr, self.momentum, self.wd = lr, momentum, weight_decay
         self.multi_stream = multi_stream
@@ -950,8 +968,42 @@ class TrainEngine:
         self.world, self.rank = world, rank
         self.allreduce = (world > 1) if allreduce is None else allreduce
         self.pdl = pdl
+        self.autotune = autotune
+        self.tuning = {}
         self._h = None
         self.prepared = False
+
+    def _autotune(self, reps: int = 5):
+        """Kernel selection for the K_CONV tasks (forward convs and 1x1 dgrads),
+        as in Engine._autotune: every SIMT / TMA-pointwise tile x split-K
+        candidate timed as a graph-captured chain; tcgen05 candidates are
+        excluded (they need weights pre-split at prepare, and these change every
+        step).  Only activation / gradient buffers are written while timing."""
+        lib = N.lib()
+        us = C.c_double()
+        for t in self.prog.tasks:
+            d = self.ops[t.tid]
+            if d.kind != K_CONV:
+                continue
+            p = d.params
+            M = p[SP_N] * p[SP_P] * p[SP_Q]
+            cands = [c for c in conv_candidates(M, p[SP_K], p[SP_R] * p[SP_S] * p[SP_C], p[SP_R], p[SP_S],
+                                                (p[SP_PAD_H], p[SP_PAD_W])) if c[0] != K_CONV_TC]
+            trial = N.OpDesc()
+            C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
+            best = None
+            for kind, variant, split in cands:
+                trial.kind, trial.variant = kind, variant
+                trial.params[SP_SPLIT_K] = split
+                if lib.sw_engine_time_op(self._h, C.byref(trial), reps, C.byref(us)) != 0:
+                    continue
+                if best is None or us.value < best[0]:
+                    best = (us.value, kind, variant, split)
+            if best is not None:
+                d.kind, d.variant = best[1], best[2]
+                d.params[SP_SPLIT_K] = best[3]
+                self.tuning[t.tid] = best
+        N.check(lib.sw_engine_synchronize(self._h))
 
     def prepare(self, x: torch.Tensor, y: torch.Tensor) -> "TrainEngine":
         lib = N.lib()
@@ -993,6 +1045,10 @@ class TrainEngine:
         N.check(lib.sw_engine_set_flags(h, 1 if self.pdl else 0))
         if self.allreduce:
             self._init_nccl()
+        t_tune = time.perf_counter()
+        if self.autotune:
+            self._autotune()
+        self.tune_seconds = time.perf_counter() - t_tune
         N.check(lib.sw_engine_set_ops(h, len(b.prog.tasks), self.ops))
         t3 = time.perf_counter()
         for slot, sched, io in ((SLOT_MULTI_IO, ts, 1), (SLOT_SINGLE_IO, ts_single, 1),

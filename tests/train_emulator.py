@@ -170,6 +170,10 @@ def run_train_op(mem: HostMemory, d, allreduce=None):
             g = _vec(mem, q[0], n)
             _put(mem, q[0], allreduce(g))
         return
+    if k == T.K_TRANSPOSE:
+        rows, cols = p[0], p[1]
+        _put(mem, q[1], _vec(mem, q[0], rows * cols).view(rows, cols).t().contiguous())
+        return
     if k == T.K_EW_BWD:
         Nb, HW, Cc, mode, act, has_res = p[0], p[1], p[2], p[3], p[4], p[5]
         if mode == T.EWB_MUL_S:
