@@ -463,7 +463,7 @@ struct GemmArgs {
   const float* res;
   float* ws;
   int64_t M, N, K, a_i, a_r, b_r, b_j, c_i;
-  int split, has_res, im2col;
+  int split, has_res, im2col, partials_only;
   int xN, xH, xW, xC, xP, xQ, xR, xS, xst, xpad;
   int64_t xsn, xsh, xsw, xsc;
 };
@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(kNT) gemm_kernel(GemmArgs g) {
     for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int v = 0; v < 4; ++v) part[(ty + 16 * u) * GBN + tx + 16 * v] = acc[u][v];
+    if (g.partials_only) return;  // folded by the K_GEMM_REDUCE task that follows
     __threadfence();
     __syncthreads();
     unsigned* ticket = reinterpret_cast<unsigned*>(g.ws + (int64_t)tiles * g.split * GBM * GBN) + tile;
@@ -581,6 +582,38 @@ __global__ void __launch_bounds__(kNT) gemm_kernel(GemmArgs g) {
       if (g.has_res) o += g.res[gi * g.c_i + gj];
       g.Cp[gi * g.c_i + gj] = o;
     }
+  }
+}
+
+// Folds wide split-K partials: a CTA owns 32 consecutive outputs (lane) and
+// 8 partial lanes (warp) that stride over the splits; fixed-order smem tree.
+__global__ void __launch_bounds__(kNT) gemm_reduce_kernel(GemmArgs g) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t tiles_n = (g.N + GBN - 1) / GBN;
+  float t = 0.f;
+  const bool ok = e < g.M * g.N;
+  int64_t i = 0, j = 0;
+  if (ok) {
+    i = e / g.N;
+    j = e - i * g.N;
+    const int64_t tile = (i / GBM) * tiles_n + j / GBN;
+    const float* base = g.ws + tile * g.split * GBM * GBN + (i % GBM) * GBN + j % GBN;
+#pragma unroll 4
+    for (int z = w; z < g.split; z += 8) t += base[(int64_t)z * GBM * GBN];
+  }
+  red[w][lane] = t;
+  __syncthreads();
+  if (w == 0 && ok) {
+    float o = 0.f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) o += red[r][lane];
+    if (g.bias) o += g.bias[j];
+    if (g.has_res) o += g.res[i * g.c_i + j];
+    g.Cp[i * g.c_i + j] = o;
   }
 }
 
@@ -789,7 +822,8 @@ int launch_train(const sw_op_desc& d, void* stream) {
         return (int)cudaErrorInvalidValue;
       break;
     }
-    case K_GEMM: {
+    case K_GEMM:
+    case K_GEMM_REDUCE: {
       GemmArgs g{};
       g.A = reinterpret_cast<const float*>(q[0]);
       g.B = reinterpret_cast<const float*>(q[1]);
@@ -822,7 +856,12 @@ int launch_train(const sw_op_desc& d, void* stream) {
       g.xsh = p[GM_X_SH];
       g.xsw = p[GM_X_SW];
       g.xsc = p[GM_X_SC];
+      g.partials_only = (int)p[GM_PARTIALS_ONLY];
       if (g.split > 1 && !g.ws) return (int)cudaErrorInvalidValue;
+      if (d.kind == K_GEMM_REDUCE) {
+        launch_k(gemm_reduce_kernel, dim3((unsigned)cdiv(g.M * g.N, 32)), dim3(kNT), 0, st, 1, g);
+        break;
+      }
       dim3 grid((unsigned)cdiv(g.N, GBN), (unsigned)cdiv(g.M, GBM), (unsigned)g.split);
       launch_k(gemm_kernel, grid, dim3(kNT), 0, st, 1, g);
       break;

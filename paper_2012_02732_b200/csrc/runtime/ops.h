@@ -35,6 +35,7 @@ enum KernelKind : int32_t {
   K_ALLREDUCE = 18,     // NCCL average of the flat gradient buffer (engine-owned comm)
   K_EW_BWD = 19,        // activation / broadcast-mul backward (EfficientNet SE)
   K_TRANSPOSE = 20,     // out[c][r] = in[r][c] (1x1 weights for the dgrad conv)
+  K_GEMM_REDUCE = 21,   // fold K_GEMM split partials (+ bias, + res): wide splits
 };
 
 // Batch-norm kinds (K_BN_*): params index
@@ -75,8 +76,11 @@ enum GemmParam : int {
   GM_X_N, GM_X_H, GM_X_W, GM_X_C, GM_X_P, GM_X_Q, GM_X_R, GM_X_S,
   GM_X_STRIDE, GM_X_PAD,
   GM_X_SN, GM_X_SH, GM_X_SW, GM_X_SC,
+  GM_PARTIALS_ONLY,              // 1: split CTAs only store partials; a K_GEMM_REDUCE task folds them
 };
 // ptrs: 0 A, 1 B, 2 C, 3 bias, 4 res, 5 ws (split > 1: split*tiles*64*64 floats + tiles tickets)
+// K_GEMM_REDUCE: same params/ptrs as the K_GEMM whose partials it folds (ws
+// layout [tile][split][64x64]); 8 partial lanes x 32 outputs per CTA.
 
 // K_XENT params: 0 N, 1 classes, 2 logits row stride; ptrs 0 logits, 1 labels (int32),
 // 2 loss (1 float), 3 dlogits [N][classes]

@@ -60,12 +60,13 @@ from .trace import ACT_NONE, ACT_SIGMOID, trace_model, _drop_identities
 
 # csrc/runtime/ops.h training kinds
 (K_BN_STATS, K_BN_APPLY, K_BN_BWD_REDUCE, K_BN_BWD_APPLY, K_DW_DGRAD, K_DW_WGRAD, K_GEMM, K_XENT,
- K_SGD, K_ALLREDUCE, K_EW_BWD, K_TRANSPOSE) = range(9, 21)
+ K_SGD, K_ALLREDUCE, K_EW_BWD, K_TRANSPOSE, K_GEMM_REDUCE) = range(9, 22)
 (BN_M, BN_C, BN_HW, BN_ACT, BN_HAS_RES, BN_EPS, BN_MOMENTUM, BN_GRID, BN_DO_SN, BN_DO_SP,
  BN_DO_SCALE, BN_LD) = range(12)
 (GM_M, GM_N, GM_K, GM_A_I, GM_A_R, GM_B_R, GM_B_J, GM_C_I, GM_SPLIT, GM_HAS_RES, GM_IM2COL,
  GM_X_N, GM_X_H, GM_X_W, GM_X_C, GM_X_P, GM_X_Q, GM_X_R, GM_X_S, GM_X_STRIDE, GM_X_PAD,
- GM_X_SN, GM_X_SH, GM_X_SW, GM_X_SC) = range(25)
+ GM_X_SN, GM_X_SH, GM_X_SW, GM_X_SC, GM_PARTIALS_ONLY) = range(26)
+TICKET_SPLIT_MAX = 16  # wider splits fold their partials in a separate K_GEMM_REDUCE task
 EWB_ACT, EWB_MUL_X, EWB_MUL_S, EWB_BCAST = 0, 1, 2, 3
 GEMM_TILE = 64
 ALIGN = 256
@@ -282,11 +283,12 @@ def _ew_fill(op, ins: list, out: Buf, act=ACT_NONE, gpool=False):
 
 
 def _gemm_fill(M, Nn, K, A: Buf, a_i, a_r, B: Buf, b_r, b_j, Cb: Buf, c_i, split, ws: Buf | None,
-               res: Buf | None = None, bias: Buf | None = None, im2col=None):
+               res: Buf | None = None, bias: Buf | None = None, im2col=None, kind=K_GEMM):
     def fill(d, ptr):
-        d.kind = K_GEMM
+        d.kind = kind
         vals = {GM_M: M, GM_N: Nn, GM_K: K, GM_A_I: a_i, GM_A_R: a_r, GM_B_R: b_r, GM_B_J: b_j,
-                GM_C_I: c_i, GM_SPLIT: split, GM_HAS_RES: int(res is not None)}
+                GM_C_I: c_i, GM_SPLIT: split, GM_HAS_RES: int(res is not None),
+                GM_PARTIALS_ONLY: int(split > TICKET_SPLIT_MAX)}
         if im2col is not None:
             vals[GM_IM2COL] = 1
             (xn, xc, xh, xw), (p, q), (r, s), st, pad, strides = im2col
@@ -311,6 +313,13 @@ def gemm_split(M, Nn, K):
     while split < 16 and tiles * split * 2 <= 2 * NUM_SMS and K // (split * 2) >= 128:
         split *= 2
     return split
+
+
+def wide_split(M, Nn, K, rows_per_cta=64):
+    """Split of a long reduction (weight gradients: K = pixels) so ~2 CTAs per
+    SM work on it, each over >= rows_per_cta rows."""
+    tiles = math.ceil(M / GEMM_TILE) * math.ceil(Nn / GEMM_TILE)
+    return max(1, min(2 * NUM_SMS // tiles, K // rows_per_cta, 256))
 
 
 def gemm_ws_bytes(M, Nn, split):
@@ -643,6 +652,23 @@ class _Builder:
                _ew_fill(EW_ADD, [self._view(g.buf, shape), self._view(gref.buf, shape)],
                         self._view(g.buf, shape)), "bwd")
 
+    def _gemm(self, kind, name, reads, out: Buf, M, Nn, K, A, a_i, a_r, B, b_r, b_j, c_i, split,
+              res=None, bias=None, im2col=None, flops=0.0):
+        """One K_GEMM task, plus a K_GEMM_REDUCE task for splits too wide for
+        the in-kernel ticket fold."""
+        P = self.prog
+        ws = P.buf(f"{name}.{kind}.ws", gemm_ws_bytes(M, Nn, split), zero=True) if split > 1 else None
+        wide = split > TICKET_SPLIT_MAX
+        extra = [res] if res is not None else []
+        args = (M, Nn, K, A, a_i, a_r, B, b_r, b_j, out, c_i, split, ws)
+        if not wide:
+            P.task(kind, name, reads + extra, [out] + ([ws] if ws is not None else []),
+                   _gemm_fill(*args, res=res, bias=bias, im2col=im2col), "bwd", flops=flops)
+            return
+        P.task(kind, name, reads, [ws], _gemm_fill(*args, res=res, bias=bias, im2col=im2col), "bwd", flops=flops)
+        P.task(kind + "_reduce", name, [ws] + ([bias] if bias is not None else []) + extra, [out],
+               _gemm_fill(*args, res=res, bias=bias, im2col=im2col, kind=K_GEMM_REDUCE), "bwd")
+
     def _view(self, b: Buf, shape) -> Buf:
         """Same storage under another logical shape (descriptor fills only)."""
         return self.prog.sub(b, b.name + ".view", 0, b.nbytes, shape)
@@ -841,25 +867,22 @@ class _Builder:
         # dense conv / linear: wgrad dW[k, (r,s,c)] = sum_m dY[m,k] X(m; r,s,c)
         Kred = M
         Nn = R * S * c
-        split = gemm_split(kk, Nn, Kred)
-        ws = P.buf(n.name + ".wws", gemm_ws_bytes(kk, Nn, split), zero=True) if split > 1 else None
+        split = wide_split(kk, Nn, Kred)
         if (R, S) == (1, 1) and tuple(st) == (1, 1) and tuple(pad) == (0, 0) and not xb.nchw:
-            fill_w = _gemm_fill(kk, Nn, Kred, gd, 1, kk, xb, c, 1, gw, Nn, split, ws)
+            self._gemm("wgrad", n.name, [gd, xb], gw, kk, Nn, Kred, gd, 1, kk, xb, c, 1, Nn, split,
+                       flops=2.0 * kk * Nn * Kred)
         else:
             if st[0] != st[1] or pad[0] != pad[1]:
                 raise NotImplementedError("training: anisotropic conv stride/pad")
-            fill_w = _gemm_fill(kk, Nn, Kred, gd, 1, kk, xb, 0, 0, gw, Nn, split, ws,
-                                im2col=(xb.shape, (p, q), (R, S), st[0], pad[0], xb.strides()))
-        P.task("wgrad", n.name, [gd, xb], [gw] + ([ws] if ws is not None else []), fill_w, "bwd",
-               flops=2.0 * kk * Nn * Kred)
+            self._gemm("wgrad", n.name, [gd, xb], gw, kk, Nn, Kred, gd, 1, kk, xb, 0, 0, Nn, split,
+                       im2col=(xb.shape, (p, q), (R, S), st[0], pad[0], xb.strides()),
+                       flops=2.0 * kk * Nn * Kred)
         if op.get("bid") is not None:
             gbias = self.gbuf[op["bid"]]
-            bsplit = gemm_split(1, kk, M)
-            bws = P.buf(n.name + ".bws", gemm_ws_bytes(1, kk, bsplit), zero=True) if bsplit > 1 else None
             if M > self.ones.nbytes // 4:
                 raise NotImplementedError("training: bias gradient over more rows than the batch")
-            P.task("bgrad", n.name, [gd, self.ones], [gbias] + ([bws] if bws is not None else []),
-                   _gemm_fill(1, kk, M, self.ones, 0, 1, gd, kk, 1, gbias, kk, bsplit, bws), "bwd")
+            self._gemm("bgrad", n.name, [gd, self.ones], gbias, 1, kk, M, self.ones, 0, 1, gd, kk, 1, kk,
+                       wide_split(1, kk, M, 16))
         if self._needs_grad(x):
             if (R, S) != (1, 1) or tuple(st) != (1, 1) or tuple(pad) != (0, 0):
                 raise NotImplementedError("training: input gradient of a k x k / strided dense conv")

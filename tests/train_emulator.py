@@ -58,6 +58,9 @@ def _mat(mem, ptr, rows, cols, ld):
     return torch.from_numpy(mem.buf[idx].copy())
 
 
+_PARTIALS = {}
+
+
 def run_train_op(mem: HostMemory, d, allreduce=None):
     p = list(d.params)
     q = list(d.ptrs)
@@ -119,6 +122,17 @@ def run_train_op(mem: HostMemory, d, allreduce=None):
             dw = torch.nn.grad.conv2d_weight(x, (Cc, 1, R, S), dy, stride=st, padding=pad, groups=Cc)
             _put(mem, q[1], dw[:, 0].permute(1, 2, 0))
         return
+    if k == T.K_GEMM_REDUCE:
+        M, Nn = p[T.GM_M], p[T.GM_N]
+        Cm = _PARTIALS.pop(q[5])
+        if q[3]:
+            Cm = Cm + _vec(mem, q[3], Nn).double()[None, :]
+        ic = mem.idx(q[2]) + np.arange(M)[:, None] * p[T.GM_C_I] + np.arange(Nn)[None, :]
+        if p[T.GM_HAS_RES]:
+            ir = mem.idx(q[4]) + np.arange(M)[:, None] * p[T.GM_C_I] + np.arange(Nn)[None, :]
+            Cm = Cm + torch.from_numpy(mem.buf[ir].copy()).double()
+        mem.buf[ic] = Cm.float().numpy()
+        return
     if k == T.K_GEMM:
         M, Nn, K = p[T.GM_M], p[T.GM_N], p[T.GM_K]
         ia = mem.idx(q[0]) + np.arange(M)[:, None] * p[T.GM_A_I] + np.arange(K)[None, :] * p[T.GM_A_R]
@@ -136,6 +150,9 @@ def run_train_op(mem: HostMemory, d, allreduce=None):
             ib = mem.idx(q[1]) + np.arange(K)[:, None] * p[T.GM_B_R] + np.arange(Nn)[None, :] * p[T.GM_B_J]
             B = torch.from_numpy(mem.buf[ib].copy()).double()
         Cm = A @ B
+        if p[T.GM_PARTIALS_ONLY]:
+            _PARTIALS[q[5]] = Cm  # folded by the K_GEMM_REDUCE op
+            return
         if q[3]:
             Cm = Cm + _vec(mem, q[3], Nn).double()[None, :]
         ic = mem.idx(q[2]) + np.arange(M)[:, None] * p[T.GM_C_I] + np.arange(Nn)[None, :]
