@@ -882,7 +882,7 @@ class _Builder:
             if M > self.ones.nbytes // 4:
                 raise NotImplementedError("training: bias gradient over more rows than the batch")
             self._gemm("bgrad", n.name, [gd, self.ones], gbias, 1, kk, M, self.ones, 0, 1, gd, kk, 1, kk,
-                       wide_split(1, kk, M, 16))
+                       wide_split(1, kk, M, 16) if M > 256 else 1)
         if self._needs_grad(x):
             if (R, S) != (1, 1) or tuple(st) != (1, 1) or tuple(pad) != (0, 0):
                 raise NotImplementedError("training: input gradient of a k x k / strided dense conv")
