@@ -249,6 +249,9 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
 /* Diagnostic: capture an empty kernel per task (same topology, same PDL
  * protocol) — the replay then measures the graph's issue / dependency floor. */
 #define SW_ENGINE_NULL_KERNELS 2u
+/* Host staging copies of the with_io slots as kernel nodes that access the
+ * pinned host buffers through their UVA mapping (instead of memcpy nodes). */
+#define SW_ENGINE_KERNEL_IO 4u
 int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
 /* ---- training step (paper_2012_02732_b200/train.py) ---- */

@@ -270,4 +270,40 @@ int launch_null(void* stream) {
   return (int)launch_k(null_task_kernel, dim3(1), dim3(32), 0, reinterpret_cast<cudaStream_t>(stream), 1);
 }
 
+// Host <-> device staging as a kernel node (SW_ENGINE_KERNEL_IO): the pinned
+// host buffer is read / written through its UVA mapping with 16-byte accesses,
+// every SM keeping several in flight.  A captured cudaMemcpy node cost ~150 µs
+// of graph time for NASNet's 602 KB input + 4 KB output (tools/e2e_breakdown.py).
+__global__ void __launch_bounds__(256) io_copy_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
+                                                      int64_t n16, const float* __restrict__ src_tail,
+                                                      float* __restrict__ dst_tail, int tail) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const float4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = src[i];
+  if (blockIdx.x == 0 && (int)threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
+}
+
+int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes <= 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return (int)cudaErrorMisalignedAddress;
+  const int64_t n16 = bytes / 16;
+  const int tail = (int)((bytes % 16) / 4);
+  const float* st = reinterpret_cast<const float*>(src) + n16 * 4;
+  float* dt = reinterpret_cast<float*>(dst) + n16 * 4;
+  int64_t blocks = cdiv(n16, 256 * 4);
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  return (int)launch_k(io_copy_kernel, dim3((unsigned)blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+                       reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), n16, st, dt, tail);
+}
+
 }  // namespace sw

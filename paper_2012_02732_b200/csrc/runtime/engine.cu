@@ -293,14 +293,19 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     return code;
   };
   cudaError_t err;
+  const bool kio = (e->flags & SW_ENGINE_KERNEL_IO) != 0;
+  auto h2d = [&](uint64_t dev, uint64_t host, int64_t bytes) -> cudaError_t {
+    if (kio) return (cudaError_t)sw::launch_io_copy(reinterpret_cast<void*>(dev), reinterpret_cast<const void*>(host),
+                                                    bytes, origin);
+    return cudaMemcpyAsync(reinterpret_cast<void*>(dev), reinterpret_cast<const void*>(host), (size_t)bytes,
+                           cudaMemcpyHostToDevice, origin);
+  };
   if (with_io && e->in_bytes > 0) {
-    err = cudaMemcpyAsync(reinterpret_cast<void*>(e->dev_in), reinterpret_cast<const void*>(e->host_in),
-                          (size_t)e->in_bytes, cudaMemcpyHostToDevice, origin);
+    err = h2d(e->dev_in, e->host_in, e->in_bytes);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture H2D"));
   }
   for (size_t i = 0; with_io && i < e->extra_host.size(); ++i) {
-    err = cudaMemcpyAsync(reinterpret_cast<void*>(e->extra_dev[i]), reinterpret_cast<const void*>(e->extra_host[i]),
-                          (size_t)e->extra_bytes[i], cudaMemcpyHostToDevice, origin);
+    err = h2d(e->extra_dev[i], e->extra_host[i], e->extra_bytes[i]);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture extra H2D"));
   }
   err = cudaEventRecord(e->fork, origin);
@@ -340,8 +345,10 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "join wait"));
   }
   if (with_io && e->out_bytes > 0) {
-    err = cudaMemcpyAsync(reinterpret_cast<void*>(e->host_out), reinterpret_cast<const void*>(e->dev_out),
-                          (size_t)e->out_bytes, cudaMemcpyDeviceToHost, origin);
+    err = kio ? (cudaError_t)sw::launch_io_copy(reinterpret_cast<void*>(e->host_out),
+                                               reinterpret_cast<const void*>(e->dev_out), e->out_bytes, origin)
+              : cudaMemcpyAsync(reinterpret_cast<void*>(e->host_out), reinterpret_cast<const void*>(e->dev_out),
+                                (size_t)e->out_bytes, cudaMemcpyDeviceToHost, origin);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture D2H"));
   }
   CU(cudaStreamEndCapture(origin, &sl.graph));

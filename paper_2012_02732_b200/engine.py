@@ -388,7 +388,7 @@ class Engine:
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
-                 tuning_cache: str | None = None):
+                 tuning_cache: str | None = None, kernel_io: bool = True):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -399,6 +399,7 @@ class Engine:
         self.conv_impl = conv_impl
         self.pdl = pdl
         self.tuning_cache = tuning_cache
+        self.kernel_io = kernel_io
         self.tuning = {}
         self.tuning_log = {}
         self._h = None
@@ -475,7 +476,7 @@ class Engine:
         N.check(lib.sw_engine_set_io(h, self.h_in.data_ptr(), self.d_in.data_ptr(),
                                      self.h_in.numel() * 4, self.h_out.data_ptr(),
                                      self.d_out_ptr, self.out_bytes))
-        N.check(lib.sw_engine_set_flags(h, 1 if self.pdl else 0))  # tuning sees the graph's PDL edges
+        N.check(lib.sw_engine_set_flags(h, self._flags()))  # tuning sees the graph's PDL edges
         t3 = time.perf_counter()
         if self.conv_impl == "auto":
             self.d_in.copy_(ex.reshape(-1).to(dev))
@@ -495,6 +496,10 @@ class Engine:
                                       dtype=np.int64)
         self.prepared = True
         return self
+
+    def _flags(self) -> int:
+        """SW_ENGINE_PDL | SW_ENGINE_KERNEL_IO (include/streamweave_b200.h)."""
+        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0)
 
     def _tuning_signature(self):
         import hashlib
@@ -583,7 +588,7 @@ class Engine:
         graph's own issue / dependency floor.  Recapture again to restore."""
         if pdl is not None:
             self.pdl = pdl
-        N.check(N.lib().sw_engine_set_flags(self._h, (1 if self.pdl else 0) | (2 if null_kernels else 0)))
+        N.check(N.lib().sw_engine_set_flags(self._h, self._flags() | (2 if null_kernels else 0)))
         self._capture(SLOT_MULTI_IO, self.schedule, True)
         self._capture(SLOT_SINGLE_IO, self.schedule_single, True)
         self._capture(SLOT_MULTI, self.schedule, False)
