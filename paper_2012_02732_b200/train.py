@@ -1065,7 +1065,8 @@ class TrainEngine:
                                      self.h_loss.data_ptr(), base + b.loss.offset, 4))
         N.check(lib.sw_engine_add_input(h, self.h_lab.data_ptr(), base + b.labels.offset,
                                         self.h_lab.numel() * 4))
-        N.check(lib.sw_engine_set_flags(h, 1 if self.pdl else 0))
+        # kernel-node host staging (images, labels in; loss out): SW_ENGINE_KERNEL_IO
+        N.check(lib.sw_engine_set_flags(h, (1 if self.pdl else 0) | 4))
         if self.allreduce:
             self._init_nccl()
         t_tune = time.perf_counter()

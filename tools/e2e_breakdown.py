@@ -61,7 +61,7 @@ def main():
     tag = "kernel-node IO" if e2.kernel_io else "memcpy-node IO"
     res[f"[{tag}] engine(x) e2e"] = wall(lambda: e2(xh), a.iters)
     res[f"[{tag}] device time per replay with IO"] = e2.time_replay(True, 200, io=True)[0]
-    ok = torch.equal(e2(xh), eng(xh))
+    ok = torch.allclose(e2(xh), eng(xh), rtol=1e-4, atol=1e-5)  # picks may differ (autotune)
     for k, v in res.items():
         print(f"{v:9.1f} us  {k}")
     print("outputs identical across IO modes:", ok)
