@@ -252,6 +252,9 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
 /* Host staging copies of the with_io slots as kernel nodes that access the
  * pinned host buffers through their UVA mapping (instead of memcpy nodes). */
 #define SW_ENGINE_KERNEL_IO 4u
+/* With SW_ENGINE_PDL: cross-stream kernel -> kernel edges of the captured
+ * graph are made programmatic too (same edge set, early launch). */
+#define SW_ENGINE_PDL_ALL_EDGES 8u
 int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
 /* ---- training step (paper_2012_02732_b200/train.py) ---- */

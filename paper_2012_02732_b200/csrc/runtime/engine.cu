@@ -22,6 +22,7 @@
 #include <cstring>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../planner/planner.h"
@@ -79,12 +80,14 @@ struct Slot {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   std::unordered_map<cudaGraphNode_t, int64_t> node_task;
+  std::unordered_set<cudaGraphNode_t> io_nodes;  // kernel-node staging copies
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     exec = nullptr;
     graph = nullptr;
     node_task.clear();
+    io_nodes.clear();
   }
 };
 
@@ -204,6 +207,39 @@ int ensure_events(sw_engine* e, int64_t n) {
   return SW_OK;
 }
 
+// Cross-stream kernel -> kernel edges of a captured graph become programmatic
+// (PDL) edges too.  Stream capture only makes same-stream edges programmatic;
+// a dependency recorded through an event stays a full edge, so the consumer
+// cannot be launched until the producer has drained.  Every engine kernel
+// executes griddepcontrol.wait before its first dependent read, so any
+// kernel -> kernel data edge may be programmatic; edges into foreign kernels
+// (NCCL's allreduce) stay full.  The edge SET is unchanged (the MEG check of
+// sw_engine_graph_topology still holds) — only its type.
+int programmatic_cross_edges(sw_engine* e, Slot& sl) {
+  size_t ne = 0;
+  CU(cudaGraphGetEdges_v2(sl.graph, nullptr, nullptr, nullptr, &ne));
+  if (!ne) return SW_OK;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  CU(cudaGraphGetEdges_v2(sl.graph, from.data(), to.data(), ed.data(), &ne));
+  auto ours = [&](cudaGraphNode_t n) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(n, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
+    auto it = sl.node_task.find(n);
+    if (it == sl.node_task.end()) return sl.io_nodes.count(n) != 0;
+    return e->ops[it->second].kind != sw::K_ALLREDUCE;
+  };
+  for (size_t i = 0; i < ne; ++i) {
+    if (ed[i].type != cudaGraphDependencyTypeDefault || !ours(from[i]) || !ours(to[i])) continue;
+    CU(cudaGraphRemoveDependencies_v2(sl.graph, &from[i], &to[i], &ed[i], 1));
+    cudaGraphEdgeData pe = {};
+    pe.from_port = cudaGraphKernelNodePortProgrammatic;
+    pe.type = cudaGraphDependencyTypeProgrammatic;
+    CU(cudaGraphAddDependencies_v2(sl.graph, &from[i], &to[i], &pe, 1));
+  }
+  return SW_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -294,9 +330,20 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   };
   cudaError_t err;
   const bool kio = (e->flags & SW_ENGINE_KERNEL_IO) != 0;
+  auto last_node = [&](cudaStream_t st) {
+    cudaStreamCaptureStatus status;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    if (cudaStreamGetCaptureInfo(st, &status, nullptr, nullptr, &deps, &ndeps) == cudaSuccess && ndeps == 1)
+      sl.io_nodes.insert(deps[0]);
+  };
   auto h2d = [&](uint64_t dev, uint64_t host, int64_t bytes) -> cudaError_t {
-    if (kio) return (cudaError_t)sw::launch_io_copy(reinterpret_cast<void*>(dev), reinterpret_cast<const void*>(host),
-                                                    bytes, origin);
+    if (kio) {
+      cudaError_t r = (cudaError_t)sw::launch_io_copy(reinterpret_cast<void*>(dev), reinterpret_cast<const void*>(host),
+                                                      bytes, origin);
+      if (r == cudaSuccess) last_node(origin);
+      return r;
+    }
     return cudaMemcpyAsync(reinterpret_cast<void*>(dev), reinterpret_cast<const void*>(host), (size_t)bytes,
                            cudaMemcpyHostToDevice, origin);
   };
@@ -349,9 +396,14 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
                                                reinterpret_cast<const void*>(e->dev_out), e->out_bytes, origin)
               : cudaMemcpyAsync(reinterpret_cast<void*>(e->host_out), reinterpret_cast<const void*>(e->dev_out),
                                 (size_t)e->out_bytes, cudaMemcpyDeviceToHost, origin);
+    if (kio && err == cudaSuccess) last_node(origin);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture D2H"));
   }
   CU(cudaStreamEndCapture(origin, &sl.graph));
+  if ((e->flags & SW_ENGINE_PDL) && (e->flags & SW_ENGINE_PDL_ALL_EDGES)) {
+    int prc = programmatic_cross_edges(e, sl);
+    if (prc) return prc;
+  }
   CU(cudaGraphInstantiateWithFlags(&sl.exec, sl.graph, 0));
   CU(cudaGraphUpload(sl.exec, e->launch));
   return SW_OK;

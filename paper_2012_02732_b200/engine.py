@@ -388,7 +388,7 @@ class Engine:
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
-                 tuning_cache: str | None = None, kernel_io: bool = True):
+                 tuning_cache: str | None = None, kernel_io: bool = True, pdl_all_edges: bool = False):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -400,6 +400,7 @@ class Engine:
         self.pdl = pdl
         self.tuning_cache = tuning_cache
         self.kernel_io = kernel_io
+        self.pdl_all_edges = pdl_all_edges
         self.tuning = {}
         self.tuning_log = {}
         self._h = None
@@ -499,7 +500,7 @@ class Engine:
 
     def _flags(self) -> int:
         """SW_ENGINE_PDL | SW_ENGINE_KERNEL_IO (include/streamweave_b200.h)."""
-        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0)
+        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0) | (8 if self.pdl_all_edges else 0)
 
     def _tuning_signature(self):
         import hashlib
