@@ -217,6 +217,10 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
                       const int64_t* order, int32_t with_io);
 /* Replay a captured slot on the engine's launch stream (async). */
 int sw_engine_replay(sw_engine* e, int32_t slot);
+/* One inference from host memory: copy host_in (in_bytes) into the pinned
+ * staging buffer, replay a with_io slot, wait, copy the staged output to
+ * host_out (out_bytes).  Either pointer may be NULL (staging used as is). */
+int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_out);
 /* Replay and wait; returns host wall time of the launch call in ns. */
 int sw_engine_replay_sync(sw_engine* e, int32_t slot, int64_t* out_launch_ns);
 /* Time `iters` replays with cudaEvents on the launch stream → mean µs,

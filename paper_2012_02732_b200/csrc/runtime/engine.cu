@@ -425,6 +425,17 @@ int sw_engine_replay_sync(sw_engine* e, int32_t slot, int64_t* out_launch_ns) {
   return SW_OK;
 }
 
+int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_out) {
+  if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  if (host_in && reinterpret_cast<uint64_t>(host_in) != e->host_in)
+    std::memcpy(reinterpret_cast<void*>(e->host_in), host_in, (size_t)e->in_bytes);
+  CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
+  CU(cudaStreamSynchronize(e->launch));
+  if (host_out && reinterpret_cast<uint64_t>(host_out) != e->host_out)
+    std::memcpy(host_out, reinterpret_cast<const void*>(e->host_out), (size_t)e->out_bytes);
+  return SW_OK;
+}
+
 int sw_engine_time_replay(sw_engine* e, int32_t slot, int32_t iters, double* out_gpu_us, double* out_host_us) {
   if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
   if (iters < 1) iters = 1;
