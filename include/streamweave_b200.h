@@ -242,6 +242,9 @@ int sw_engine_graph_topology(sw_engine* e, int32_t slot, int64_t cap, int64_t* o
 /* Per-op device time (µs) of one eager pass, CUDA events around each op. */
 int sw_engine_profile_ops(sw_engine* e, int64_t n, const int64_t* order, int32_t reps,
                           double* out_us);
+/* Per-task start / end (µs since the traced graph's start) of the last replay
+ * of a slot captured with SW_ENGINE_TRACE; -1 for tasks never recorded. */
+int sw_engine_trace_read(sw_engine* e, int64_t n, double* out_start_us, double* out_end_us);
 /* Launch stream handle (cudaStream_t as integer) for external interop. */
 int sw_engine_stream(sw_engine* e, uint64_t* out_stream);
 /* Kernel selection support: device time (µs, mean of `reps` back-to-back
@@ -259,6 +262,10 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
 /* With SW_ENGINE_PDL: cross-stream kernel -> kernel edges of the captured
  * graph are made programmatic too (same edge set, early launch). */
 #define SW_ENGINE_PDL_ALL_EDGES 8u
+/* Diagnostic: timing events around every task of subsequent captures; after a
+ * replay, sw_engine_trace_read returns each task's start / end in µs from the
+ * graph's start (the measured timeline behind a Chrome trace). */
+#define SW_ENGINE_TRACE 16u
 int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
 /* ---- training step (paper_2012_02732_b200/train.py) ---- */

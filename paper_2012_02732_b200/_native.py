@@ -93,6 +93,7 @@ PROTOTYPES = {
     "sw_engine_replay": (C.c_int, [C.c_void_p, i32]),
     "sw_engine_replay_sync": (C.c_int, [C.c_void_p, i32, P64]),
     "sw_engine_infer": (C.c_int, [C.c_void_p, i32, C.c_void_p, C.c_void_p]),
+    "sw_engine_trace_read": (C.c_int, [C.c_void_p, i64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "sw_engine_time_replay": (C.c_int, [C.c_void_p, i32, i32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]),
     "sw_engine_launch_op": (C.c_int, [C.c_void_p, i64]),

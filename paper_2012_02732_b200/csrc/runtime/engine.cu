@@ -110,6 +110,9 @@ struct sw_engine {
   std::vector<uint64_t> extra_host, extra_dev;
   std::vector<int64_t> extra_bytes;
   void* nccl_comm = nullptr;  // ncclComm_t of the data-parallel group (K_ALLREDUCE)
+  // SW_ENGINE_TRACE: timing events around every task (measured Chrome trace)
+  std::vector<cudaEvent_t> tr_start, tr_end;
+  cudaEvent_t tr0 = nullptr;
   int nccl_ranks = 0;
 };
 
@@ -272,6 +275,9 @@ int sw_engine_destroy(sw_engine* e) {
   for (auto s : e->streams) cudaStreamDestroy(s);
   for (auto ev : e->events) cudaEventDestroy(ev);
   for (auto ev : e->joins) cudaEventDestroy(ev);
+  for (auto ev : e->tr_start) cudaEventDestroy(ev);
+  for (auto ev : e->tr_end) cudaEventDestroy(ev);
+  if (e->tr0) cudaEventDestroy(e->tr0);
   cudaEventDestroy(e->fork);
   cudaEventDestroy(e->t0);
   cudaEventDestroy(e->t1);
@@ -316,8 +322,28 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   rc = ensure_events(e, max_event + 1);
   if (rc) return rc;
 
+  const bool trace = (e->flags & SW_ENGINE_TRACE) != 0;
+  if (trace) {
+    if (!e->tr0) CU(cudaEventCreate(&e->tr0));
+    while (e->tr_start.size() < e->ops.size()) {
+      cudaEvent_t a, b;
+      CU(cudaEventCreate(&a));
+      CU(cudaEventCreate(&b));
+      e->tr_start.push_back(a);
+      e->tr_end.push_back(b);
+    }
+  }
   cudaStream_t origin = e->launch;
   CU(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
+  if (trace) {
+    cudaError_t te = cudaEventRecord(e->tr0, origin);
+    if (te != cudaSuccess) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(origin, &g);
+      if (g) cudaGraphDestroy(g);
+      return cuda_fail(te, "trace t0 record");
+    }
+  }
   struct PdlScope {
     explicit PdlScope(bool on) { sw::g_launch_pdl = on; }
     ~PdlScope() { sw::g_launch_pdl = false; }
@@ -370,6 +396,8 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     cudaStream_t st = e->streams[s];
     if (op_kind[k] == SW_OP_LAUNCH) {
       int64_t t = op_arg[k];
+      if (trace && (err = cudaEventRecord(e->tr_start[t], st)) != cudaSuccess)
+        return abort_capture(cuda_fail(err, "trace record"));
       rc = (e->flags & SW_ENGINE_NULL_KERNELS) ? (sw::launch_null(st) ? SW_CUDA_ERROR : 0) : launch_task(e, e->ops[t], st);
       if (rc) return abort_capture(rc);
       cudaStreamCaptureStatus status;
@@ -377,6 +405,8 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
       size_t ndeps = 0;
       err = cudaStreamGetCaptureInfo(st, &status, nullptr, nullptr, &deps, &ndeps);
       if (err == cudaSuccess && ndeps == 1) sl.node_task[deps[0]] = t;
+      if (trace && (err = cudaEventRecord(e->tr_end[t], st)) != cudaSuccess)
+        return abort_capture(cuda_fail(err, "trace record"));
     } else if (op_kind[k] == SW_OP_RECORD) {
       err = cudaEventRecord(e->events[op_arg[k]], st);
       if (err != cudaSuccess) return abort_capture(cuda_fail(err, "event record"));
@@ -609,6 +639,23 @@ int sw_engine_nccl_init(sw_engine* e, int32_t nranks, int32_t rank, const char* 
   if (r != 0) return sw::fail(SW_CUDA_ERROR, std::string("ncclCommInitRank: ") + (g_nccl.err ? g_nccl.err(r) : "?"));
   e->nccl_comm = comm;
   e->nccl_ranks = nranks;
+  return SW_OK;
+}
+
+int sw_engine_trace_read(sw_engine* e, int64_t n, double* out_start_us, double* out_end_us) {
+  if (!e->tr0) return sw::fail(SW_VALUE_ERROR, "no traced capture (SW_ENGINE_TRACE)");
+  CU(cudaStreamSynchronize(e->launch));
+  for (int64_t t = 0; t < n; ++t) {
+    out_start_us[t] = out_end_us[t] = -1.0;
+    if (t >= (int64_t)e->tr_start.size()) continue;
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, e->tr0, e->tr_start[t]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, e->tr0, e->tr_end[t]) == cudaSuccess) {
+      out_start_us[t] = 1000.0 * a;
+      out_end_us[t] = 1000.0 * b;
+    }
+  }
+  cudaGetLastError();  // never-recorded events leave a sticky-free error
   return SW_OK;
 }
 

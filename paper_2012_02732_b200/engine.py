@@ -678,6 +678,38 @@ class Engine:
         e = int(ne[0])
         return kinds[:n], task[:n], edges[:2 * e].reshape(-1, 2)
 
+    def trace(self, multi: bool = True, warm: int = 3):
+        """Measured timeline of one device-resident replay:
+        the schedule is re-captured with timing events around every task
+        (SW_ENGINE_TRACE; the events sit between kernels, so same-stream PDL
+        overlap is lost in this diagnostic capture), replayed, read back, and
+        the normal capture restored.  Returns (intervals {task: (start_us,
+        end_us)}, Chrome-trace JSON in the reference's format, sim.py:277-294,
+        tid = logical stream)."""
+        from .sim import SimResult, chrome_trace
+        lib = N.lib()
+        slot = SLOT_MULTI if multi else SLOT_SINGLE
+        ts = self.schedule if multi else self.schedule_single
+        try:
+            N.check(lib.sw_engine_set_flags(self._h, self._flags() | 16))
+            self._capture(slot, ts, False)
+            for _ in range(warm + 1):
+                N.check(lib.sw_engine_replay(self._h, slot))
+            n = len(self.program.tasks)
+            a = np.zeros(n, dtype=np.float64)
+            b = np.zeros(n, dtype=np.float64)
+            N.check(lib.sw_engine_trace_read(self._h, n, a.ctypes.data_as(C.POINTER(C.c_double)),
+                                             b.ctypes.data_as(C.POINTER(C.c_double))))
+        finally:
+            N.check(lib.sw_engine_set_flags(self._h, self._flags()))
+            self._capture(slot, ts, False)
+        intervals = {t: (float(a[t]), float(b[t])) for t in range(len(a)) if a[t] >= 0}
+        stream_of = self.assignment.stream_of if multi else {t: 0 for t in intervals}
+        lo = min(v[0] for v in intervals.values())
+        hi = max(v[1] for v in intervals.values())
+        res = SimResult(hi - lo, sum(e - s for s, e in intervals.values()), intervals, {})
+        return intervals, chrome_trace(res, self.graph, stream_of)
+
     def roofline_sum_us(self, hbm_gbs: float, tflops: float) -> float:
         return sum(roofline_us(t, hbm_gbs, tflops) for t in self.program.tasks)
 

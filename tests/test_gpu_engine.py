@@ -397,3 +397,23 @@ def test_captured_graph_edges_are_the_meg(name):
 def test_engine_rejects_cpu_only_use():
     # the public engine has no CPU fallback
     assert hasattr(sw, "Engine")
+
+
+@pytest.mark.parametrize("name", ["cell", "nasnet_mobile"])
+def test_measured_trace_respects_the_dag(name):
+    """the measured timeline (timing events around every task
+    of a replay) covers every task, follows every DAG edge, and the normal
+    capture is restored afterwards (same output)."""
+    import json
+    model, shape = build_model(name)
+    x = example_input(shape)
+    eng = Engine(model, conv_impl="simt").prepare(x)
+    y0 = eng(x)
+    iv, js = eng.trace(multi=True)
+    assert set(iv) == {t.tid for t in eng.program.tasks}
+    for u, v in eng.graph.edges:
+        assert iv[v][0] >= iv[u][1] - 1e-3, (u, v)
+    rows = json.loads(js)
+    assert len(rows) == len(iv) and {r["tid"] for r in rows} <= set(eng.assignment.stream_of.values())
+    assert torch.equal(eng(x), y0)
+    eng.close()
