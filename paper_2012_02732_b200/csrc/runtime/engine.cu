@@ -336,7 +336,7 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   cudaStream_t origin = e->launch;
   CU(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
   if (trace) {
-    cudaError_t te = cudaEventRecord(e->tr0, origin);
+    cudaError_t te = cudaEventRecordWithFlags(e->tr0, origin, cudaEventRecordExternal);
     if (te != cudaSuccess) {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(origin, &g);
@@ -396,7 +396,7 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     cudaStream_t st = e->streams[s];
     if (op_kind[k] == SW_OP_LAUNCH) {
       int64_t t = op_arg[k];
-      if (trace && (err = cudaEventRecord(e->tr_start[t], st)) != cudaSuccess)
+      if (trace && (err = cudaEventRecordWithFlags(e->tr_start[t], st, cudaEventRecordExternal)) != cudaSuccess)
         return abort_capture(cuda_fail(err, "trace record"));
       rc = (e->flags & SW_ENGINE_NULL_KERNELS) ? (sw::launch_null(st) ? SW_CUDA_ERROR : 0) : launch_task(e, e->ops[t], st);
       if (rc) return abort_capture(rc);
@@ -405,7 +405,7 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
       size_t ndeps = 0;
       err = cudaStreamGetCaptureInfo(st, &status, nullptr, nullptr, &deps, &ndeps);
       if (err == cudaSuccess && ndeps == 1) sl.node_task[deps[0]] = t;
-      if (trace && (err = cudaEventRecord(e->tr_end[t], st)) != cudaSuccess)
+      if (trace && (err = cudaEventRecordWithFlags(e->tr_end[t], st, cudaEventRecordExternal)) != cudaSuccess)
         return abort_capture(cuda_fail(err, "trace record"));
     } else if (op_kind[k] == SW_OP_RECORD) {
       err = cudaEventRecord(e->events[op_arg[k]], st);
