@@ -120,12 +120,12 @@ __device__ __forceinline__ void tile_epilogue(const Epi& ep, const float* part, 
       v = reinterpret_cast<const float4*>(part)[g];
     } else {
       v = make_float4(0.f, 0.f, 0.f, 0.f);
-      float4 t[8];
+      float4 t[16];  // up to 16 ranks (non-portable cluster size)
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < 16; ++r)
         if (r < nr) t[r] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, r))[g];
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < 16; ++r)
         if (r < nr) v = f4add(v, t[r]);
     }
     const int q = m % ep.Q;

@@ -272,8 +272,12 @@ static size_t simt_smem_bytes(int bm, int bn) {
 void init_simt_kernels() {
   for (int i = 0; i < kNumSimt; ++i)
     for (int j = 0; j < 2; ++j)
+    {
       cudaFuncSetAttribute(kSimt[i].fn[j], cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)simt_smem_bytes(kSimt[i].bm, kSimt[i].bn));
+      // split-K clusters of 16 (weight-streaming layers at batch 1 want >8 CTAs per tile)
+      cudaFuncSetAttribute(kSimt[i].fn[j], cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
 }
 
 int launch_conv(const sw_op_desc& op, void* stream) {

@@ -404,9 +404,13 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
 // Pre-set the dynamic smem limits outside any stream capture.
 void init_tc_kernels() {
   cudaFuncSetAttribute(conv_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<64>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_kernel<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<128>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_kernel<128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<256>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_kernel<256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
 }  // namespace sw

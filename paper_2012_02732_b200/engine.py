@@ -119,7 +119,7 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
             continue  # tile mostly padding
         if ctas > 16 * NUM_SMS and bm * bn < 2048:
             continue  # far too many tiny CTAs
-        for split in (1, 2, 4, 8):
+        for split in (1, 2, 4, 8, 16):
             if split > 1 and (ksteps // split < 2 or ctas * split > 4 * NUM_SMS):
                 continue
             out.append((K_CONV, v, split))
@@ -143,7 +143,7 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
         if bn > max(32, kcap):
             continue
         ctas = math.ceil(M / 128) * math.ceil(K / bn)
-        for split in (1, 2, 4, 8):
+        for split in (1, 2, 4, 8, 16):
             if split > 1 and (ktiles // split < 1 or ctas * split > 2 * NUM_SMS):
                 continue
             out.append((K_CONV_TC, bn, split))
