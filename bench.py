@@ -379,6 +379,8 @@ def run_ours(args, world, rank, local):
                     "d2h_bytes_per_step": int(eng.out_bytes)},
             "gpu_launches": n_tasks * args.steps,
             "tasks": n_tasks, "streams": eng.assignment.num_streams, "syncs": len(eng.plan),
+            "arena": {"mode": eng.arena_mode, "bytes": int(eng.arena.numel()),
+                      "never_free_bytes": int(eng.arena_layout.reference_total) if eng.arena_layout else None},
             "clocks": clock_info,
             "parity": parity,
             "prepare_s": {k: round(v, 3) for k, v in eng.plan_seconds.items()},
@@ -451,6 +453,7 @@ def other_configs(args, dev, hbm, bf16, flush, stream):
             "multi_over_single": round(single_us / multi_us, 4),
             "tasks": len(eng.program.tasks), "streams": eng.assignment.num_streams,
             "syncs": len(eng.plan), "roofline_sum_us": round(roof, 3),
+            "arena_mb": round(eng.arena.numel() / 1e6, 2),
             "prepare_s": round(time.perf_counter() - t0, 2)}
         eng.close()
     return out

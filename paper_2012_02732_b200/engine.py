@@ -388,7 +388,8 @@ class Engine:
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
-                 tuning_cache: str | None = None, kernel_io: bool = True, pdl_all_edges: bool = False):
+                 tuning_cache: str | None = None, kernel_io: bool = True, pdl_all_edges: bool = False,
+                 arena: str = "hb"):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -401,6 +402,9 @@ class Engine:
         self.tuning_cache = tuning_cache
         self.kernel_io = kernel_io
         self.pdl_all_edges = pdl_all_edges
+        if arena not in ("hb", "reference"):
+            raise ValueError(f"arena must be 'hb' or 'reference', not {arena!r}")
+        self.arena_mode = arena
         self.tuning = {}
         self.tuning_log = {}
         self._h = None
@@ -427,18 +431,29 @@ class Engine:
         self.plan_seconds = {"trace": t1 - t0, "assign+pre_run": t2 - t1}
 
         dev = torch.device("cuda", self.device)
-        # activation arena: offsets straight from the reference arena layout
-        self.arena = torch.empty(max(ts.arena.total, 256), dtype=torch.uint8, device=dev)
+        # activation arena: happens-before-aware reuse (arena.py, SURVEY §8(f)
+        # f2) by default; "reference" = the reference arena layout as
+        # pre_run computed it (no frees, every activation lives all pass)
+        if self.arena_mode == "hb":
+            from .arena import plan_arena
+            layout = plan_arena(prog, ts)
+            offset_of = dict(layout.offsets)
+            arena_total = layout.total
+            self.arena_layout = layout
+        else:
+            offset_of = {}
+            owned = {}
+            for st in prog.storages:
+                if st.owner >= 0:
+                    owned.setdefault(st.owner, []).append(st)
+            for tid, sts in owned.items():
+                offs = ts.task_args[tid]
+                for st, off in zip(sts, offs):
+                    offset_of[st.sid] = off
+            arena_total = ts.arena.total
+            self.arena_layout = None
+        self.arena = torch.empty(max(arena_total, 256), dtype=torch.uint8, device=dev)
         abase = self.arena.data_ptr()
-        offset_of = {}
-        owned = {}
-        for st in prog.storages:
-            if st.owner >= 0:
-                owned.setdefault(st.owner, []).append(st)
-        for tid, sts in owned.items():
-            offs = ts.task_args[tid]
-            for st, off in zip(sts, offs):
-                offset_of[st.sid] = off
         inp = prog.input_view.st
         self.d_in = torch.empty(inp.n * inp.c * inp.h * inp.w, dtype=torch.float32, device=dev)
         base_map = {}

@@ -188,15 +188,26 @@ def run_op(mem: HostMemory, d):
         raise NotImplementedError(d.kind)
 
 
-def emulate(model, x, fuse=True, multi_stream=True):
-    """Run the lowered program on the host; returns (output, program, ops)."""
+def emulate(model, x, fuse=True, multi_stream=True, hb_arena=False):
+    """Run the lowered program on the host; returns (output, program, ops).
+    hb_arena=True places the activations with the engine's happens-before
+    arena (arena.py): storages share memory wherever the capture orders them."""
     prog = build_program(model, x, fuse=fuse)
     g = prog.graph
     total = sum(st.alloc_bytes for st in prog.storages)
     arrays = E._pack_weights(prog)
     wtotal = sum((a.nbytes + 255) // 256 * 256 for a in arrays.values())
     mem = HostMemory(total + wtotal + 8192)
-    base = {st.sid: mem.alloc(st.alloc_bytes) for st in prog.storages}
+    if hb_arena:
+        from paper_2012_02732_b200 import assign_streams as _as
+        from paper_2012_02732_b200.arena import plan_arena
+        f0, p0 = _as(g) if multi_stream else (StreamAssignment({t.id: 0 for t in g.nodes}), SyncPlan(()))
+        layout = plan_arena(prog, pre_run(g, f0, p0))
+        abase = mem.alloc(layout.total)
+        base = {st.sid: (mem.alloc(st.alloc_bytes) if st.role == "input" else abase + layout.offsets[st.sid])
+                for st in prog.storages}
+    else:
+        base = {st.sid: mem.alloc(st.alloc_bytes) for st in prog.storages}
     wbase = mem.alloc(wtotal)
     woff = {}
     off = 0

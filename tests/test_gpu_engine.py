@@ -417,3 +417,20 @@ def test_measured_trace_respects_the_dag(name):
     assert len(rows) == len(iv) and {r["tid"] for r in rows} <= set(eng.assignment.stream_of.values())
     assert torch.equal(eng(x), y0)
     eng.close()
+
+
+@pytest.mark.parametrize("name", ["nasnet_mobile", "inception_v3"])
+def test_hb_arena_matches_never_free_arena(name):
+    """the happens-before arena reuses memory yet the replay
+    (multi- and single-stream) is bit-identical to the never-free layout."""
+    model, shape = build_model(name)
+    x = example_input(shape)
+    a = Engine(model, conv_impl="simt", arena="hb").prepare(x)
+    b = Engine(model, conv_impl="simt", arena="reference").prepare(x)
+    assert a.arena.numel() < 0.6 * b.arena.numel()
+    for multi in (True, False):
+        a.multi_stream = b.multi_stream = multi
+        for _ in range(3):
+            assert torch.equal(a(x), b(x))
+    a.close()
+    b.close()
