@@ -105,9 +105,9 @@ def summarize_launches(path: str) -> str:
     return "\n".join(out) + "\n"
 
 
-FAMILY = {"sepconv_kernel": "sepconv", "conv_simt_kernel": "conv", "conv_tc_kernel": "conv",
-          "conv_gemv_kernel": "conv", "spatial_kernel<0": "dwconv", "spatial_kernel<1": "pool",
-          "global_pool": "gpool", "ew_": "eltwise"}
+FAMILY = {"sepconv_kernel": "sepconv", "sepconv_tma_kernel": "sepconv", "conv_simt_kernel": "conv",
+          "conv_tc_kernel": "conv", "pw_tma_kernel": "conv", "conv_gemv_kernel": "conv",
+          "spatial_kernel<0": "dwconv", "spatial_kernel<1": "pool", "global_pool": "gpool", "ew_": "eltwise"}
 
 
 def traffic_json(path: str) -> dict:
