@@ -259,9 +259,6 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
 /* Host staging copies of the with_io slots as kernel nodes that access the
  * pinned host buffers through their UVA mapping (instead of memcpy nodes). */
 #define SW_ENGINE_KERNEL_IO 4u
-/* With SW_ENGINE_PDL: cross-stream kernel -> kernel edges of the captured
- * graph are made programmatic too (same edge set, early launch). */
-#define SW_ENGINE_PDL_ALL_EDGES 8u
 /* Diagnostic: timing events around every task of subsequent captures; after a
  * replay, sw_engine_trace_read returns each task's start / end in µs from the
  * graph's start (the measured timeline behind a Chrome trace). */

@@ -19,6 +19,8 @@
 #include <dlfcn.h>
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -210,39 +212,6 @@ int ensure_events(sw_engine* e, int64_t n) {
   return SW_OK;
 }
 
-// Cross-stream kernel -> kernel edges of a captured graph become programmatic
-// (PDL) edges too.  Stream capture only makes same-stream edges programmatic;
-// a dependency recorded through an event stays a full edge, so the consumer
-// cannot be launched until the producer has drained.  Every engine kernel
-// executes griddepcontrol.wait before its first dependent read, so any
-// kernel -> kernel data edge may be programmatic; edges into foreign kernels
-// (NCCL's allreduce) stay full.  The edge SET is unchanged (the MEG check of
-// sw_engine_graph_topology still holds) — only its type.
-int programmatic_cross_edges(sw_engine* e, Slot& sl) {
-  size_t ne = 0;
-  CU(cudaGraphGetEdges_v2(sl.graph, nullptr, nullptr, nullptr, &ne));
-  if (!ne) return SW_OK;
-  std::vector<cudaGraphNode_t> from(ne), to(ne);
-  std::vector<cudaGraphEdgeData> ed(ne);
-  CU(cudaGraphGetEdges_v2(sl.graph, from.data(), to.data(), ed.data(), &ne));
-  auto ours = [&](cudaGraphNode_t n) {
-    cudaGraphNodeType t;
-    if (cudaGraphNodeGetType(n, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
-    auto it = sl.node_task.find(n);
-    if (it == sl.node_task.end()) return sl.io_nodes.count(n) != 0;
-    return e->ops[it->second].kind != sw::K_ALLREDUCE;
-  };
-  for (size_t i = 0; i < ne; ++i) {
-    if (ed[i].type != cudaGraphDependencyTypeDefault || !ours(from[i]) || !ours(to[i])) continue;
-    CU(cudaGraphRemoveDependencies_v2(sl.graph, &from[i], &to[i], &ed[i], 1));
-    cudaGraphEdgeData pe = {};
-    pe.from_port = cudaGraphKernelNodePortProgrammatic;
-    pe.type = cudaGraphDependencyTypeProgrammatic;
-    CU(cudaGraphAddDependencies_v2(sl.graph, &from[i], &to[i], &pe, 1));
-  }
-  return SW_OK;
-}
-
 }  // namespace
 
 extern "C" {
@@ -430,10 +399,6 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture D2H"));
   }
   CU(cudaStreamEndCapture(origin, &sl.graph));
-  if ((e->flags & SW_ENGINE_PDL) && (e->flags & SW_ENGINE_PDL_ALL_EDGES)) {
-    int prc = programmatic_cross_edges(e, sl);
-    if (prc) return prc;
-  }
   CU(cudaGraphInstantiateWithFlags(&sl.exec, sl.graph, 0));
   CU(cudaGraphUpload(sl.exec, e->launch));
   return SW_OK;

@@ -388,8 +388,7 @@ class Engine:
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
-                 tuning_cache: str | None = None, kernel_io: bool = True, pdl_all_edges: bool = False,
-                 arena: str = "hb"):
+                 tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb"):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -401,7 +400,6 @@ class Engine:
         self.pdl = pdl
         self.tuning_cache = tuning_cache
         self.kernel_io = kernel_io
-        self.pdl_all_edges = pdl_all_edges
         if arena not in ("hb", "reference"):
             raise ValueError(f"arena must be 'hb' or 'reference', not {arena!r}")
         self.arena_mode = arena
@@ -515,7 +513,7 @@ class Engine:
 
     def _flags(self) -> int:
         """SW_ENGINE_PDL | SW_ENGINE_KERNEL_IO (include/streamweave_b200.h)."""
-        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0) | (8 if self.pdl_all_edges else 0)
+        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0)
 
     def _tuning_signature(self):
         import hashlib
