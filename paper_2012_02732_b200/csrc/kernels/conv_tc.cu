@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -339,6 +340,169 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant for 1x1 / stride-1 convolutions (pure GEMMs on NHWC:
+// A = activations [M pixels][C], B = pre-split weights [K][Kpad]).
+//   * operands arrive by cp.async.bulk.tensor (3-D tensor maps whose box is
+//     exactly the canonical no-swizzle K-major UMMA layout [k16-chunk][row][16 B]),
+//     completing on a per-stage "full" mbarrier; one thread issues every copy;
+//   * the weights of the first stages are requested before the PDL wait
+//     (constants), the activations after it;
+//   * the 128 threads split the activation stage into tf32 hi / lo (3xTF32),
+//     one elected thread issues the 12 MMAs of the stage and commits them to a
+//     per-stage "done" mbarrier, and the same thread immediately refills the
+//     stage the previous MMAs just released — the other threads never wait on
+//     the tensor pipe, only on data.
+// ---------------------------------------------------------------------------
+struct TcMaps {
+  CUtensorMap a, bh, bl;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    conv_tc_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
+                       const __grid_constant__ CUtensorMap tbl, TcArgs a) {
+  using L = TcSmem<BN>;
+  constexpr int S = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BODY);
+  uint64_t* done = full + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + S);
+  const uint32_t sbase = smem_u32(smem);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int m0 = blockIdx.x * TC_BM;
+  const int n0 = blockIdx.y * BN;
+  const int ktiles = (a.Kdim + TC_BK - 1) / TC_BK;
+  const int per = (ktiles + a.split - 1) / a.split;
+  const int kt0 = blockIdx.z * per;
+  const int iters = max(0, min(ktiles, kt0 + per) - kt0);
+  constexpr uint32_t A_TX = L::A_BYTES, B_TX = 2 * L::B_BYTES;
+
+  if (tid == 0) {
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tbh);
+    prefetch_tmap(&tbl);
+    for (int st = 0; st < S; ++st) {
+      mbar_init(smem_u32(&full[st]), 1);
+      mbar_init(smem_u32(&done[st]), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)L::NCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto load_b = [&](int kt, int st) {
+    const uint32_t stage = sbase + st * L::STAGE;
+    const int kc = (kt0 + kt) * (TC_BK / 4);
+    const uint32_t bar = smem_u32(&full[st]);
+    tma_load_3d(stage + 2 * L::A_BYTES, &tbh, 0, n0, kc, bar);
+    tma_load_3d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, 0, n0, kc, bar);
+  };
+  auto load_a = [&](int kt, int st) {
+    const uint32_t stage = sbase + st * L::STAGE;
+    tma_load_3d(stage, &ta, 0, m0, (kt0 + kt) * (TC_BK / 4), smem_u32(&full[st]));
+  };
+  if (tid == 0) {
+    for (int st = 0; st < S && st < iters; ++st) {
+      mbar_expect_tx(smem_u32(&full[st]), A_TX + B_TX);
+      load_b(st, st);
+    }
+  }
+  pdl_trigger();
+  pdl_wait();
+  if (tid == 0)
+    for (int st = 0; st < S && st < iters; ++st) load_a(st, st);
+
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                         ((uint32_t)(TC_BM >> 4) << 24);
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+    const int st = it % S;
+    mbar_wait(smem_u32(&full[st]), (it / S) & 1);
+    {
+      float4* hi = reinterpret_cast<float4*>(smem + st * L::STAGE);
+      float4* lo = reinterpret_cast<float4*>(smem + st * L::STAGE + L::A_BYTES);
+#pragma unroll 2
+      for (int i = tid; i < L::A_BYTES / 16; i += TC_THREADS) {
+        float4 x = hi[i];
+        if (a.pre_relu) {
+          x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+        }
+        const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+        hi[i] = h;
+        lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t a_hi = sbase + st * L::STAGE, a_lo = a_hi + L::A_BYTES;
+      const uint32_t b_hi = a_hi + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
+      constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
+#pragma unroll
+      for (int ks = 0; ks < TC_BK / 8; ++ks) {
+        const uint64_t ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
+        const uint64_t al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
+        const uint64_t bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
+        const uint64_t bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+        mma_tf32(tmem, ah, bh, idesc, (it | ks) ? 1u : 0u);
+        mma_tf32(tmem, ah, bl, idesc, 1u);
+        mma_tf32(tmem, al, bh, idesc, 1u);
+      }
+      mma_commit(smem_u32(&done[st]));
+      // refill the stage the PREVIOUS tile's MMAs are releasing
+      if (it >= 1 && it - 1 + S < iters) {
+        const int ps = (it - 1) % S;
+        mbar_wait(smem_u32(&done[ps]), ((it - 1) / S) & 1);
+        mbar_expect_tx(smem_u32(&full[ps]), A_TX + B_TX);
+        load_b(it - 1 + S, ps);
+        load_a(it - 1 + S, ps);
+      }
+    }
+  }
+  if (iters > 0) {
+    const int last = iters - 1;
+    mbar_wait(smem_u32(&done[last % S]), (last / S) & 1);
+  }
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  float* part = reinterpret_cast<float*>(smem);
+  __syncthreads();
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    float v[16];
+    if (iters > 0) {
+      tmem_ld16(t_row + c0, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+  }
+  cg::cluster_group cluster = cg::this_cluster();
+  tile_epilogue<TC_BM, BN, TC_THREADS>(a.epi, part, m0, n0, a.split, cluster);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)L::NCOLS)
+                 : "memory");
+  }
+}
+
 static TcArgs tc_args(const sw_op_desc& op) {
   const int64_t* p = op.params;
   TcArgs a;
@@ -373,11 +537,44 @@ static TcArgs tc_args(const sw_op_desc& op) {
 }
 
 // variant = N tile (32, 64, 128, 256); SP_SPLIT_K = cluster split along K.
+template <int BN>
+static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st) {
+  // 1x1 / stride 1 / no padding on 16-B aligned NHWC rows only
+  if (a.R != 1 || a.S != 1 || a.sh != 1 || a.sw != 1 || a.ph != 0 || a.pw != 0 || !a.vec)
+    return (int)cudaErrorInvalidValue;
+  if (a.in_sn != (int64_t)a.H * a.W * a.in_sw || a.in_sh != (int64_t)a.W * a.in_sw) return (int)cudaErrorInvalidValue;
+  CUtensorMap ta, tbh, tbl;
+  {  // activations: (4 floats, M rows, C/4 chunks)
+    const uint64_t dims[3] = {4, (uint64_t)a.M, (uint64_t)(a.C / 4)};
+    const uint64_t str[2] = {(uint64_t)a.in_sw * 4, 16};
+    const uint32_t box[3] = {4, TC_BM, TC_BK / 4};
+    if (!encode_tmap_f32(&ta, a.in, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
+  }
+  {  // weights hi / lo: (4 floats, K rows, Kpad/4 chunks)
+    const uint64_t dims[3] = {4, (uint64_t)a.K, (uint64_t)(a.Kpad / 4)};
+    const uint64_t str[2] = {(uint64_t)a.Kpad * 4, 16};
+    const uint32_t box[3] = {4, (uint32_t)BN, TC_BK / 4};
+    if (!encode_tmap_f32(&tbh, a.w_hi, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
+    if (!encode_tmap_f32(&tbl, a.w_lo, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
+  }
+  dim3 grid((unsigned)cdiv(a.M, TC_BM), (unsigned)cdiv(a.K, BN), (unsigned)a.split);
+  return (int)launch_k(conv_tc_tma_kernel<BN>, grid, dim3(TC_THREADS), (size_t)TcSmem<BN>::TOTAL, st,
+                       (unsigned)a.split, ta, tbh, tbl, a);
+}
+
 int launch_conv_tc(const sw_op_desc& op, void* stream) {
   TcArgs a = tc_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a.M == 0 || a.K == 0) return 0;
   if (!a.w_hi || !a.w_lo || a.Kpad < a.Kdim || a.Kpad % TC_BK) return (int)cudaErrorInvalidValue;
+  // variants 1000 + BN: the TMA-fed kernel (1x1 convolutions)
+  switch (op.variant) {
+    case 1032: return launch_tc_tma<32>(a, op, st);
+    case 1064: return launch_tc_tma<64>(a, op, st);
+    case 1128: return launch_tc_tma<128>(a, op, st);
+    case 1256: return launch_tc_tma<256>(a, op, st);
+    default: break;
+  }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), 1, (unsigned)a.split);
   switch (op.variant) {
     case 32:
@@ -405,12 +602,20 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
 void init_tc_kernels() {
   cudaFuncSetAttribute(conv_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32>::TOTAL);
   cudaFuncSetAttribute(conv_tc_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<64>::TOTAL);
   cudaFuncSetAttribute(conv_tc_kernel<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<64>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<128>::TOTAL);
   cudaFuncSetAttribute(conv_tc_kernel<128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<128>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<128>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<256>::TOTAL);
   cudaFuncSetAttribute(conv_tc_kernel<256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<256>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
 }  // namespace sw

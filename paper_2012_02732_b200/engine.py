@@ -139,6 +139,7 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
     kcap = 32
     while kcap < K:
         kcap *= 2
+    pointwise = R == 1 and S == 1 and tuple(pad) == (0, 0)
     for bn in (32, 64, 128, 256):
         if bn > max(32, kcap):
             continue
@@ -147,6 +148,8 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
             if split > 1 and (ktiles // split < 1 or ctas * split > 2 * NUM_SMS):
                 continue
             out.append((K_CONV_TC, bn, split))
+            if pointwise:  # TMA-fed tcgen05 kernel (conv_tc.cu); refuses strided / unaligned layouts
+                out.append((K_CONV_TC, 1000 + bn, split))
     return out
 
 

@@ -100,6 +100,37 @@ def test_tcgen05_tiles_and_splits(bn, split):
     eng.close()
 
 
+@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+@pytest.mark.parametrize("split", [1, 2, 8, 16])
+@pytest.mark.parametrize("cin,cout,hw,batch,pre", [(264, 88, 28, 2, True), (1056, 200, 7, 1, False),
+                                                   (44, 1000, 9, 3, True)])
+def test_tcgen05_tma_pointwise(bn, split, cin, cout, hw, batch, pre):
+    """TMA-fed tcgen05 1x1 conv (variants 1000 + N tile): every N tile and
+    split-K cluster size, ragged M / N / K, pre-ReLU on load, fused BN bias."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
+    torch.manual_seed(3)
+    m = Conv(cin, cout, 1, 1, 0, bias=False, act=None, bn=True).eval()
+    if pre:
+        m = nn.Sequential(nn.ReLU(), nn.Conv2d(cin, cin, 1, bias=False), m)  # relu on the 2nd conv's input
+    x = torch.randn(batch, cin, hw, hw)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="tc").prepare(x)
+    last = eng.ops[len(eng.program.tasks) - 1]
+    assert last.kind == K_CONV_TC
+    last.variant = 1000 + bn
+    last.params[SP_SPLIT_K] = split
+    rc = N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops)
+    N.check(rc)
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 class DW(nn.Module):
     def __init__(self, c, k, s, p, pre_relu=True):
         super().__init__()
