@@ -111,8 +111,10 @@ def test_tcgen05_tma_pointwise(bn, split, cin, cout, hw, batch, pre):
     from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
     torch.manual_seed(3)
     m = Conv(cin, cout, 1, 1, 0, bias=False, act=None, bn=True).eval()
-    if pre:
-        m = nn.Sequential(nn.ReLU(), nn.Conv2d(cin, cin, 1, bias=False), m)  # relu on the 2nd conv's input
+    # a leading 1x1 conv makes the tested conv read an NHWC activation (the
+    # network input is NCHW); with `pre` a ReLU between them is applied on load
+    lead = [nn.Conv2d(cin, cin, 1, bias=False)] + ([nn.ReLU()] if pre else [])
+    m = nn.Sequential(*lead, m).eval()
     x = torch.randn(batch, cin, hw, hw)
     with torch.no_grad():
         ref = m(x)
