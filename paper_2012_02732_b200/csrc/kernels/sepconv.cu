@@ -54,7 +54,54 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 
 }  // namespace
 
-template <int KS, bool VEC, int BM, int BN, int TM, int TN>
+// Row-blocked depthwise (PX > 1, large batches): a thread owns PX adjacent
+// output pixels of one row and slides the k-tap window along the input row in
+// registers, so each input element is loaded once per row of taps instead of
+// up to k times (7x7 s1: 10 loads for 4 outputs instead of 28 per tap row).
+template <int KS, int SWC, int PX, int V, bool VEC>
+__device__ __forceinline__ void dw_row_block(const SepArgs& a, const float* base, const float* Wd, int Cp, int c,
+                                             int ih0, int iw0, float (&acc)[PX][V]) {
+  constexpr int NW = (PX - 1) * SWC + KS;
+#pragma unroll
+  for (int r = 0; r < KS; ++r) {
+    const int ih = ih0 + r;
+    if ((unsigned)ih >= (unsigned)a.H) continue;
+    float xr[NW][V];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      const int iw = iw0 + j;
+      const bool ok = (unsigned)iw < (unsigned)a.W;
+      const float* src = base + (ok ? ih * a.in_sh + iw * a.in_sw : 0);
+      if constexpr (VEC) {
+        float4 x = __ldg(reinterpret_cast<const float4*>(src));
+        const float msk = ok ? 1.f : 0.f;
+        xr[j][0] = x.x * msk; xr[j][1 % V] = x.y * msk; xr[j][2 % V] = x.z * msk; xr[j][3 % V] = x.w * msk;
+      } else {
+        xr[j][0] = ok ? __ldg(src) : 0.f;
+      }
+      if (a.pre_relu) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) xr[j][v] = fmaxf(xr[j][v], 0.f);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      float w[V];
+      if constexpr (VEC) {
+        const float4 w4 = *reinterpret_cast<const float4*>(&Wd[(r * KS + s) * Cp + c]);
+        w[0] = w4.x; w[1 % V] = w4.y; w[2 % V] = w4.z; w[3 % V] = w4.w;
+      } else {
+        w[0] = Wd[(r * KS + s) * Cp + c];
+      }
+#pragma unroll
+      for (int px = 0; px < PX; ++px)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[px][v] = fmaf(xr[px * SWC + s][v], w[v], acc[px][v]);
+    }
+  }
+}
+
+template <int KS, bool VEC, int BM, int BN, int TM, int TN, int PX = 1>
 __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   static_assert((BM / TM) * (BN / TN) == SEP_THREADS, "256 threads");
   extern __shared__ __align__(16) float smem[];
@@ -115,6 +162,65 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   // ---- depthwise into D[px][c] (zero for padded channels / pixels past M) ----
   constexpr int V = VEC ? 4 : 1;
   const int cgroups = Cp / V;
+  if constexpr (PX > 1 && KS > 0) {
+#pragma unroll 1
+    for (int e = tid; e < (BM / PX) * cgroups; e += SEP_THREADS) {
+      const int cg = e % cgroups;
+      const int px0 = (e / cgroups) * PX;
+      const int c = cg * V;
+      const int m = m0 + px0;
+      float acc[PX][V];
+#pragma unroll
+      for (int j = 0; j < PX; ++j)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[j][v] = 0.f;
+      if (m < a.M && c < a.C) {
+        const int q = m % a.Q;
+        const int t = m / a.Q;
+        const int p = t % a.P, nb = t / a.P;
+        const float* base = a.in + nb * a.in_sn + c * a.in_sc;
+        const int ih0 = p * a.sh - a.ph, iw0 = q * a.sw - a.pw;
+        if (q + PX - 1 < a.Q && m + PX - 1 < a.M && a.sw <= 2) {
+          if (a.sw == 1)
+            dw_row_block<KS, 1, PX, V, VEC>(a, base, Wd, Cp, c, ih0, iw0, acc);
+          else
+            dw_row_block<KS, 2, PX, V, VEC>(a, base, Wd, Cp, c, ih0, iw0, acc);
+        } else {
+          // row wrap / ragged end: pixel by pixel (unrolled: acc stays in registers)
+#pragma unroll
+          for (int j = 0; j < PX; ++j) {
+            const int mj = m + j;
+            if (mj >= a.M) continue;
+            const int qj = mj % a.Q, tj = mj / a.Q;
+            const int pj = tj % a.P, nj = tj / a.P;
+            const float* bj = a.in + nj * a.in_sn + c * a.in_sc;
+            float one[1][V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) one[0][v] = 0.f;
+            if (a.sw == 1)
+              dw_row_block<KS, 1, 1, V, VEC>(a, bj, Wd, Cp, c, pj * a.sh - a.ph, qj * a.sw - a.pw, one);
+            else
+              dw_row_block<KS, 2, 1, V, VEC>(a, bj, Wd, Cp, c, pj * a.sh - a.ph, qj * a.sw - a.pw, one);
+#pragma unroll
+            for (int v = 0; v < V; ++v) acc[j][v] = one[0][v];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < PX; ++j)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[j][v] = apply_act(acc[j][v] + (a.b_dw ? a.b_dw[c + v] : 0.f), a.dw_act);
+      }
+#pragma unroll
+      for (int j = 0; j < PX; ++j) {
+        if constexpr (VEC) {
+          *reinterpret_cast<float4*>(&D[(px0 + j) * Cp + c]) = make_float4(acc[j][0], acc[j][1 % V], acc[j][2 % V],
+                                                                          acc[j][3 % V]);
+        } else {
+          D[(px0 + j) * Cp + c] = acc[j][0];
+        }
+      }
+    }
+  } else
 #pragma unroll 1
   for (int e = tid; e < BM * cgroups; e += SEP_THREADS) {
     const int cg = e % cgroups;
@@ -480,6 +586,10 @@ struct SepCfg {
 // variant → tile (all 256 threads)
 constexpr SepCfg kSep[] = {{16, 32}, {8, 64}, {16, 64}, {32, 32}, {8, 32}, {32, 64}};
 constexpr int kNumSep = sizeof(kSep) / sizeof(kSep[0]);
+// row-blocked depthwise variants (4 pixels per thread), after the TMA ones
+constexpr int kSepRowFirst = 11;
+constexpr SepCfg kSepRow[] = {{64, 32}, {128, 32}, {64, 64}};
+constexpr int kNumSepRow = 3;
 constexpr int kSepSmemMax = 227 * 1024;
 }  // namespace
 
@@ -498,6 +608,9 @@ static cudaError_t launch_sep_v(int v, const SepArgs& a, dim3 grid, size_t smem,
     case 3: return launch_k(sepconv_kernel<KS, VEC, 32, 32, 2, 2>, grid, dim3(SEP_THREADS), smem, st, 1, a);
     case 4: return launch_k(sepconv_kernel<KS, VEC, 8, 32, 1, 1>, grid, dim3(SEP_THREADS), smem, st, 1, a);
     case 5: return launch_k(sepconv_kernel<KS, VEC, 32, 64, 2, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 11: return launch_k(sepconv_kernel<KS, VEC, 64, 32, 2, 4, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 12: return launch_k(sepconv_kernel<KS, VEC, 128, 32, 4, 4, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 13: return launch_k(sepconv_kernel<KS, VEC, 64, 64, 4, 4, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
     default: return launch_k(sepconv_kernel<KS, VEC, 16, 32, 1, 2>, grid, dim3(SEP_THREADS), smem, st, 1, a);
   }
 }
@@ -631,11 +744,17 @@ int launch_sepconv(const sw_op_desc& op, void* stream) {
       default: return (int)cudaErrorInvalidValue;
     }
   }
-  const int v = (op.variant >= 0 && op.variant < kNumSep) ? op.variant : 0;
-  const size_t smem = sep_smem(a.C, a.R, a.S, kSep[v].bm, kSep[v].bn);
-  if (smem > (size_t)kSepSmemMax) return (int)cudaErrorInvalidValue;  // the autotuner skips it
-  dim3 grid((unsigned)cdiv(a.M, kSep[v].bm), (unsigned)cdiv(a.K, kSep[v].bn));
   const int ks = (a.R == a.S && (a.R == 3 || a.R == 5 || a.R == 7)) ? a.R : 0;
+  int v = (op.variant >= 0 && op.variant < kNumSep) ? op.variant : 0;
+  SepCfg cfg = kSep[v];
+  if (op.variant >= kSepRowFirst && op.variant < kSepRowFirst + kNumSepRow) {
+    if (!ks || a.sw > 2) return (int)cudaErrorInvalidValue;  // row blocking needs a fixed k x k window
+    v = op.variant;
+    cfg = kSepRow[v - kSepRowFirst];
+  }
+  const size_t smem = sep_smem(a.C, a.R, a.S, cfg.bm, cfg.bn);
+  if (smem > (size_t)kSepSmemMax) return (int)cudaErrorInvalidValue;  // the autotuner skips it
+  dim3 grid((unsigned)cdiv(a.M, cfg.bm), (unsigned)cdiv(a.K, cfg.bn));
   return (int)(a.vec ? launch_sep_ks<true>(ks, v, a, grid, smem, st) : launch_sep_ks<false>(ks, v, a, grid, smem, st));
 }
 
@@ -647,6 +766,14 @@ static void init_sep_ks() {
   cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 32, 32, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
   cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 8, 32, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
   cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 32, 64, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSepSmemMax);
+  if constexpr (KS > 0) {
+    cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 64, 32, 2, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSepSmemMax);
+    cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 128, 32, 4, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSepSmemMax);
+    cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 64, 64, 4, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSepSmemMax);
+  }
 }
 
 template <int KS, int SW>

@@ -83,8 +83,11 @@ def pick_conv_variant(M: int, K: int, Kdim: int, R: int, S: int, pad, stride) ->
 # csrc/kernels/sepconv.cu kSep[]: variant → (BM pixels, BN channels), 256 threads
 SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (32, 64),
              # TMA-staged kernel (one output row per CTA): BM pixels x BN channels
-             6: (4, 32), 7: (8, 32), 8: (8, 64), 9: (16, 32), 10: (16, 64)}
+             6: (4, 32), 7: (8, 32), 8: (8, 64), 9: (16, 32), 10: (16, 64),
+             # row-blocked depthwise (4 pixels per thread, large batches)
+             11: (64, 32), 12: (128, 32), 13: (64, 64)}
 SEP_TMA_FIRST = 6
+SEP_ROW_FIRST = 11
 
 # csrc/kernels/conv1x1.cu: TMA-staged pointwise conv, conv variant → (BM, BN)
 PW_TILES = {16: (8, 32), 17: (16, 32), 18: (32, 32), 19: (16, 64), 20: (32, 64), 21: (64, 32)}
@@ -571,7 +574,7 @@ class Engine:
                 cands = [(K_SEPCONV, v, 1) for v in SEP_TILES]
                 # TMA kernel with the depthwise split over a cluster of the column blocks
                 cands += [(K_SEPCONV, v, 2) for v, (bm, bn) in SEP_TILES.items()
-                          if v >= SEP_TMA_FIRST and 2 <= math.ceil(K / bn) <= 8]
+                          if SEP_TMA_FIRST <= v < SEP_ROW_FIRST and 2 <= math.ceil(K / bn) <= 8]
             else:
                 cands = conv_candidates(M, K, Kdim, p[SP_R], p[SP_S], (p[SP_PAD_H], p[SP_PAD_W]))
             for kind, variant, split in cands:

@@ -156,6 +156,33 @@ def test_depthwise(c, k, s, p, h):
     close(y, ref)
 
 
+@pytest.mark.parametrize("variant", [11, 12, 13])
+@pytest.mark.parametrize("c,k,s,h,batch", [(44, 5, 1, 14, 3), (11, 7, 2, 23, 2), (32, 7, 2, 111, 2),
+                                           (176, 3, 1, 7, 5), (24, 3, 2, 9, 3)])
+def test_sepconv_row_blocked_variants(variant, c, k, s, h, batch):
+    """Row-blocked depthwise (4 pixels per thread): rows that wrap inside a
+    4-pixel group, ragged image ends, stride 1 / 2, NHWC vector (leading 1x1
+    conv) and scalar channel counts."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_SEPCONV, SLOT_MULTI
+    torch.manual_seed(4)
+    m = nn.Sequential(nn.Conv2d(c, c, 1, bias=False), DW(c, k, s, k // 2)).eval()
+    x = torch.randn(batch, c, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    idx = [i for i in range(len(eng.program.tasks)) if eng.ops[i].kind == K_SEPCONV]
+    assert len(idx) == 1
+    eng.ops[idx[0]].variant = variant
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 @pytest.mark.parametrize("variant", range(6))
 @pytest.mark.parametrize("c,k,s,h", [(44, 5, 1, 14), (11, 7, 2, 23), (176, 3, 1, 7)])
 def test_sepconv_tile_variants(variant, c, k, s, h):
