@@ -263,6 +263,92 @@ static const SimtCfg kSimt[] = {
 };
 constexpr int kNumSimt = sizeof(kSimt) / sizeof(kSimt[0]);
 
+// Direct convolution for thin layers (variant 9): K <= 32 output channels and
+// R*S*C <= 576 (NASNet's stem: 3x3 s2 3→32 on the NCHW image, 1x1 32→11 /
+// 44→22 at 111² / 56²).  A GEMM tile would be mostly padding there and the
+// layer is memory bound: one thread per output pixel keeps all K
+// accumulators in registers, the filter sits in shared memory as [rsc][K]
+// (warp-uniform broadcast reads), and each pixel's outputs leave as one
+// contiguous run (float4 when the layout allows).
+template <int KB>
+__global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
+  extern __shared__ float wsm[];  // [Kdim][KB] + bias[KB]
+  const int tid = threadIdx.x;
+  for (int e = tid; e < a.Kdim * KB; e += blockDim.x) {
+    const int k = e % KB, j = e / KB;  // j = (r, s, c) in the [K][R][S][C] weight order
+    wsm[e] = k < a.K ? __ldg(a.w + (int64_t)k * a.Kdim + j) : 0.f;
+  }
+  float* bsm = wsm + a.Kdim * KB;
+  if (tid < KB) bsm[tid] = (a.bias && tid < a.K) ? __ldg(a.bias + tid) : 0.f;
+  pdl_trigger();
+  pdl_wait();
+  __syncthreads();
+  const int m = blockIdx.x * blockDim.x + tid;
+  if (m >= a.M) return;
+  const int q = m % a.Q;
+  const int t = m / a.Q;
+  const int p = t % a.P, nb = t / a.P;
+  float acc[KB];
+#pragma unroll
+  for (int k = 0; k < KB; ++k) acc[k] = bsm[k];
+  const int ih0 = p * a.sh - a.ph, iw0 = q * a.sw - a.pw;
+  const float* base = a.in + nb * a.in_sn;
+  const bool cvec = a.in_sc == 1 && (a.C & 3) == 0;
+#pragma unroll 1
+  for (int r = 0; r < a.R; ++r) {
+    const int ih = ih0 + r;
+    if ((unsigned)ih >= (unsigned)a.H) continue;
+#pragma unroll 1
+    for (int s = 0; s < a.S; ++s) {
+      const int iw = iw0 + s;
+      if ((unsigned)iw >= (unsigned)a.W) continue;
+      const float* src = base + ih * a.in_sh + iw * a.in_sw;
+      const float* wr = wsm + ((r * a.S + s) * a.C) * KB;
+      if (cvec) {
+#pragma unroll 1
+        for (int c = 0; c < a.C; c += 4) {
+          float4 x = __ldg(reinterpret_cast<const float4*>(src + c));
+          if (a.pre_relu) {
+            x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+          }
+          const float* w0 = wr + c * KB;
+#pragma unroll
+          for (int k = 0; k < KB; ++k)
+            acc[k] = fmaf(x.x, w0[k], fmaf(x.y, w0[KB + k], fmaf(x.z, w0[2 * KB + k], fmaf(x.w, w0[3 * KB + k], acc[k]))));
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < a.C; ++c) {
+          float x = __ldg(src + c * a.in_sc);
+          if (a.pre_relu) x = fmaxf(x, 0.f);
+          const float* w0 = wr + c * KB;
+#pragma unroll
+          for (int k = 0; k < KB; ++k) acc[k] = fmaf(x, w0[k], acc[k]);
+        }
+      }
+    }
+  }
+  float* o = a.out + nb * a.out_sn + p * a.out_sh + q * a.out_sw;
+  const float* rp = a.has_res ? a.res + nb * a.res_sn + p * a.res_sh + q * a.res_sw : nullptr;
+  if (a.epi.vec && (a.K & 3) == 0) {
+#pragma unroll
+    for (int k = 0; k < KB; k += 4) {
+      if (k >= a.K) break;
+      float4 v = make_float4(acc[k], acc[k + 1], acc[k + 2], acc[k + 3]);
+      if (rp) v = f4add(v, *reinterpret_cast<const float4*>(rp + k));
+      *reinterpret_cast<float4*>(o + k) = act4(v, a.act);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      if (k >= a.K) break;
+      float v = acc[k];
+      if (rp) v += rp[k * a.res_sc];
+      o[k * a.out_sc] = apply_act(v, a.act);
+    }
+  }
+}
+
 static size_t simt_smem_bytes(int bm, int bn) {
   const size_t tile = 8 * 16 * (size_t)(bm + 4) + 8 * 16 * (size_t)(bn + 4);  // STAGES * BK * (B? + PAD)
   const size_t part = (size_t)bm * bn;
@@ -270,6 +356,9 @@ static size_t simt_smem_bytes(int bm, int bn) {
 }
 
 void init_simt_kernels() {
+  cudaFuncSetAttribute(conv_direct_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32) * 4);
   for (int i = 0; i < kNumSimt; ++i)
     for (int j = 0; j < 2; ++j)
     {
@@ -288,6 +377,15 @@ int launch_conv(const sw_op_desc& op, void* stream) {
     if (a.M > 8 || a.R != 1 || a.S != 1) return (int)cudaErrorInvalidValue;
     int blocks = (int)cdiv((int64_t)a.K * 32, 256);
     return (int)launch_k(conv_gemv_kernel<8>, dim3(blocks), dim3(256), 0, st, 1, a);
+  }
+  if (op.variant == 9) {
+    if (a.K > 32 || a.Kdim > 576 || a.split != 1) return (int)cudaErrorInvalidValue;
+    const int kb = a.K <= 8 ? 8 : (a.K <= 16 ? 16 : 32);
+    const size_t smem = ((size_t)a.Kdim * kb + kb) * sizeof(float);
+    const dim3 grid((unsigned)cdiv(a.M, 128));
+    if (kb == 8) return (int)launch_k(conv_direct_kernel<8>, grid, dim3(128), smem, st, 1, a);
+    if (kb == 16) return (int)launch_k(conv_direct_kernel<16>, grid, dim3(128), smem, st, 1, a);
+    return (int)launch_k(conv_direct_kernel<32>, grid, dim3(128), smem, st, 1, a);
   }
   if (op.variant >= 16) return launch_conv_pw(op, op.variant - 16, stream);  // conv1x1.cu (TMA)
   if (op.variant < 0 || op.variant >= kNumSimt) return (int)cudaErrorInvalidValue;

@@ -115,6 +115,8 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
     out = []
     if M <= 8 and R == 1 and S == 1 and tuple(pad) == (0, 0):
         out.append((K_CONV, 8, 1))
+    if K <= 32 and Kdim <= 576 and M >= 1024:
+        out.append((K_CONV, 9, 1))  # direct thin-layer kernel (conv.cu conv_direct_kernel)
     ksteps = math.ceil(Kdim / 16)
     for v, (bm, bn) in SIMT_TILES.items():
         ctas = math.ceil(M / bm) * math.ceil(K / bn)

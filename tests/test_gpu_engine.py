@@ -156,6 +156,36 @@ def test_depthwise(c, k, s, p, h):
     close(y, ref)
 
 
+@pytest.mark.parametrize("cin,cout,k,s,p,h,lead,relu", [
+    (3, 32, 3, 2, 0, 45, False, False),    # NASNet conv0 shape: NCHW image, scalar channel loads
+    (32, 11, 1, 1, 0, 37, True, True),     # stem conv_1x1: odd K, scalar stores, ReLU on load
+    (44, 24, 1, 1, 0, 28, True, False),    # float4 loads and stores
+    (11, 13, 5, 2, 2, 23, True, True),     # odd everything, padding
+])
+def test_direct_thin_conv(cin, cout, k, s, p, h, lead, relu):
+    """conv variant 9 (direct, one thread per output pixel) forced."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV, SLOT_MULTI
+    torch.manual_seed(5)
+    layers = ([nn.Conv2d(cin, cin, 1, bias=False)] if lead else []) + ([nn.ReLU()] if relu else [])
+    m = nn.Sequential(*layers, Conv(cin, cout, k, s, p, bias=False, act=None, bn=True)).eval()
+    x = torch.randn(3, cin, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    t = len(eng.program.tasks) - 1
+    assert eng.ops[t].kind == K_CONV
+    eng.ops[t].variant = 9
+    eng.ops[t].params[30] = 1  # SP_SPLIT_K
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 @pytest.mark.parametrize("variant", [11, 12, 13])
 @pytest.mark.parametrize("c,k,s,h,batch", [(44, 5, 1, 14, 3), (11, 7, 2, 23, 2), (32, 7, 2, 111, 2),
                                            (176, 3, 1, 7, 5), (24, 3, 2, 9, 3)])
