@@ -92,8 +92,12 @@ def dist_setup(gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available() and torch.cuda.device_count() > 0:
+        # one GPU per rank; more ranks than GPUs (a plumbing check on a 1-GPU
+        # box with SW_DIST_BACKEND=gloo) share devices round-robin
+        local = local % torch.cuda.device_count()
     if world > 1:
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("SW_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
         dist.init_process_group(backend, init_method="env://")
@@ -111,6 +115,8 @@ def reduce_max(world, value, device=None):
         return value
     import torch
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = None  # gloo reduces host tensors
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
