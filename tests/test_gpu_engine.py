@@ -542,3 +542,19 @@ def test_engine_call_pinned_and_pageable_inputs_agree():
     assert not torch.equal(y2, y_pin)
     assert torch.equal(eng(x2.clone()), y2)
     eng.close()
+
+
+def test_engine_call_pinned_and_pageable_inputs_agree():
+    """engine(x) from pinned and pageable host tensors: same result; a later
+    call with another input sees the new input."""
+    model, shape = build_model("nasnet_mobile")
+    x = example_input(shape)
+    eng = Engine(model, conv_impl="simt").prepare(x)
+    y_page = eng(x.clone())
+    y_pin = eng(x.clone().pin_memory())
+    assert torch.equal(y_page, y_pin)
+    x2 = example_input(shape, seed=7)
+    y2 = eng(x2.clone().pin_memory())
+    assert not torch.equal(y2, y_pin)
+    assert torch.equal(eng(x2.clone()), y2)
+    eng.close()
