@@ -274,24 +274,11 @@ int launch_null(void* stream) {
 // host buffer is read / written through its UVA mapping with 16-byte accesses,
 // every SM keeping several in flight.  A captured cudaMemcpy node cost ~150 µs
 // of graph time for NASNet's 602 KB input + 4 KB output (tools/e2e_breakdown.py).
-// With a pointer slot (pinned host word, UVA-visible) the source / destination
-// of this replay is read at run time: sw_engine_infer points it at the
-// caller's own pinned buffer, so no host-side staging memcpy is needed.
 __global__ void __launch_bounds__(256) io_copy_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
                                                       int64_t n16, const float* __restrict__ src_tail,
-                                                      float* __restrict__ dst_tail, int tail,
-                                                      const volatile uint64_t* src_slot,
-                                                      const volatile uint64_t* dst_slot) {
+                                                      float* __restrict__ dst_tail, int tail) {
   pdl_trigger();
   pdl_wait();
-  if (src_slot) {
-    src = reinterpret_cast<const float4*>(*src_slot);
-    src_tail = reinterpret_cast<const float*>(src + n16);
-  }
-  if (dst_slot) {
-    dst = reinterpret_cast<float4*>(*dst_slot);
-    dst_tail = reinterpret_cast<float*>(dst + n16);
-  }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (; i + 3 * stride < n16; i += 4 * stride) {
@@ -305,8 +292,7 @@ __global__ void __launch_bounds__(256) io_copy_kernel(const float4* __restrict__
   if (blockIdx.x == 0 && (int)threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
 }
 
-int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream, const uint64_t* src_slot,
-                   const uint64_t* dst_slot) {
+int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream) {
   if (bytes <= 0) return 0;
   if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return (int)cudaErrorMisalignedAddress;
   const int64_t n16 = bytes / 16;
@@ -317,8 +303,7 @@ int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream, cons
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 4) blocks = 148 * 4;
   return (int)launch_k(io_copy_kernel, dim3((unsigned)blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
-                       reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), n16, st, dt, tail,
-                       src_slot, dst_slot);
+                       reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), n16, st, dt, tail);
 }
 
 }  // namespace sw

@@ -105,10 +105,6 @@ struct sw_engine {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   std::vector<sw_op_desc> ops;
   uint64_t host_in = 0, dev_in = 0, host_out = 0, dev_out = 0;
-  // pinned words read by the staging kernels at run time: [0] input source,
-  // [1] output destination (the staging buffers unless sw_engine_infer is
-  // handed pinned caller buffers)
-  uint64_t* io_slot = nullptr;
   int64_t in_bytes = 0, out_bytes = 0;
   uint32_t flags = 0;  // SW_ENGINE_PDL | SW_ENGINE_NULL_KERNELS
   Slot slots[kSlots];
@@ -256,7 +252,6 @@ int sw_engine_destroy(sw_engine* e) {
   cudaEventDestroy(e->t1);
   cudaStreamDestroy(e->launch);
   if (e->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(e->nccl_comm);
-  if (e->io_slot) cudaFreeHost(e->io_slot);
   delete e;
   return SW_OK;
 }
@@ -274,13 +269,6 @@ int sw_engine_set_io(sw_engine* e, uint64_t host_in, uint64_t dev_in, int64_t in
   e->host_out = host_out;
   e->dev_out = dev_out;
   e->out_bytes = out_bytes;
-  if (!e->io_slot) {
-    void* p = nullptr;
-    CU(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
-    e->io_slot = static_cast<uint64_t*>(p);
-  }
-  e->io_slot[0] = host_in;
-  e->io_slot[1] = host_out;
   return SW_OK;
 }
 
@@ -344,10 +332,10 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     if (cudaStreamGetCaptureInfo(st, &status, nullptr, nullptr, &deps, &ndeps) == cudaSuccess && ndeps == 1)
       sl.io_nodes.insert(deps[0]);
   };
-  auto h2d = [&](uint64_t dev, uint64_t host, int64_t bytes, const uint64_t* slot) -> cudaError_t {
+  auto h2d = [&](uint64_t dev, uint64_t host, int64_t bytes) -> cudaError_t {
     if (kio) {
       cudaError_t r = (cudaError_t)sw::launch_io_copy(reinterpret_cast<void*>(dev), reinterpret_cast<const void*>(host),
-                                                      bytes, origin, slot, nullptr);
+                                                      bytes, origin);
       if (r == cudaSuccess) last_node(origin);
       return r;
     }
@@ -355,11 +343,11 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
                            cudaMemcpyHostToDevice, origin);
   };
   if (with_io && e->in_bytes > 0) {
-    err = h2d(e->dev_in, e->host_in, e->in_bytes, e->io_slot);
+    err = h2d(e->dev_in, e->host_in, e->in_bytes);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture H2D"));
   }
   for (size_t i = 0; with_io && i < e->extra_host.size(); ++i) {
-    err = h2d(e->extra_dev[i], e->extra_host[i], e->extra_bytes[i], nullptr);
+    err = h2d(e->extra_dev[i], e->extra_host[i], e->extra_bytes[i]);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture extra H2D"));
   }
   err = cudaEventRecord(e->fork, origin);
@@ -404,8 +392,7 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   }
   if (with_io && e->out_bytes > 0) {
     err = kio ? (cudaError_t)sw::launch_io_copy(reinterpret_cast<void*>(e->host_out),
-                                               reinterpret_cast<const void*>(e->dev_out), e->out_bytes, origin,
-                                               nullptr, e->io_slot ? e->io_slot + 1 : nullptr)
+                                               reinterpret_cast<const void*>(e->dev_out), e->out_bytes, origin)
               : cudaMemcpyAsync(reinterpret_cast<void*>(e->host_out), reinterpret_cast<const void*>(e->dev_out),
                                 (size_t)e->out_bytes, cudaMemcpyDeviceToHost, origin);
     if (kio && err == cudaSuccess) last_node(origin);
@@ -433,28 +420,9 @@ int sw_engine_replay_sync(sw_engine* e, int32_t slot, int64_t* out_launch_ns) {
   return SW_OK;
 }
 
-static bool pinned16(const void* p) {
-  if (!p || (reinterpret_cast<uint64_t>(p) & 15)) return false;
-  cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return at.type == cudaMemoryTypeHost;
-}
-
 int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_out) {
   if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
-  // kernel-node staging reads / writes pinned caller buffers in place
-  const bool direct = (e->flags & SW_ENGINE_KERNEL_IO) && e->io_slot;
-  bool in_direct = false, out_direct = false;
-  if (direct) {
-    in_direct = host_in && pinned16(host_in);
-    out_direct = host_out && pinned16(host_out);
-    e->io_slot[0] = in_direct ? reinterpret_cast<uint64_t>(host_in) : e->host_in;
-    e->io_slot[1] = out_direct ? reinterpret_cast<uint64_t>(host_out) : e->host_out;
-  }
-  if (host_in && !in_direct && reinterpret_cast<uint64_t>(host_in) != e->host_in)
+  if (host_in && reinterpret_cast<uint64_t>(host_in) != e->host_in)
     std::memcpy(reinterpret_cast<void*>(e->host_in), host_in, (size_t)e->in_bytes);
   CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
   // spin on the stream instead of a blocking synchronize: the wake-up of a
@@ -464,12 +432,8 @@ int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_
   while ((q = cudaStreamQuery(e->launch)) == cudaErrorNotReady) {
   }
   if (q != cudaSuccess) return cuda_fail(q, "cudaStreamQuery");
-  if (host_out && !out_direct && reinterpret_cast<uint64_t>(host_out) != e->host_out)
+  if (host_out && reinterpret_cast<uint64_t>(host_out) != e->host_out)
     std::memcpy(host_out, reinterpret_cast<const void*>(e->host_out), (size_t)e->out_bytes);
-  if (direct) {  // later replays through the other entry points use the staging buffers
-    e->io_slot[0] = e->host_in;
-    e->io_slot[1] = e->host_out;
-  }
   return SW_OK;
 }
 

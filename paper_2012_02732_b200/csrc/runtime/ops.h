@@ -144,9 +144,7 @@ enum EwPtr : int { EP_A = 0, EP_B, EP_C, EP_OUT, EP_SCALE, EP_SHIFT };
 // Launch one op on a stream (kernels/*.cu). Returns cudaError_t as int.
 int launch_conv(const sw_op_desc& op, void* stream);
 int launch_null(void* stream);  // diagnostic empty task
-// staging copy as a kernel; a non-null slot supplies the host pointer at run time
-int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream, const uint64_t* src_slot = nullptr,
-                   const uint64_t* dst_slot = nullptr);
+int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream);  // staging copy as a kernel
 int launch_conv_pw(const sw_op_desc& op, int variant, void* stream);  // conv variants 16..21
 int launch_conv_tc(const sw_op_desc& op, void* stream);
 int launch_dwconv(const sw_op_desc& op, void* stream);

@@ -632,8 +632,7 @@ class Engine:
         out = torch.empty(self.out_shape, dtype=torch.float32)
         if xs.device.type == "cpu" and xs.dtype == torch.float32 and xs.is_contiguous() and \
                 xs.numel() == self.h_in.numel():
-            # one C call: replay (a pinned x is read in place by the staging
-            # kernel, a pageable one is first copied to the pinned staging), wait, copy out
+            # one C call: host copy into the pinned staging, replay, wait, copy out
             N.check(N.lib().sw_engine_infer(self._h, slot, xs.data_ptr(), out.data_ptr()))
             return out
         self.h_in.copy_(xs.reshape(self.h_in.shape))

@@ -527,24 +527,6 @@ def test_hb_arena_matches_never_free_arena(name):
 
 
 def test_engine_call_pinned_and_pageable_inputs_agree():
-    """engine(x) reads a pinned x in place (pointer slot of the staging kernel)
-    and copies a pageable one through the staging buffer: same result, and
-    later replays through the staging buffers still see the staged input."""
-    model, shape = build_model("nasnet_mobile")
-    x = example_input(shape)
-    eng = Engine(model, conv_impl="simt").prepare(x)
-    y_page = eng(x.clone())
-    xp = x.clone().pin_memory()
-    y_pin = eng(xp)
-    assert torch.equal(y_page, y_pin)
-    x2 = example_input(shape, seed=7)
-    y2 = eng(x2.clone().pin_memory())
-    assert not torch.equal(y2, y_pin)
-    assert torch.equal(eng(x2.clone()), y2)
-    eng.close()
-
-
-def test_engine_call_pinned_and_pageable_inputs_agree():
     """engine(x) from pinned and pageable host tensors: same result; a later
     call with another input sees the new input."""
     model, shape = build_model("nasnet_mobile")
