@@ -271,8 +271,9 @@ def run_ours(args, world, rank, local):
     eager = [eager_once() for _ in range(max(5, args.steps // 4))]
     eager_ms = 1e3 * sum(eager) / len(eager)
 
-    # e2e through the public API: host tensor in (pinned, as the contract's
-    # e2e specifies; the staging kernel reads it in place), host tensor out
+    # e2e through the public API: host tensor in (pinned host memory, as the
+    # contract's e2e specifies; copied into the engine's pinned staging buffer
+    # inside the call), host tensor out
     xh = x.clone().pin_memory()
     for _ in range(3):
         eng(xh)
