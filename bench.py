@@ -189,7 +189,6 @@ def run_reference(args, world, rank):
 # ----------------------------------------------------------------------------
 
 def run_ours(args, world, rank, local):
-    import numpy as np
     import torch
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import Engine, task_cost

@@ -126,7 +126,6 @@ struct sw_engine {
 namespace {
 struct NcclApi {
   typedef int (*GetUniqueId)(void* id);
-  typedef int (*CommInitRank)(void** comm, int nranks, const char id[128], int rank);
   typedef int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
   typedef int (*CommDestroy)(void*);
   typedef const char* (*ErrStr)(int);
@@ -140,7 +139,7 @@ struct NcclApi {
 NcclApi g_nccl;
 struct NcclId { char internal[128]; };
 typedef int (*CommInitRankV)(void** comm, int nranks, NcclId id, int rank);
-constexpr int kNcclFloat32 = 7, kNcclSum = 0, kNcclAvg = 4;
+constexpr int kNcclFloat32 = 7, kNcclAvg = 4;  // ncclFloat32, ncclAvg
 }  // namespace
 
 namespace {

@@ -36,7 +36,7 @@ from . import _native as N
 from .assign import StreamAssignment, SyncPlan, assign_streams_full
 from .errors import CudaError
 from .schedule import TaskSchedule, pre_run, schedule_arrays
-from .trace import ACT_NONE, Program, Task, View, build_program
+from .trace import Program, Task, View, build_program
 
 # kernel kinds / enums (csrc/runtime/ops.h)
 K_CONV, K_DWCONV, K_POOL, K_ELTWISE, K_GLOBAL_POOL, K_CONV_TC, K_CONCAT = 1, 2, 3, 4, 5, 6, 7

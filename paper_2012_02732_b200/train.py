@@ -56,7 +56,7 @@ from .engine import (EP_A, EP_B, EP_OUT, EW_A_SN, EW_ACT, EW_B_SN, EW_C, EW_H, E
 from .errors import CudaError
 from .graph import CompGraph, TaskNode
 from .schedule import pre_run, schedule_arrays
-from .trace import ACT_NONE, ACT_SIGMOID, trace_model, _drop_identities
+from .trace import ACT_NONE, trace_model, _drop_identities
 
 # csrc/runtime/ops.h training kinds
 (K_BN_STATS, K_BN_APPLY, K_BN_BWD_REDUCE, K_BN_BWD_APPLY, K_DW_DGRAD, K_DW_WGRAD, K_GEMM, K_XENT,
@@ -97,10 +97,6 @@ class Buf:
         if self.nchw:
             return (c * h * w, w, 1, h * w)
         return (h * w * c, w * c, c, 1)
-
-    @property
-    def key(self):
-        return self.parent.bid if self.parent is not None else self.bid
 
 
 @dataclass(eq=False)
@@ -377,14 +373,12 @@ def _flat_to_kernel(t):
 
 
 class _Builder:
-    def __init__(self, model: nn.Module, x_shape, num_classes: int, lr, momentum, weight_decay,
-                 allreduce: bool):
+    def __init__(self, model: nn.Module, x_shape, lr, momentum, weight_decay, allreduce: bool):
         self.model = model
         self.x_shape = tuple(x_shape)
         self.prog = TrainProgram()
         self.lr, self.momentum, self.wd = lr, momentum, weight_decay
         self.allreduce = allreduce
-        self.num_classes = num_classes
         self.val: dict[int, Buf] = {}        # INode id -> forward value buffer
         self.grad: dict[int, GradRef] = {}
         self.node_of: dict[int, object] = {}
@@ -925,7 +919,7 @@ def _numel_k(t) -> int:
 
 def build_train_program(model: nn.Module, x_shape, lr=0.05, momentum=0.9, weight_decay=4e-5,
                         allreduce=False) -> "_Builder":
-    b = _Builder(model, x_shape, 0, lr, momentum, weight_decay, allreduce)
+    b = _Builder(model, x_shape, lr, momentum, weight_decay, allreduce)
     b.build()
     return b
 

@@ -19,7 +19,6 @@ import os
 import socket
 
 import numpy as np
-import pytest
 import torch
 
 from oracle.numerics import cpu_train_steps

@@ -11,7 +11,6 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-import torch  # noqa: E402
 
 from paper_2012_02732_b200.networks import build_train_model, train_batch  # noqa: E402
 from paper_2012_02732_b200.train import TrainEngine  # noqa: E402
