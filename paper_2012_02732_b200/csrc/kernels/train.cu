@@ -207,6 +207,183 @@ __global__ void __launch_bounds__(kNT) bn_reduce_kernel(BnArgs a) {
   if (threadIdx.x == 0) *ticket = 0u;  // ready for the next replay
 }
 
+// Fused batch norm (MODE 0 forward: statistics + normalise; MODE 1 backward:
+// dgamma/dbeta + dx).  Phase 1 is bn_reduce_kernel's partial sums; then the
+// gx CTAs of a channel block meet at a barrier (atomic arrive counter, spin
+// bounded by a trap so a broken co-residency assumption fails loudly instead
+// of hanging), every CTA folds the gx partials of its 32 channels itself
+// (fixed order, fp64: no second barrier), CTA 0 of the block publishes the
+// statistics / parameter gradients, and phase 3 runs the elementwise pass on
+// the CTA's own rows while they are still in L2.  One launch instead of two
+// on the training step's critical chain.
+__device__ __forceinline__ void block_barrier(unsigned* arrive, unsigned expected) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(arrive, 1u);
+    unsigned spins = 0;
+    while (atomicAdd(arrive, 0u) < expected) {
+      if (++spins > (1u << 28)) __trap();
+      __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kNT) bn_fused_kernel(BnArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double red[2][kNT];
+  __shared__ float fin[4][32];  // mean / istd (fwd) or dgamma / dbeta (bwd) of the block's channels
+  const int C = (int)a.C;
+  constexpr int TC = 32, RL = kNT / TC;
+  const int lane_c = threadIdx.x % TC, lane_r = threadIdx.x / TC;
+  const int gx = gridDim.x;
+  const int64_t rows = (a.M + gx - 1) / gx;
+  const int64_t m0 = blockIdx.x * rows, m1 = min(a.M, m0 + rows);
+  const int c = blockIdx.y * TC + lane_c;
+  float mean = 0.f, istd = 0.f, g = 0.f, b = 0.f;
+  if (c < C) {
+    g = a.gamma[c];
+    b = a.gamma[C + c];
+    if (MODE == 1) {
+      mean = a.stats[c];
+      istd = a.stats[C + c];
+    }
+  }
+  // ---- phase 1: partial sums of this CTA's rows ----
+  float s0 = 0.f, s1 = 0.f;
+  if (c < C) {
+    for (int64_t mb = m0 + lane_r; mb < m1; mb += (int64_t)RL * kU) {
+      float v[kU], d[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t m = mb + (int64_t)u * RL;
+        v[u] = 0.f;
+        d[u] = 0.f;
+        if (m < m1) {
+          v[u] = a.y[m * a.ld + c];
+          if (MODE == 1) {
+            const int64_t n = m / a.HW, p = m - n * a.HW;
+            d[u] = a.dout[n * a.do_sn + p * a.do_sp + c];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (MODE == 0) {
+          s0 += v[u];
+          s1 += v[u] * v[u];
+        } else {
+          const float xh = (v[u] - mean) * istd;
+          const float dd = d[u] * a.do_scale;
+          const float dz = a.act == ACT_NONE ? dd : dd * act_grad(g * xh + b, a.act);
+          s0 += dz;
+          s1 += dz * xh;
+        }
+      }
+    }
+  }
+  red[0][threadIdx.x] = s0;
+  red[1][threadIdx.x] = s1;
+  __syncthreads();
+  if (lane_r == 0 && c < C) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int r = 0; r < RL; ++r) {
+      t0 += red[0][r * TC + lane_c];
+      t1 += red[1][r * TC + lane_c];
+    }
+    double* part = a.ws + (int64_t)blockIdx.x * 2 * C;
+    part[c] = t0;
+    part[C + c] = t1;
+  }
+  // ---- phase 2: barrier of the channel block, every CTA folds the partials ----
+  unsigned* arrive = reinterpret_cast<unsigned*>(a.ws + (int64_t)gx * 2 * C) + 2 * blockIdx.y;
+  unsigned* leave = arrive + 1;
+  block_barrier(arrive, (unsigned)gx);
+  double t0 = 0.0, t1 = 0.0;
+  if (c < C) {
+    const volatile double* pw = a.ws;
+#pragma unroll 4
+    for (int gi = lane_r; gi < gx; gi += RL) {
+      t0 += pw[(int64_t)gi * 2 * C + c];
+      t1 += pw[(int64_t)gi * 2 * C + C + c];
+    }
+  }
+  __syncthreads();
+  red[0][threadIdx.x] = t0;
+  red[1][threadIdx.x] = t1;
+  __syncthreads();
+  if (lane_r == 0) {
+    double u0 = 0.0, u1 = 0.0;
+    for (int r = 0; r < RL; ++r) {
+      u0 += red[0][r * TC + lane_c];
+      u1 += red[1][r * TC + lane_c];
+    }
+    if (MODE == 0) {
+      const double mu = u0 / (double)a.M;
+      double var = u1 / (double)a.M - mu * mu;
+      if (var < 0.0) var = 0.0;
+      fin[0][lane_c] = (float)mu;
+      fin[1][lane_c] = (float)(1.0 / sqrt(var + (double)a.eps));
+      if (blockIdx.x == 0 && c < C) {
+        a.stats[c] = fin[0][lane_c];
+        a.stats[C + c] = fin[1][lane_c];
+        if (a.running) {
+          const double unb = a.M > 1 ? var * (double)a.M / (double)(a.M - 1) : var;
+          a.running[c] = (float)((1.0 - a.momentum) * a.running[c] + a.momentum * mu);
+          a.running[C + c] = (float)((1.0 - a.momentum) * a.running[C + c] + a.momentum * unb);
+        }
+      }
+    } else {
+      fin[2][lane_c] = (float)u1;  // dgamma
+      fin[3][lane_c] = (float)u0;  // dbeta
+      if (blockIdx.x == 0 && c < C) {
+        a.dgamma[c] = (float)u1;
+        a.dgamma[C + c] = (float)u0;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase 3: elementwise over this CTA's rows ----
+  if (c < C) {
+    if (MODE == 0) {
+      mean = fin[0][lane_c];
+      istd = fin[1][lane_c];
+    }
+    const float invM = 1.f / (float)a.M;
+    const float dg = MODE == 1 ? fin[2][lane_c] * invM : 0.f, db = MODE == 1 ? fin[3][lane_c] * invM : 0.f;
+    for (int64_t m = m0 + lane_r; m < m1; m += RL) {
+      const float y = a.y[m * a.ld + c];
+      const float xh = (y - mean) * istd;
+      float o;
+      if (MODE == 0) {
+        o = g * xh + b;
+        if (a.has_res) o += a.res[m * a.ld + c];
+        o = apply_act(o, a.act);
+      } else {
+        const int64_t n = m / a.HW, p = m - n * a.HW;
+        const float d = a.dout[n * a.do_sn + p * a.do_sp + c] * a.do_scale;
+        const float dz = a.act == ACT_NONE ? d : d * act_grad(g * xh + b, a.act);
+        o = g * istd * (dz - db - xh * dg);
+        if (a.has_res) o += a.res[m * a.ld + c];
+      }
+      a.out[m * a.ld + c] = o;
+    }
+  }
+  // the last CTA of the block to leave resets both counters for the next replay
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(leave, 1u) == (unsigned)(gx - 1)) {
+      *arrive = 0u;
+      *leave = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // out = act(gamma * (y - mean) * invstd + beta (+ res))
 __global__ void __launch_bounds__(kNT) bn_apply_kernel(BnArgs a) {
   pdl_trigger();
@@ -767,6 +944,48 @@ int launch_train(const sw_op_desc& d, void* stream) {
         launch_k(bn_reduce_kernel<1>, dim3(a.grid, (unsigned)cdiv(a.C, chan_tile((int)a.C))), dim3(kNT), 0, st, 1, a);
       }
       break;
+    }
+    case K_BN_FWD:
+    case K_BN_BWD: {
+      BnArgs a = bn_args(d);
+      if (d.kind == K_BN_FWD) {
+        a.y = reinterpret_cast<const float*>(q[0]);
+        a.stats = reinterpret_cast<float*>(q[1]);
+        a.running = reinterpret_cast<float*>(q[2]);
+        a.gamma = reinterpret_cast<const float*>(q[3]);
+        a.res = reinterpret_cast<const float*>(q[4]);
+        a.out = reinterpret_cast<float*>(q[5]);
+      } else {
+        a.dout = reinterpret_cast<const float*>(q[0]);
+        a.y = reinterpret_cast<const float*>(q[1]);
+        a.stats = reinterpret_cast<float*>(q[2]);
+        a.gamma = reinterpret_cast<const float*>(q[3]);
+        a.dgamma = reinterpret_cast<float*>(q[4]);
+        a.res = reinterpret_cast<const float*>(q[5]);
+        a.out = reinterpret_cast<float*>(q[6]);
+      }
+      a.ws = reinterpret_cast<double*>(q[7]);
+      const dim3 grid(a.grid, (unsigned)cdiv(a.C, 32));
+      // every CTA of a channel block must be resident at the barrier: cooperative launch
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(kNT);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[2];
+      unsigned na = 0;
+      attr[na].id = cudaLaunchAttributeCooperative;
+      attr[na].val.cooperative = 1;
+      ++na;
+      if (g_launch_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+      }
+      cfg.attrs = attr;
+      cfg.numAttrs = na;
+      if (d.kind == K_BN_FWD)
+        return (int)cudaLaunchKernelEx(&cfg, bn_fused_kernel<0>, a);
+      return (int)cudaLaunchKernelEx(&cfg, bn_fused_kernel<1>, a);
     }
     case K_BN_APPLY: {
       BnArgs a = bn_args(d);

@@ -168,7 +168,9 @@ int launch_task(sw_engine* e, const sw_op_desc& op, cudaStream_t st) {
     case sw::K_SGD:
     case sw::K_EW_BWD:
     case sw::K_TRANSPOSE:
-    case sw::K_GEMM_REDUCE: rc = sw::launch_train(op, st); break;
+    case sw::K_GEMM_REDUCE:
+    case sw::K_BN_FWD:
+    case sw::K_BN_BWD: rc = sw::launch_train(op, st); break;
     case sw::K_ALLREDUCE: {
       if (!e->nccl_comm || !g_nccl.all_reduce) return sw::fail(SW_CUDA_ERROR, "allreduce task without an NCCL communicator");
       int r = g_nccl.all_reduce(reinterpret_cast<const void*>(op.ptrs[0]), reinterpret_cast<void*>(op.ptrs[0]),

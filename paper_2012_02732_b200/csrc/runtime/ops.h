@@ -36,6 +36,8 @@ enum KernelKind : int32_t {
   K_EW_BWD = 19,        // activation / broadcast-mul backward (EfficientNet SE)
   K_TRANSPOSE = 20,     // out[c][r] = in[r][c] (1x1 weights for the dgrad conv)
   K_GEMM_REDUCE = 21,   // fold K_GEMM split partials (+ bias, + res): wide splits
+  K_BN_FWD = 22,        // fused K_BN_STATS + K_BN_APPLY (per-channel-block barrier)
+  K_BN_BWD = 23,        // fused K_BN_BWD_REDUCE + K_BN_BWD_APPLY (per-channel-block barrier)
 };
 
 // Batch-norm kinds (K_BN_*): params index
@@ -57,6 +59,10 @@ enum BnParam : int {
 // APPLY ptrs: 0 y, 1 stats, 2 gamma [gamma C | beta C], 3 res, 4 out
 // BWD_REDUCE ptrs: 0 dOut, 1 y, 2 stats, 3 gamma|beta, 4 dgamma|dbeta, 7 ws
 // BWD_APPLY ptrs: 0 dOut, 1 y, 2 stats, 3 gamma|beta, 4 dgamma|dbeta, 5 res, 6 out
+// K_BN_FWD ptrs: 0 y, 1 stats, 2 running, 3 gamma|beta, 4 res, 5 out, 7 ws
+// K_BN_BWD ptrs: as BWD_APPLY + 7 ws.  The fused kinds keep all BN_GRID x
+// ceil(C/32) CTAs co-resident (cooperative launch) and meet at a barrier per
+// channel block between the reduction and the elementwise pass.
 
 // K_DW_DGRAD / K_DW_WGRAD reuse the SpatialParam geometry (SP_N..SP_PAD_W, the
 // forward op's dims: input N,H,W,C → output P,Q); dense NHWC.

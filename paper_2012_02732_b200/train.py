@@ -60,7 +60,7 @@ from .trace import ACT_NONE, trace_model, _drop_identities
 
 # csrc/runtime/ops.h training kinds
 (K_BN_STATS, K_BN_APPLY, K_BN_BWD_REDUCE, K_BN_BWD_APPLY, K_DW_DGRAD, K_DW_WGRAD, K_GEMM, K_XENT,
- K_SGD, K_ALLREDUCE, K_EW_BWD, K_TRANSPOSE, K_GEMM_REDUCE) = range(9, 22)
+ K_SGD, K_ALLREDUCE, K_EW_BWD, K_TRANSPOSE, K_GEMM_REDUCE, K_BN_FWD, K_BN_BWD) = range(9, 24)
 (BN_M, BN_C, BN_HW, BN_ACT, BN_HAS_RES, BN_EPS, BN_MOMENTUM, BN_GRID, BN_DO_SN, BN_DO_SP,
  BN_DO_SCALE, BN_LD) = range(12)
 (GM_M, GM_N, GM_K, GM_A_I, GM_A_R, GM_B_R, GM_B_J, GM_C_I, GM_SPLIT, GM_HAS_RES, GM_IM2COL,
@@ -341,6 +341,11 @@ def reduce_grid(m: int, c: int, rows_per_thread: int, cap: int) -> int:
     return max(1, min(gx, cap, max(1, 2 * NUM_SMS // gy)))
 
 
+def fused_ws_bytes(grid: int, c: int) -> int:
+    """Fused BN kinds: fp64 partials [grid][2][c] + (arrive, leave) counters per channel block."""
+    return 16 * grid * c + 8 * math.ceil(c / chan_tile(c)) + 16
+
+
 def reduce_ws_bytes(grid: int, c: int, elem_bytes: int, per_chan: int) -> int:
     """Partials [grid][per_chan][c] + one ticket per channel block."""
     return elem_bytes * grid * per_chan * c + 4 * math.ceil(c / chan_tile(c)) + 16
@@ -373,12 +378,14 @@ def _flat_to_kernel(t):
 
 
 class _Builder:
-    def __init__(self, model: nn.Module, x_shape, lr, momentum, weight_decay, allreduce: bool):
+    def __init__(self, model: nn.Module, x_shape, lr, momentum, weight_decay, allreduce: bool,
+                 fuse_bn: bool = True):
         self.model = model
         self.x_shape = tuple(x_shape)
         self.prog = TrainProgram()
         self.lr, self.momentum, self.wd = lr, momentum, weight_decay
         self.allreduce = allreduce
+        self.fuse_bn = fuse_bn
         self.val: dict[int, Buf] = {}        # INode id -> forward value buffer
         self.grad: dict[int, GradRef] = {}
         self.node_of: dict[int, object] = {}
@@ -541,6 +548,22 @@ class _Builder:
             act = op["act"]
             op.update(y=y, stats=stats, ws=ws, M=M, grid=grid, outb=out, c=c, hw=h * w)
 
+            if self.fuse_bn:
+                fws = P.buf(f"{bn.name}.fws", fused_ws_bytes(grid, c), zero=True)
+
+                def fill_fused(d, ptr):
+                    d.kind = K_BN_FWD
+                    for key, v in {BN_M: M, BN_C: c, BN_HW: h * w, BN_ACT: act, BN_HAS_RES: int(res is not None),
+                                   BN_EPS: fbits(eps), BN_MOMENTUM: fbits(mom), BN_GRID: grid, BN_LD: c}.items():
+                        d.params[key] = int(v)
+                    d.ptrs[0], d.ptrs[1], d.ptrs[2], d.ptrs[3] = ptr(y), ptr(stats), ptr(running), ptr(gb)
+                    d.ptrs[4] = ptr(res) if res is not None else 0
+                    d.ptrs[5], d.ptrs[7] = ptr(out), ptr(fws)
+                P.task("bn_fwd", bn.name, [y, gb] + ([res] if res is not None else []), [stats, running, out, fws],
+                       fill_fused, "fwd", nbytes=4.0 * M * c * (3 if res is not None else 2))
+                self.val[id(op["out"])] = out
+                return
+
             def fill_stats(d, ptr):
                 d.kind = K_BN_STATS
                 for key, v in {BN_M: M, BN_C: c, BN_HW: h * w, BN_EPS: fbits(eps),
@@ -693,6 +716,25 @@ class _Builder:
                 self._contribute_alias(op["res"], op["res"].shape, gout)
             bnp = {BN_M: M, BN_C: c, BN_HW: hw, BN_ACT: act, BN_GRID: grid, BN_DO_SN: gout.sn,
                    BN_DO_SP: gout.sp, BN_DO_SCALE: fbits(gout.scale), BN_LD: c}
+
+            src = bn.inputs[0]
+            if self.fuse_bn and self._needs_grad(src):
+                fws = P.buf(f"{bn.name}.bfws", fused_ws_bytes(grid, c), zero=True)
+
+                def emit_fused(out, res):
+                    def fill(d, ptr):
+                        d.kind = K_BN_BWD
+                        for key, v in bnp.items():
+                            d.params[key] = int(v)
+                        d.params[BN_HAS_RES] = int(res is not None)
+                        d.ptrs[0], d.ptrs[1], d.ptrs[2], d.ptrs[3], d.ptrs[4] = (
+                            ptr(gout.buf), ptr(y), ptr(stats), ptr(gb), ptr(gg))
+                        d.ptrs[5] = ptr(res) if res is not None else 0
+                        d.ptrs[6], d.ptrs[7] = ptr(out), ptr(fws)
+                    reads = [gout.buf, y, stats, gb] + ([res] if res is not None else [])
+                    P.task("bn_bwd", bn.name, reads, [gg, out, fws], fill, "bwd", nbytes=12.0 * M * c)
+                self._contribute(src, y.shape, emit_fused)
+                return
 
             def fill_red(d, ptr):
                 d.kind = K_BN_BWD_REDUCE
@@ -918,8 +960,8 @@ def _numel_k(t) -> int:
 
 
 def build_train_program(model: nn.Module, x_shape, lr=0.05, momentum=0.9, weight_decay=4e-5,
-                        allreduce=False) -> "_Builder":
-    b = _Builder(model, x_shape, lr, momentum, weight_decay, allreduce)
+                        allreduce=False, fuse_bn=True) -> "_Builder":
+    b = _Builder(model, x_shape, lr, momentum, weight_decay, allreduce, fuse_bn)
     b.build()
     return b
 
@@ -977,7 +1019,7 @@ class TrainEngine:
     def __init__(self, model: nn.Module, lr: float = 0.05, momentum: float = 0.9,
                  weight_decay: float = 4e-5, multi_stream: bool = True, device: int = 0,
                  world: int = 1, rank: int = 0, allreduce: bool | None = None, pdl: bool = False,
-                 autotune: bool = True):
+                 autotune: bool = True, fuse_bn: bool = True):
         self.model = model
         self.lr, self.momentum, self.wd = lr, momentum, weight_decay
         self.multi_stream = multi_stream
@@ -986,6 +1028,7 @@ class TrainEngine:
         self.allreduce = (world > 1) if allreduce is None else allreduce
         self.pdl = pdl
         self.autotune = autotune
+        self.fuse_bn = fuse_bn
         self.tuning = {}
         self._h = None
         self.prepared = False
@@ -1028,7 +1071,7 @@ class TrainEngine:
             raise CudaError("TrainEngine.prepare needs a CUDA device (there is no CPU fallback)")
         t0 = time.perf_counter()
         b = build_train_program(self.model, tuple(x.shape), self.lr, self.momentum, self.wd,
-                                self.allreduce)
+                                self.allreduce, self.fuse_bn)
         self.builder, self.prog = b, b.prog
         g = b.prog.graph
         t1 = time.perf_counter()

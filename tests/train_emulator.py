@@ -61,10 +61,29 @@ def _mat(mem, ptr, rows, cols, ld):
 _PARTIALS = {}
 
 
+def _clone_desc(d, kind, ptrs):
+    from paper_2012_02732_b200 import _native as N
+    e = N.OpDesc()
+    e.kind = kind
+    for i in range(len(d.params)):
+        e.params[i] = d.params[i]
+    for i, v in enumerate(ptrs):
+        e.ptrs[i] = v
+    return e
+
+
 def run_train_op(mem: HostMemory, d, allreduce=None):
     p = list(d.params)
     q = list(d.ptrs)
     k = d.kind
+    if k == T.K_BN_FWD:   # = K_BN_STATS then K_BN_APPLY
+        run_train_op(mem, _clone_desc(d, T.K_BN_STATS, [q[0], q[1], q[2], 0, 0, 0, 0, q[7]]))
+        run_train_op(mem, _clone_desc(d, T.K_BN_APPLY, [q[0], q[1], q[3], q[4], q[5], 0, 0, 0]))
+        return
+    if k == T.K_BN_BWD:   # = K_BN_BWD_REDUCE then K_BN_BWD_APPLY
+        run_train_op(mem, _clone_desc(d, T.K_BN_BWD_REDUCE, [q[0], q[1], q[2], q[3], q[4], 0, 0, q[7]]))
+        run_train_op(mem, _clone_desc(d, T.K_BN_BWD_APPLY, q[:7] + [0]))
+        return
     if k in (T.K_BN_STATS, T.K_BN_APPLY, T.K_BN_BWD_REDUCE, T.K_BN_BWD_APPLY):
         M, Cc, HW, act, has_res = p[T.BN_M], p[T.BN_C], p[T.BN_HW], p[T.BN_ACT], p[T.BN_HAS_RES]
         ld = p[T.BN_LD] or Cc
