@@ -355,22 +355,36 @@ __global__ void __launch_bounds__(kNT) bn_fused_kernel(BnArgs a) {
     }
     const float invM = 1.f / (float)a.M;
     const float dg = MODE == 1 ? fin[2][lane_c] * invM : 0.f, db = MODE == 1 ? fin[3][lane_c] * invM : 0.f;
-    for (int64_t m = m0 + lane_r; m < m1; m += RL) {
-      const float y = a.y[m * a.ld + c];
-      const float xh = (y - mean) * istd;
-      float o;
-      if (MODE == 0) {
-        o = g * xh + b;
-        if (a.has_res) o += a.res[m * a.ld + c];
-        o = apply_act(o, a.act);
-      } else {
-        const int64_t n = m / a.HW, p = m - n * a.HW;
-        const float d = a.dout[n * a.do_sn + p * a.do_sp + c] * a.do_scale;
-        const float dz = a.act == ACT_NONE ? d : d * act_grad(g * xh + b, a.act);
-        o = g * istd * (dz - db - xh * dg);
-        if (a.has_res) o += a.res[m * a.ld + c];
+    for (int64_t mb = m0 + lane_r; mb < m1; mb += (int64_t)RL * kU) {
+      float yv[kU], dv[kU], rv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {  // all loads of the kU rows in flight first
+        const int64_t m = mb + (int64_t)u * RL;
+        yv[u] = dv[u] = rv[u] = 0.f;
+        if (m < m1) {
+          yv[u] = a.y[m * a.ld + c];
+          if (a.has_res) rv[u] = a.res[m * a.ld + c];
+          if (MODE == 1) {
+            const int64_t n = m / a.HW, p = m - n * a.HW;
+            dv[u] = a.dout[n * a.do_sn + p * a.do_sp + c];
+          }
+        }
       }
-      a.out[m * a.ld + c] = o;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t m = mb + (int64_t)u * RL;
+        if (m >= m1) break;
+        const float xh = (yv[u] - mean) * istd;
+        float o;
+        if (MODE == 0) {
+          o = apply_act(g * xh + b + rv[u], a.act);
+        } else {
+          const float d = dv[u] * a.do_scale;
+          const float dz = a.act == ACT_NONE ? d : d * act_grad(g * xh + b, a.act);
+          o = g * istd * (dz - db - xh * dg) + rv[u];
+        }
+        a.out[m * a.ld + c] = o;
+      }
     }
   }
   // the last CTA of the block to leave resets both counters for the next replay
