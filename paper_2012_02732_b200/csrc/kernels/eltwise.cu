@@ -292,6 +292,40 @@ __global__ void __launch_bounds__(256) io_copy_kernel(const float4* __restrict__
   if (blockIdx.x == 0 && (int)threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
 }
 
+static void io_geometry(int64_t bytes, int64_t* n16, int* tail, unsigned* blocks) {
+  *n16 = bytes / 16;
+  *tail = (int)((bytes % 16) / 4);
+  int64_t b = cdiv(*n16, 256 * 4);
+  if (b < 1) b = 1;
+  if (b > 148 * 4) b = 148 * 4;
+  *blocks = (unsigned)b;
+}
+
+// Re-point a captured staging-copy node of an instantiated graph (same size,
+// other host buffer): a pinned caller buffer is then read / written in place,
+// with no host-side memcpy through the engine's staging buffer.
+int set_io_copy_node(void* exec, void* node, void* dst, const void* src, int64_t bytes) {
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return (int)cudaErrorMisalignedAddress;
+  int64_t n16;
+  int tail;
+  unsigned blocks;
+  io_geometry(bytes, &n16, &tail, &blocks);
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  const float* st = reinterpret_cast<const float*>(src) + n16 * 4;
+  float* dt = reinterpret_cast<float*>(dst) + n16 * 4;
+  void* args[] = {&s4, &d4, &n16, &st, &dt, &tail};
+  cudaKernelNodeParams kp = {};
+  kp.func = reinterpret_cast<void*>(io_copy_kernel);
+  kp.gridDim = dim3(blocks);
+  kp.blockDim = dim3(256);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  return (int)cudaGraphExecKernelNodeSetParams(reinterpret_cast<cudaGraphExec_t>(exec),
+                                               reinterpret_cast<cudaGraphNode_t>(node), &kp);
+}
+
 int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream) {
   if (bytes <= 0) return 0;
   if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return (int)cudaErrorMisalignedAddress;

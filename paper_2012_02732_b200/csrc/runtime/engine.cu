@@ -83,6 +83,8 @@ struct Slot {
   cudaGraphExec_t exec = nullptr;
   std::unordered_map<cudaGraphNode_t, int64_t> node_task;
   std::unordered_set<cudaGraphNode_t> io_nodes;  // kernel-node staging copies
+  cudaGraphNode_t io_in = nullptr, io_out = nullptr;  // the main input / output staging nodes
+  bool io_in_custom = false, io_out_custom = false;  // re-pointed at a caller buffer
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -90,6 +92,8 @@ struct Slot {
     graph = nullptr;
     node_task.clear();
     io_nodes.clear();
+    io_in = io_out = nullptr;
+    io_in_custom = io_out_custom = false;
   }
 };
 
@@ -346,6 +350,13 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   if (with_io && e->in_bytes > 0) {
     err = h2d(e->dev_in, e->host_in, e->in_bytes);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture H2D"));
+    if (kio) {
+      cudaStreamCaptureStatus cs;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      if (cudaStreamGetCaptureInfo(origin, &cs, nullptr, nullptr, &deps, &nd) == cudaSuccess && nd == 1)
+        sl.io_in = deps[0];
+    }
   }
   for (size_t i = 0; with_io && i < e->extra_host.size(); ++i) {
     err = h2d(e->extra_dev[i], e->extra_host[i], e->extra_bytes[i]);
@@ -396,7 +407,14 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
                                                reinterpret_cast<const void*>(e->dev_out), e->out_bytes, origin)
               : cudaMemcpyAsync(reinterpret_cast<void*>(e->host_out), reinterpret_cast<const void*>(e->dev_out),
                                 (size_t)e->out_bytes, cudaMemcpyDeviceToHost, origin);
-    if (kio && err == cudaSuccess) last_node(origin);
+    if (kio && err == cudaSuccess) {
+      last_node(origin);
+      cudaStreamCaptureStatus cs;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      if (cudaStreamGetCaptureInfo(origin, &cs, nullptr, nullptr, &deps, &nd) == cudaSuccess && nd == 1)
+        sl.io_out = deps[0];
+    }
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture D2H"));
   }
   CU(cudaStreamEndCapture(origin, &sl.graph));
@@ -405,14 +423,25 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   return SW_OK;
 }
 
+static int restore_io(sw_engine* e, Slot& sl) {
+  if (!sl.io_in_custom) return SW_OK;
+  int r = sw::set_io_copy_node(sl.exec, sl.io_in, reinterpret_cast<void*>(e->dev_in),
+                               reinterpret_cast<const void*>(e->host_in), e->in_bytes);
+  if (r) return cuda_fail((cudaError_t)r, "restore the input staging node");
+  sl.io_in_custom = false;
+  return SW_OK;
+}
+
 int sw_engine_replay(sw_engine* e, int32_t slot) {
   if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  if (int r = restore_io(e, e->slots[slot])) return r;
   CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
   return SW_OK;
 }
 
 int sw_engine_replay_sync(sw_engine* e, int32_t slot, int64_t* out_launch_ns) {
   if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  if (int r = restore_io(e, e->slots[slot])) return r;
   auto a = std::chrono::steady_clock::now();
   CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
   auto b = std::chrono::steady_clock::now();
@@ -421,10 +450,36 @@ int sw_engine_replay_sync(sw_engine* e, int32_t slot, int64_t* out_launch_ns) {
   return SW_OK;
 }
 
+static bool pinned16(const void* p) {
+  if (!p || (reinterpret_cast<uint64_t>(p) & 15)) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_out) {
   if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
-  if (host_in && reinterpret_cast<uint64_t>(host_in) != e->host_in)
-    std::memcpy(reinterpret_cast<void*>(e->host_in), host_in, (size_t)e->in_bytes);
+  Slot& sl = e->slots[slot];
+  // a pinned caller input is read in place by the captured staging kernel
+  // (its node re-pointed), a pageable one goes through the pinned staging buffer
+  const bool in_direct = sl.io_in && host_in && pinned16(host_in);
+  if (in_direct && reinterpret_cast<uint64_t>(host_in) != e->host_in) {
+    int r = sw::set_io_copy_node(sl.exec, sl.io_in, reinterpret_cast<void*>(e->dev_in), host_in, e->in_bytes);
+    if (r) return cuda_fail((cudaError_t)r, "re-point the input staging node");
+    sl.io_in_custom = true;
+  } else {
+    if (sl.io_in_custom) {
+      int r = sw::set_io_copy_node(sl.exec, sl.io_in, reinterpret_cast<void*>(e->dev_in),
+                                   reinterpret_cast<const void*>(e->host_in), e->in_bytes);
+      if (r) return cuda_fail((cudaError_t)r, "restore the input staging node");
+      sl.io_in_custom = false;
+    }
+    if (host_in && reinterpret_cast<uint64_t>(host_in) != e->host_in)
+      std::memcpy(reinterpret_cast<void*>(e->host_in), host_in, (size_t)e->in_bytes);
+  }
   CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
   // spin on the stream instead of a blocking synchronize: the wake-up of a
   // yielding wait costs ~15 µs per call (tools/ab_edges.py, cell: 46 µs e2e
@@ -440,6 +495,7 @@ int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_
 
 int sw_engine_time_replay(sw_engine* e, int32_t slot, int32_t iters, double* out_gpu_us, double* out_host_us) {
   if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  if (int r = restore_io(e, e->slots[slot])) return r;
   if (iters < 1) iters = 1;
   CU(cudaStreamSynchronize(e->launch));
   double host_ns = 0;
