@@ -190,6 +190,7 @@ int launch_task(sw_engine* e, const sw_op_desc& op, cudaStream_t st) {
     case sw::K_GLOBAL_POOL: rc = sw::launch_global_pool(op, st); break;
     case sw::K_CONCAT: rc = sw::launch_concat(op, st); break;
     case sw::K_SEPCONV: rc = sw::launch_sepconv(op, st); break;
+    case sw::K_SEP2: rc = sw::launch_sep2(op, st); break;
     default: return sw::fail(SW_VALUE_ERROR, "unknown kernel kind " + std::to_string(op.kind));
   }
   if (rc != 0) return cuda_fail((cudaError_t)rc, "kernel launch");
@@ -234,6 +235,7 @@ int sw_engine_create(int32_t device, sw_engine** out) {
   sw::init_simt_kernels();
   sw::init_pw_kernels();
   sw::init_sep_kernels();
+  sw::init_sep2_kernels();
   CU(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   CU(cudaEventCreate(&e->t0));
   CU(cudaEventCreate(&e->t1));

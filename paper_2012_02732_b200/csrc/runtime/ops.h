@@ -38,7 +38,30 @@ enum KernelKind : int32_t {
   K_GEMM_REDUCE = 21,   // fold K_GEMM split partials (+ bias, + res): wide splits
   K_BN_FWD = 22,        // fused K_BN_STATS + K_BN_APPLY (per-channel-block barrier)
   K_BN_BWD = 23,        // fused K_BN_BWD_REDUCE + K_BN_BWD_APPLY (per-channel-block barrier)
+  K_SEP2 = 24,          // NASNet separable block: two chained sepconvs in one cluster kernel
 };
+
+// K_SEP2 extra params (after the SpatialParam block; spatial params describe
+// the FIRST sepconv's input / stride / pad, SP_P/SP_Q the map both stages
+// share, SP_K the final channels, SP_ACT / residual the second pointwise's
+// epilogue, SP_PRE_RELU the first depthwise's input ReLU, SP_SPLIT_K the
+// cluster size = row bands per image)
+enum Sep2Param : int {
+  S2_MID = 35,      // channels between the two sepconvs
+  S2_ACT1,          // activation after the first pointwise (+ folded BN)
+  S2_DW_ACT1,       // activation after the first depthwise
+  S2_DW_ACT2,       // activation after the second depthwise
+  S2_PRE_RELU2,     // ReLU on load of the intermediate
+  S2_OFF_DW1,       // offsets (floats) into the packed weights (PT_W):
+  S2_OFF_PW1,       //   dw1 [k][k][C], pw1 [C][MID], b1 [MID], db1 [C] (or -1),
+  S2_OFF_B1,        //   dw2 [k][k][MID], pw2 [MID][K], b2 [K], db2 [MID] (or -1)
+  S2_OFF_DB1,
+  S2_OFF_DW2,
+  S2_OFF_PW2,
+  S2_OFF_B2,
+  S2_OFF_DB2,
+};
+// K_SEP2 ptrs: PT_IN, PT_OUT, PT_W (packed weights), PT_RES
 
 // Batch-norm kinds (K_BN_*): params index
 enum BnParam : int {
@@ -165,5 +188,7 @@ void init_pw_kernels();
 int launch_sepconv(const sw_op_desc& op, void* stream);
 void init_sep_kernels();
 int launch_train(const sw_op_desc& op, void* stream);  // K_BN_* .. K_SGD, K_EW_BWD
+int launch_sep2(const sw_op_desc& op, void* stream);   // K_SEP2 (sep2.cu)
+void init_sep2_kernels();
 
 }  // namespace sw

@@ -48,6 +48,9 @@ EW_ADD, EW_MUL, EW_AFFINE, EW_COPY = 0, 1, 2, 3
 PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS, PT_W_TC_HI, PT_W_TC_LO = range(8)
 PT_DW_BIAS = 6  # K_SEPCONV
 K_SEPCONV = 8
+K_SEP2 = 24  # fused NASNet separable block (csrc/kernels/sep2.cu)
+(S2_MID, S2_ACT1, S2_DW_ACT1, S2_DW_ACT2, S2_PRE_RELU2, S2_OFF_DW1, S2_OFF_PW1, S2_OFF_B1, S2_OFF_DB1,
+ S2_OFF_DW2, S2_OFF_PW2, S2_OFF_B2, S2_OFF_DB2) = range(35, 48)
 TC_BK = 32  # K tile of the tcgen05 conv; its pre-split weights are padded to a multiple
 (EW_N, EW_H, EW_W, EW_C, EW_OP, EW_ACT, EW_A_SN, EW_A_SH, EW_A_SW, EW_A_SC, EW_B_SN, EW_B_SH,
  EW_B_SW, EW_B_SC, EW_C_SN, EW_C_SH, EW_C_SW, EW_C_SC, EW_O_SN, EW_O_SH, EW_O_SW, EW_O_SC,
@@ -95,6 +98,13 @@ PW_TILES = {16: (8, 32), 17: (16, 32), 18: (32, 32), 19: (16, 64), 20: (32, 64),
 # csrc/kernels/conv.cu kSimt[]: variant → (BM, BN); every variant runs 256 threads
 SIMT_TILES = {0: (64, 64), 1: (32, 64), 2: (32, 32), 3: (128, 64), 4: (16, 32), 5: (16, 64),
               6: (16, 16), 7: (64, 32)}
+
+
+def sep2_cluster(P: int, rows: int = 0) -> int:
+    """Cluster size (row bands per image) of the fused separable block: about
+    one band per row, at most 16 CTAs (csrc/kernels/sep2.cu)."""
+    rows = rows or max(1, math.ceil(P / 16))
+    return max(1, math.ceil(P / rows))
 
 
 def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
@@ -211,6 +221,26 @@ def _pack_weights(prog: Program):
             arrays[(t.tid, "dw")] = dw.numpy().reshape(-1)
             if n.attrs["dw_bias"] is not None:
                 arrays[(t.tid, "dwb")] = n.attrs["dw_bias"].float().numpy().reshape(-1)
+        elif t.kind == "sep2":
+            a = n.attrs
+            parts = {"dw1": a["dw1"].float()[:, 0].permute(1, 2, 0).contiguous().numpy().reshape(-1),
+                     "pw1": a["pw1"].float().reshape(a["pw1"].shape[0], -1).t().contiguous().numpy().reshape(-1),
+                     "b1": (a["b1"].float() if a["b1"] is not None else torch.zeros(a["mid"])).numpy(),
+                     "dw2": a["dw2"].float()[:, 0].permute(1, 2, 0).contiguous().numpy().reshape(-1),
+                     "pw2": a["pw2"].float().reshape(a["pw2"].shape[0], -1).t().contiguous().numpy().reshape(-1),
+                     "b2": (a["b2"].float() if a["b2"] is not None else
+                            torch.zeros(a["pw2"].shape[0])).numpy()}
+            if a["db1"] is not None:
+                parts["db1"] = a["db1"].float().numpy()
+            if a["db2"] is not None:
+                parts["db2"] = a["db2"].float().numpy()
+            offs, chunks, off = {}, [], 0
+            for key, arr in parts.items():
+                offs[key] = off
+                chunks.append(arr.reshape(-1))
+                off += arr.size
+            t.attrs["sep2_offsets"] = offs
+            arrays[(t.tid, "pack")] = np.concatenate(chunks).astype(np.float32)
         elif t.kind == "affine":
             arrays[(t.tid, "scale")] = n.attrs["scale"].float().numpy().reshape(-1)
             arrays[(t.tid, "shift")] = n.attrs["shift"].float().numpy().reshape(-1)
@@ -226,7 +256,7 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
         p = d.params
         q = d.ptrs
         wptr = lambda key: weight_base + weight_offsets[(t.tid, key)] if (t.tid, key) in weight_offsets else 0  # noqa: E731
-        if t.kind in ("conv", "dwconv", "pool", "sepconv"):
+        if t.kind in ("conv", "dwconv", "pool", "sepconv", "sep2"):
             n = t.node
             x = t.inputs[0]
             st_in = x.st
@@ -263,6 +293,17 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 d.kind = K_DWCONV
                 q[PT_W] = wptr("w")
                 q[PT_BIAS] = wptr("b")
+            elif t.kind == "sep2":
+                d.kind = K_SEP2
+                q[PT_W] = wptr("pack")
+                a2 = n.attrs
+                offs = t.attrs["sep2_offsets"]
+                vals.update({S2_MID: a2["mid"], S2_ACT1: a2["act1"], S2_DW_ACT1: a2["dw_act1"],
+                             S2_DW_ACT2: a2["dw_act2"], S2_PRE_RELU2: int(a2["pre_relu2"]),
+                             S2_OFF_DW1: offs["dw1"], S2_OFF_PW1: offs["pw1"], S2_OFF_B1: offs["b1"],
+                             S2_OFF_DB1: offs.get("db1", -1), S2_OFF_DW2: offs["dw2"], S2_OFF_PW2: offs["pw2"],
+                             S2_OFF_B2: offs["b2"], S2_OFF_DB2: offs.get("db2", -1),
+                             SP_SPLIT_K: sep2_cluster(P)})
             elif t.kind == "sepconv":
                 d.kind = K_SEPCONV
                 q[PT_W] = wptr("w")
@@ -374,6 +415,13 @@ def task_cost(t: Task) -> tuple[float, float]:
         pix = o.st.n * o.st.h * o.st.w
         flops = 2.0 * pix * c * R * S + 2.0 * pix * c * o.c
         wbytes = (c * R * S + c + o.c * c + o.c) * 4
+    elif t.kind == "sep2":
+        R, S = t.node.attrs["k"]
+        c = t.inputs[0].c
+        mid = t.node.attrs["mid"]
+        pix = o.st.n * o.st.h * o.st.w
+        flops = 2.0 * pix * (c * R * S + c * mid + mid * R * S + mid * o.c)
+        wbytes = (c * R * S + c * mid + mid + mid * R * S + mid * o.c + o.c) * 4
     elif t.kind == "pool":
         R, S = t.node.attrs["k"]
         flops = 1.0 * out_elems * R * S
@@ -396,7 +444,8 @@ class Engine:
 
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
-                 tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb"):
+                 tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb",
+                 fuse_sep_pairs: bool = False):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -411,6 +460,7 @@ class Engine:
         if arena not in ("hb", "reference"):
             raise ValueError(f"arena must be 'hb' or 'reference', not {arena!r}")
         self.arena_mode = arena
+        self.fuse_sep_pairs = fuse_sep_pairs
         self.tuning = {}
         self.tuning_log = {}
         self._h = None
@@ -423,7 +473,7 @@ class Engine:
             raise CudaError("Engine.prepare needs a CUDA device (there is no CPU fallback)")
         t0 = time.perf_counter()
         ex = example.detach().float().cpu().contiguous()
-        prog = build_program(self.model, ex, fuse=self.fuse)
+        prog = build_program(self.model, ex, fuse=self.fuse, fuse_sep_pairs=self.fuse_sep_pairs)
         t1 = time.perf_counter()
         g = prog.graph
         f, plan, meg = assign_streams_full(g)
@@ -562,7 +612,7 @@ class Engine:
         lib = N.lib()
         us = C.c_double()
         for t in self.program.tasks:
-            if t.kind not in ("conv", "sepconv"):
+            if t.kind not in ("conv", "sepconv", "sep2"):
                 continue
             d = self.ops[t.tid]
             p = d.params
@@ -572,7 +622,10 @@ class Engine:
             best = None
             trial = N.OpDesc()
             C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
-            if t.kind == "sepconv":
+            if t.kind == "sep2":
+                P = p[SP_P]
+                cands = sorted({(K_SEP2, 0, sep2_cluster(P, r)) for r in (1, 2, 3, 4, 7) if r <= P})
+            elif t.kind == "sepconv":
                 cands = [(K_SEPCONV, v, 1) for v in SEP_TILES]
                 # TMA kernel with the depthwise split over a cluster of the column blocks
                 cands += [(K_SEPCONV, v, 2) for v, (bm, bn) in SEP_TILES.items()

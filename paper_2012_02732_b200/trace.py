@@ -447,7 +447,38 @@ def _fuse_separable(nodes):
     return [n for n in nodes if id(n) not in drop]
 
 
-def optimize(nodes: list[INode], fuse_separable: bool = True) -> list[INode]:
+def _fuse_sep_pairs(nodes):
+    """sepconv → sepconv (NASNet's BranchSep: the second one stride 1, same k,
+    'same' padding, sole consumer of the first) becomes ONE 'sep2' task
+    (csrc/kernels/sep2.cu): one graph node instead of two on the cell's
+    critical path, the intermediate map kept on chip."""
+    users = _users(nodes)
+    drop = set()
+    for n in nodes:
+        if n.kind != "sepconv":
+            continue
+        d = n.inputs[0]
+        if d.kind != "sepconv" or id(d) in drop or len(users[id(d)]) != 1 or d.residual is not None:
+            continue
+        k = tuple(n.attrs["k"])
+        if k[0] != k[1] or tuple(d.attrs["k"]) != k or k[0] not in (3, 5, 7):
+            continue
+        if tuple(n.attrs["stride"]) != (1, 1) or tuple(n.attrs["pad"]) != (k[0] // 2, k[0] // 2):
+            continue
+        n.attrs = {"k": k, "stride": d.attrs["stride"], "pad": d.attrs["pad"],
+                   "dw1": d.attrs["dw_weight"], "db1": d.attrs["dw_bias"], "dw_act1": d.attrs["dw_act"],
+                   "pw1": d.attrs["weight"], "b1": d.attrs["bias"], "act1": d.act,
+                   "pre_relu2": n.pre_relu,
+                   "dw2": n.attrs["dw_weight"], "db2": n.attrs["dw_bias"], "dw_act2": n.attrs["dw_act"],
+                   "pw2": n.attrs["weight"], "b2": n.attrs["bias"], "mid": d.shape[1]}
+        n.kind = "sep2"
+        n.pre_relu = d.pre_relu
+        n.inputs = [d.inputs[0]]
+        drop.add(id(d))
+    return [n for n in nodes if id(n) not in drop]
+
+
+def optimize(nodes: list[INode], fuse_separable: bool = True, fuse_sep_pairs: bool = False) -> list[INode]:
     out_node = nodes[-1]
     nodes = _drop_identities(nodes)
     nodes = _fold_bn(nodes)
@@ -456,6 +487,8 @@ def optimize(nodes: list[INode], fuse_separable: bool = True) -> list[INode]:
     nodes = _pre_relu(nodes)
     if fuse_separable:
         nodes = _fuse_separable(nodes)
+        if fuse_sep_pairs:
+            nodes = _fuse_sep_pairs(nodes)
     return nodes
 
 
@@ -668,10 +701,10 @@ def to_compgraph(prog: Program, durations=None) -> CompGraph:
 
 
 def build_program(model: nn.Module, example: torch.Tensor, fuse: bool = True,
-                  fuse_separable: bool = True) -> Program:
+                  fuse_separable: bool = True, fuse_sep_pairs: bool = False) -> Program:
     nodes = trace_model(model, example)
     if fuse:
-        nodes = optimize(nodes, fuse_separable=fuse_separable)
+        nodes = optimize(nodes, fuse_separable=fuse_separable, fuse_sep_pairs=fuse_sep_pairs)
     else:
         nodes = _drop_identities(nodes)
         for n in nodes:

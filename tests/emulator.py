@@ -81,9 +81,50 @@ def _window(x, ph, pw, P, Q, R, S, sh, sw, fill):
     return out, valid
 
 
+def _sep2(mem, d, p, q):
+    """K_SEP2 = two chained sepconvs (csrc/kernels/sep2.cu)."""
+    Nb, H, W, Cc, P, Q, K, R = (p[E.SP_N], p[E.SP_H], p[E.SP_W], p[E.SP_C], p[E.SP_P], p[E.SP_Q],
+                                p[E.SP_K], p[E.SP_R])
+    mid = p[E.S2_MID]
+    base = mem.idx(q[E.PT_W])
+
+    def arr(off, n):
+        return torch.from_numpy(mem.buf[base + off:base + off + n].copy()).double()
+    x = mem.gather(q[E.PT_IN], (Nb, Cc, H, W), (p[E.SP_IN_SN], p[E.SP_IN_SH], p[E.SP_IN_SW], p[E.SP_IN_SC]))
+    if p[E.SP_PRE_RELU]:
+        x = F.relu(x)
+    sh, sw, ph, pw = p[E.SP_STRIDE_H], p[E.SP_STRIDE_W], p[E.SP_PAD_H], p[E.SP_PAD_W]
+    w1 = arr(p[E.S2_OFF_DW1], R * R * Cc).view(R, R, Cc).permute(2, 0, 1)[:, None]
+    xw, _ = _window(x, ph, pw, P, Q, R, R, sh, sw, 0.0)
+    y = F.conv2d(xw.double(), w1, stride=(sh, sw), groups=Cc)
+    if p[E.S2_OFF_DB1] >= 0:
+        y = y + arr(p[E.S2_OFF_DB1], Cc).view(1, -1, 1, 1)
+    y = _act(y.float(), p[E.S2_DW_ACT1]).double()
+    pw1 = arr(p[E.S2_OFF_PW1], Cc * mid).view(Cc, mid).t()
+    y = F.conv2d(y, pw1[:, :, None, None]) + arr(p[E.S2_OFF_B1], mid).view(1, -1, 1, 1)
+    y = _act(y.float(), p[E.S2_ACT1])
+    if p[E.S2_PRE_RELU2]:
+        y = F.relu(y)
+    w2 = arr(p[E.S2_OFF_DW2], R * R * mid).view(R, R, mid).permute(2, 0, 1)[:, None]
+    y = F.conv2d(y.double(), w2, padding=R // 2, groups=mid)
+    if p[E.S2_OFF_DB2] >= 0:
+        y = y + arr(p[E.S2_OFF_DB2], mid).view(1, -1, 1, 1)
+    y = _act(y.float(), p[E.S2_DW_ACT2]).double()
+    pw2 = arr(p[E.S2_OFF_PW2], mid * K).view(mid, K).t()
+    y = (F.conv2d(y, pw2[:, :, None, None]) + arr(p[E.S2_OFF_B2], K).view(1, -1, 1, 1)).float()
+    if p[E.SP_HAS_RES]:
+        y = y + mem.gather(q[E.PT_RES], (Nb, K, P, Q),
+                           (p[E.SP_RES_SN], p[E.SP_RES_SH], p[E.SP_RES_SW], p[E.SP_RES_SC] or 1))
+    y = _act(y, p[E.SP_ACT])
+    mem.scatter(q[E.PT_OUT], y, (p[E.SP_OUT_SN], p[E.SP_OUT_SH], p[E.SP_OUT_SW], p[E.SP_OUT_SC] or 1))
+
+
 def run_op(mem: HostMemory, d):
     p = list(d.params)
     q = list(d.ptrs)
+    if d.kind == E.K_SEP2:
+        _sep2(mem, d, p, q)
+        return
     if d.kind in (E.K_CONV, E.K_DWCONV, E.K_POOL, E.K_SEPCONV):
         Nb, H, W, Cc, P, Q, K, R, S = (p[E.SP_N], p[E.SP_H], p[E.SP_W], p[E.SP_C], p[E.SP_P],
                                        p[E.SP_Q], p[E.SP_K], p[E.SP_R], p[E.SP_S])
@@ -188,11 +229,11 @@ def run_op(mem: HostMemory, d):
         raise NotImplementedError(d.kind)
 
 
-def emulate(model, x, fuse=True, multi_stream=True, hb_arena=False):
+def emulate(model, x, fuse=True, multi_stream=True, hb_arena=False, fuse_sep_pairs=False):
     """Run the lowered program on the host; returns (output, program, ops).
     hb_arena=True places the activations with the engine's happens-before
     arena (arena.py): storages share memory wherever the capture orders them."""
-    prog = build_program(model, x, fuse=fuse)
+    prog = build_program(model, x, fuse=fuse, fuse_sep_pairs=fuse_sep_pairs)
     g = prog.graph
     total = sum(st.alloc_bytes for st in prog.storages)
     arrays = E._pack_weights(prog)
