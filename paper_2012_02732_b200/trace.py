@@ -447,7 +447,7 @@ def _fuse_separable(nodes):
     return [n for n in nodes if id(n) not in drop]
 
 
-def _fuse_sep_pairs(nodes):
+def _fuse_sep_pairs(nodes, max_hw: int = 196):
     """sepconv → sepconv (NASNet's BranchSep: the second one stride 1, same k,
     'same' padding, sole consumer of the first) becomes ONE 'sep2' task
     (csrc/kernels/sep2.cu): one graph node instead of two on the cell's
@@ -465,6 +465,8 @@ def _fuse_sep_pairs(nodes):
             continue
         if tuple(n.attrs["stride"]) != (1, 1) or tuple(n.attrs["pad"]) != (k[0] // 2, k[0] // 2):
             continue
+        if n.shape[2] * n.shape[3] > max_hw:
+            continue  # one cluster per image: only small maps keep enough CTAs busy
         n.attrs = {"k": k, "stride": d.attrs["stride"], "pad": d.attrs["pad"],
                    "dw1": d.attrs["dw_weight"], "db1": d.attrs["dw_bias"], "dw_act1": d.attrs["dw_act"],
                    "pw1": d.attrs["weight"], "b1": d.attrs["bias"], "act1": d.act,
@@ -478,7 +480,7 @@ def _fuse_sep_pairs(nodes):
     return [n for n in nodes if id(n) not in drop]
 
 
-def optimize(nodes: list[INode], fuse_separable: bool = True, fuse_sep_pairs: bool = False) -> list[INode]:
+def optimize(nodes: list[INode], fuse_separable: bool = True, fuse_sep_pairs=False) -> list[INode]:
     out_node = nodes[-1]
     nodes = _drop_identities(nodes)
     nodes = _fold_bn(nodes)
@@ -488,7 +490,7 @@ def optimize(nodes: list[INode], fuse_separable: bool = True, fuse_sep_pairs: bo
     if fuse_separable:
         nodes = _fuse_separable(nodes)
         if fuse_sep_pairs:
-            nodes = _fuse_sep_pairs(nodes)
+            nodes = _fuse_sep_pairs(nodes, 196 if fuse_sep_pairs is True else int(fuse_sep_pairs))
     return nodes
 
 

@@ -25,7 +25,7 @@ def main():
     model, shape = build_model(a.config)
     x = example_input(shape, batch=a.batch)
     ref = cpu_forward(model, x) if a.batch <= 8 else None
-    for fused in (False, True):
+    for fused in (False, 49, 196, 784):
         eng = Engine(model, fuse_sep_pairs=fused).prepare(x)
         y = eng(x)
         err = (y - ref).abs().max().item() if ref is not None else float("nan")
