@@ -100,3 +100,17 @@ def test_batch_gt_one_program(programs):
         ref = model(xb)
     y, prog, _ = emulate(model, xb, fuse=True)
     torch.testing.assert_close(y, ref, rtol=1e-4, atol=1e-5)
+
+
+def test_fused_separable_blocks_emulated(programs):
+    """Experimental sep2 pass (opt-in): every NASNet BranchSep becomes one task
+    and the emulated lowered program still equals the CPU forward."""
+    from emulator import emulate
+    from oracle.numerics import cpu_forward
+    from paper_2012_02732_b200.networks import build_model, example_input
+    model, shape = build_model("nasnet_mobile")
+    x = example_input(shape)
+    y, prog, _ = emulate(model, x, fuse_sep_pairs=784)
+    assert prog.stats().get("sep2", 0) == 75 and "sepconv" in prog.stats()
+    ref = cpu_forward(model, x)
+    torch.testing.assert_close(y, ref, rtol=1e-3, atol=1e-4)

@@ -540,3 +540,14 @@ def test_engine_call_pinned_and_pageable_inputs_agree():
     assert not torch.equal(y2, y_pin)
     assert torch.equal(eng(x2.clone()), y2)
     eng.close()
+
+
+def test_fused_separable_block_kernel_parity():
+    """K_SEP2 (experimental, opt-in) on the GPU: NASNet with every separable
+    block on maps <= 28x28 fused, against the fp32 CPU forward."""
+    model, shape = build_model("nasnet_mobile")
+    x = example_input(shape)
+    eng, y, ref = run(model, x, fuse_sep_pairs=784)
+    assert eng.program.stats().get("sep2", 0) > 0
+    close(y, ref)
+    eng.close()
