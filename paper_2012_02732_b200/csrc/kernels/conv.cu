@@ -270,7 +270,7 @@ constexpr int kNumSimt = sizeof(kSimt) / sizeof(kSimt[0]);
 // accumulators in registers, the filter sits in shared memory as [rsc][K]
 // (warp-uniform broadcast reads), and each pixel's outputs leave as one
 // contiguous run (float4 when the layout allows).
-template <int KB>
+template <int KB, int KS>
 __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   extern __shared__ float wsm[];  // [Kdim][KB] + bias[KB]
   const int tid = threadIdx.x;
@@ -294,36 +294,74 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   const int ih0 = p * a.sh - a.ph, iw0 = q * a.sw - a.pw;
   const float* base = a.in + nb * a.in_sn;
   const bool cvec = a.in_sc == 1 && (a.C & 3) == 0;
+  if constexpr (KS > 0) {
+    // fixed k x k window, channel by channel: the KS*KS tap loads of a channel
+    // are issued together from clamped addresses and masked (branch-free),
+    // so a thread waits one memory round trip per channel, not per tap
 #pragma unroll 1
-  for (int r = 0; r < a.R; ++r) {
-    const int ih = ih0 + r;
-    if ((unsigned)ih >= (unsigned)a.H) continue;
-#pragma unroll 1
-    for (int s = 0; s < a.S; ++s) {
-      const int iw = iw0 + s;
-      if ((unsigned)iw >= (unsigned)a.W) continue;
-      const float* src = base + ih * a.in_sh + iw * a.in_sw;
-      const float* wr = wsm + ((r * a.S + s) * a.C) * KB;
-      if (cvec) {
-#pragma unroll 1
-        for (int c = 0; c < a.C; c += 4) {
-          float4 x = __ldg(reinterpret_cast<const float4*>(src + c));
-          if (a.pre_relu) {
-            x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
-          }
-          const float* w0 = wr + c * KB;
+    for (int c = 0; c < a.C; ++c) {
+      float x[KS * KS];
 #pragma unroll
-          for (int k = 0; k < KB; ++k)
-            acc[k] = fmaf(x.x, w0[k], fmaf(x.y, w0[KB + k], fmaf(x.z, w0[2 * KB + k], fmaf(x.w, w0[3 * KB + k], acc[k]))));
+      for (int r = 0; r < KS; ++r)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const int ih = ih0 + r, iw = iw0 + s;
+          const bool ok = (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
+          const float v = __ldg(base + (ok ? ih * a.in_sh + iw * a.in_sw : 0) + c * a.in_sc);
+          x[r * KS + s] = ok ? (a.pre_relu ? fmaxf(v, 0.f) : v) : 0.f;
         }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < a.C; ++c) {
-          float x = __ldg(src + c * a.in_sc);
-          if (a.pre_relu) x = fmaxf(x, 0.f);
-          const float* w0 = wr + c * KB;
 #pragma unroll
-          for (int k = 0; k < KB; ++k) acc[k] = fmaf(x, w0[k], acc[k]);
+      for (int r = 0; r < KS; ++r)
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          const float* w0 = wsm + ((r * KS + s) * a.C + c) * KB;
+#pragma unroll
+          for (int k = 0; k < KB; ++k) acc[k] = fmaf(x[r * KS + s], w0[k], acc[k]);
+        }
+    }
+  } else {
+#pragma unroll 1
+    for (int r = 0; r < a.R; ++r) {
+      const int ih = ih0 + r;
+      if ((unsigned)ih >= (unsigned)a.H) continue;
+#pragma unroll 1
+      for (int s = 0; s < a.S; ++s) {
+        const int iw = iw0 + s;
+        if ((unsigned)iw >= (unsigned)a.W) continue;
+        const float* src = base + ih * a.in_sh + iw * a.in_sw;
+        const float* wr = wsm + ((r * a.S + s) * a.C) * KB;
+        if (cvec) {
+          // 16 channels of loads in flight per step
+#pragma unroll 1
+          for (int c0 = 0; c0 < a.C; c0 += 16) {
+            float4 xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              xv[u] = c0 + 4 * u < a.C ? __ldg(reinterpret_cast<const float4*>(src + c0 + 4 * u))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int c = c0 + 4 * u;
+              if (c >= a.C) break;
+              float4 x = xv[u];
+              if (a.pre_relu) {
+                x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+              }
+              const float* w0 = wr + c * KB;
+#pragma unroll
+              for (int k = 0; k < KB; ++k)
+                acc[k] = fmaf(x.x, w0[k], fmaf(x.y, w0[KB + k], fmaf(x.z, w0[2 * KB + k], fmaf(x.w, w0[3 * KB + k], acc[k]))));
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < a.C; ++c) {
+            float x = __ldg(src + c * a.in_sc);
+            if (a.pre_relu) x = fmaxf(x, 0.f);
+            const float* w0 = wr + c * KB;
+#pragma unroll
+            for (int k = 0; k < KB; ++k) acc[k] = fmaf(x, w0[k], acc[k]);
+          }
         }
       }
     }
@@ -356,9 +394,12 @@ static size_t simt_smem_bytes(int bm, int bn) {
 }
 
 void init_simt_kernels() {
-  cudaFuncSetAttribute(conv_direct_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32) * 4);
   for (int i = 0; i < kNumSimt; ++i)
     for (int j = 0; j < 2; ++j)
     {
@@ -383,9 +424,15 @@ int launch_conv(const sw_op_desc& op, void* stream) {
     const int kb = a.K <= 8 ? 8 : (a.K <= 16 ? 16 : 32);
     const size_t smem = ((size_t)a.Kdim * kb + kb) * sizeof(float);
     const dim3 grid((unsigned)cdiv(a.M, 128));
-    if (kb == 8) return (int)launch_k(conv_direct_kernel<8>, grid, dim3(128), smem, st, 1, a);
-    if (kb == 16) return (int)launch_k(conv_direct_kernel<16>, grid, dim3(128), smem, st, 1, a);
-    return (int)launch_k(conv_direct_kernel<32>, grid, dim3(128), smem, st, 1, a);
+    const bool k3 = a.R == 3 && a.S == 3;
+    if (kb == 8)
+      return (int)(k3 ? launch_k(conv_direct_kernel<8, 3>, grid, dim3(128), smem, st, 1, a)
+                      : launch_k(conv_direct_kernel<8, 0>, grid, dim3(128), smem, st, 1, a));
+    if (kb == 16)
+      return (int)(k3 ? launch_k(conv_direct_kernel<16, 3>, grid, dim3(128), smem, st, 1, a)
+                      : launch_k(conv_direct_kernel<16, 0>, grid, dim3(128), smem, st, 1, a));
+    return (int)(k3 ? launch_k(conv_direct_kernel<32, 3>, grid, dim3(128), smem, st, 1, a)
+                    : launch_k(conv_direct_kernel<32, 0>, grid, dim3(128), smem, st, 1, a));
   }
   if (op.variant >= 16) return launch_conv_pw(op, op.variant - 16, stream);  // conv1x1.cu (TMA)
   if (op.variant < 0 || op.variant >= kNumSimt) return (int)cudaErrorInvalidValue;
