@@ -283,8 +283,8 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   pdl_trigger();
   pdl_wait();
   __syncthreads();
-  const int m = blockIdx.x * blockDim.x + tid;
-  if (m >= a.M) return;
+  const int m0 = blockIdx.x * blockDim.x;
+  const int m = min(m0 + tid, a.M - 1);  // tail threads recompute the last pixel (not stored)
   const int q = m % a.Q;
   const int t = m / a.Q;
   const int p = t % a.P, nb = t / a.P;
@@ -369,21 +369,35 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   float* o = a.out + nb * a.out_sn + p * a.out_sh + q * a.out_sw;
   const float* rp = a.has_res ? a.res + nb * a.res_sn + p * a.res_sh + q * a.res_sw : nullptr;
   if (a.epi.vec && (a.K & 3) == 0) {
+    // stage the CTA's [128 px][K] tile in smem, then store it with consecutive
+    // threads on consecutive 16-byte chunks (a per-thread K-float run would
+    // make every store instruction touch 32 different lines)
+    float* tile = bsm + KB;  // [128][KB + 4]
+    constexpr int LD = KB + 4;
 #pragma unroll
-    for (int k = 0; k < KB; k += 4) {
-      if (k >= a.K) break;
-      float4 v = make_float4(acc[k], acc[k + 1], acc[k + 2], acc[k + 3]);
-      if (rp) v = f4add(v, *reinterpret_cast<const float4*>(rp + k));
-      *reinterpret_cast<float4*>(o + k) = act4(v, a.act);
+    for (int k = 0; k < KB; ++k) tile[tid * LD + k] = acc[k];
+    __syncthreads();
+    const int npx = min(128, a.M - m0);
+    const int g4 = a.K / 4;
+    for (int e = tid; e < npx * g4; e += 128) {
+      const int px = e / g4, k = (e % g4) * 4;
+      const int mm = m0 + px;
+      const int qq = mm % a.Q, tt = mm / a.Q;
+      const int pp = tt % a.P, nn = tt / a.P;
+      float4 v = *reinterpret_cast<const float4*>(&tile[px * LD + k]);
+      if (a.has_res)
+        v = f4add(v, *reinterpret_cast<const float4*>(a.res + nn * a.res_sn + pp * a.res_sh + qq * a.res_sw + k));
+      *reinterpret_cast<float4*>(a.out + nn * a.out_sn + pp * a.out_sh + qq * a.out_sw + k) = act4(v, a.act);
     }
-  } else {
+    return;
+  }
+  if (m0 + tid >= a.M) return;
 #pragma unroll
-    for (int k = 0; k < KB; ++k) {
-      if (k >= a.K) break;
-      float v = acc[k];
-      if (rp) v += rp[k * a.res_sc];
-      o[k * a.out_sc] = apply_act(v, a.act);
-    }
+  for (int k = 0; k < KB; ++k) {
+    if (k >= a.K) break;
+    float v = acc[k];
+    if (rp) v += rp[k * a.res_sc];
+    o[k * a.out_sc] = apply_act(v, a.act);
   }
 }
 
@@ -394,12 +408,12 @@ static size_t simt_smem_bytes(int bm, int bn) {
 }
 
 void init_simt_kernels() {
-  cudaFuncSetAttribute(conv_direct_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8 + 128 * (8 + 4)) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16 + 128 * (16 + 4)) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32 + 128 * (32 + 4)) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8 + 128 * (8 + 4)) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16 + 128 * (16 + 4)) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32 + 128 * (32 + 4)) * 4);
   for (int i = 0; i < kNumSimt; ++i)
     for (int j = 0; j < 2; ++j)
     {
@@ -422,7 +436,7 @@ int launch_conv(const sw_op_desc& op, void* stream) {
   if (op.variant == 9) {
     if (a.K > 32 || a.Kdim > 576 || a.split != 1) return (int)cudaErrorInvalidValue;
     const int kb = a.K <= 8 ? 8 : (a.K <= 16 ? 16 : 32);
-    const size_t smem = ((size_t)a.Kdim * kb + kb) * sizeof(float);
+    const size_t smem = ((size_t)a.Kdim * kb + kb + 128 * (size_t)(kb + 4)) * sizeof(float);
     const dim3 grid((unsigned)cdiv(a.M, 128));
     const bool k3 = a.R == 3 && a.S == 3;
     if (kb == 8)
