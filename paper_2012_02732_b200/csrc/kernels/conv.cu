@@ -314,9 +314,16 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
       for (int r = 0; r < KS; ++r)
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
-          const float* w0 = wsm + ((r * KS + s) * a.C + c) * KB;
+          const float4* w4 = reinterpret_cast<const float4*>(wsm + ((r * KS + s) * a.C + c) * KB);
+          const float xv = x[r * KS + s];
 #pragma unroll
-          for (int k = 0; k < KB; ++k) acc[k] = fmaf(x[r * KS + s], w0[k], acc[k]);
+          for (int k4 = 0; k4 < KB / 4; ++k4) {
+            const float4 w = w4[k4];  // one 16-B shared load per 4 FMAs
+            acc[4 * k4] = fmaf(xv, w.x, acc[4 * k4]);
+            acc[4 * k4 + 1] = fmaf(xv, w.y, acc[4 * k4 + 1]);
+            acc[4 * k4 + 2] = fmaf(xv, w.z, acc[4 * k4 + 2]);
+            acc[4 * k4 + 3] = fmaf(xv, w.w, acc[4 * k4 + 3]);
+          }
         }
     }
   } else {
@@ -347,10 +354,16 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
               if (a.pre_relu) {
                 x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
               }
-              const float* w0 = wr + c * KB;
+              const float4* w4 = reinterpret_cast<const float4*>(wr + c * KB);
+              constexpr int G = KB / 4;
 #pragma unroll
-              for (int k = 0; k < KB; ++k)
-                acc[k] = fmaf(x.x, w0[k], fmaf(x.y, w0[KB + k], fmaf(x.z, w0[2 * KB + k], fmaf(x.w, w0[3 * KB + k], acc[k]))));
+              for (int k4 = 0; k4 < G; ++k4) {
+                const float4 w0 = w4[k4], w1 = w4[G + k4], w2 = w4[2 * G + k4], w3 = w4[3 * G + k4];
+                acc[4 * k4] = fmaf(x.x, w0.x, fmaf(x.y, w1.x, fmaf(x.z, w2.x, fmaf(x.w, w3.x, acc[4 * k4]))));
+                acc[4 * k4 + 1] = fmaf(x.x, w0.y, fmaf(x.y, w1.y, fmaf(x.z, w2.y, fmaf(x.w, w3.y, acc[4 * k4 + 1]))));
+                acc[4 * k4 + 2] = fmaf(x.x, w0.z, fmaf(x.y, w1.z, fmaf(x.z, w2.z, fmaf(x.w, w3.z, acc[4 * k4 + 2]))));
+                acc[4 * k4 + 3] = fmaf(x.x, w0.w, fmaf(x.y, w1.w, fmaf(x.z, w2.w, fmaf(x.w, w3.w, acc[4 * k4 + 3]))));
+              }
             }
           }
         } else {
@@ -358,9 +371,15 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
           for (int c = 0; c < a.C; ++c) {
             float x = __ldg(src + c * a.in_sc);
             if (a.pre_relu) x = fmaxf(x, 0.f);
-            const float* w0 = wr + c * KB;
+            const float4* w4 = reinterpret_cast<const float4*>(wr + c * KB);
 #pragma unroll
-            for (int k = 0; k < KB; ++k) acc[k] = fmaf(x, w0[k], acc[k]);
+            for (int k4 = 0; k4 < KB / 4; ++k4) {
+              const float4 w = w4[k4];
+              acc[4 * k4] = fmaf(x, w.x, acc[4 * k4]);
+              acc[4 * k4 + 1] = fmaf(x, w.y, acc[4 * k4 + 1]);
+              acc[4 * k4 + 2] = fmaf(x, w.z, acc[4 * k4 + 2]);
+              acc[4 * k4 + 3] = fmaf(x, w.w, acc[4 * k4 + 3]);
+            }
           }
         }
       }
