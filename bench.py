@@ -368,7 +368,8 @@ def run_ours(args, world, rank, local):
             },
             "host_overhead": {"launch_us_per_iter": round(host_us, 3),
                               "gpu_us_per_iter": round(gpu_us, 3),
-                              "fraction_of_gpu_time": round(host_us / gpu_us, 5)},
+                              "fraction_of_gpu_time": round(host_us / gpu_us, 5),
+                              "fraction_of_roofline_sum": round(host_us / roof_sum, 5)},
             "simulated_from_measured": {"multi_stream_us": round(sim_multi, 2),
                                         "single_stream_us": round(sim_single, 2),
                                         "critical_path_us": round(crit, 2)},
