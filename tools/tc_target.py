@@ -21,14 +21,18 @@ def main():
     ap.add_argument("--variant", type=int, default=1128)
     ap.add_argument("--split", type=int, default=1)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--kind", type=int, default=6, help="6 = tcgen05, 1 = SIMT")
     a = ap.parse_args()
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import Engine, K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
-    m = nn.Sequential(nn.Conv2d(a.cin, a.cin, 1), nn.ReLU(), nn.Conv2d(a.cin, a.cout, 1)).eval()
+    m = nn.Sequential(nn.Conv2d(a.cin, a.cin, 1), nn.ReLU(),
+                      nn.Conv2d(a.cin, a.cout, a.k, padding=a.k // 2)).eval()
     x = torch.randn(a.batch, a.cin, a.hw, a.hw)
     eng = Engine(m, conv_impl="tc").prepare(x)
     d = eng.ops[1]
     assert d.kind == K_CONV_TC
+    d.kind = a.kind
     d.variant = a.variant
     d.params[SP_SPLIT_K] = a.split
     N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
@@ -38,7 +42,7 @@ def main():
         eng.replay(True)
     eng.synchronize()
     gpu, _ = eng.time_replay(True, 20)
-    flops = 2.0 * a.batch * a.hw * a.hw * a.cin * a.cout
+    flops = 2.0 * a.batch * a.hw * a.hw * a.cin * a.cout * a.k * a.k
     print(f"replay (both convs) {gpu:.1f} us; layer {flops / 1e9:.2f} GFLOP")
 
 
