@@ -190,7 +190,7 @@ typedef struct sw_engine sw_engine;
 /* One kernel task of the op table.  kind = enum sw_kernel_kind (see
  * paper_2012_02732_b200/csrc/runtime/ops.h); params/ptrs meanings per kind are
  * documented there and in DESIGN.md §Kernels. */
-#define SW_OP_MAX_PARAMS 48
+#define SW_OP_MAX_PARAMS 56
 #define SW_OP_MAX_PTRS 8
 typedef struct sw_op_desc {
   int32_t kind;

@@ -50,7 +50,7 @@ class SimConfigC(C.Structure):
                 ("framework_mode", i32)]
 
 
-SW_OP_MAX_PARAMS = 48
+SW_OP_MAX_PARAMS = 56
 SW_OP_MAX_PTRS = 8
 
 

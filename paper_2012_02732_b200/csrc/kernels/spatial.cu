@@ -20,6 +20,7 @@ struct SpatialArgs {
   const float* __restrict__ bias;  // [C]
   const float* __restrict__ res;
   int N, H, W, C, P, Q, R, S, sh, sw, ph, pw, act, pre_relu, has_res, mode, count_pad, pad_b, pad_r;
+  float mul;  // pool output multiplier (twin pools of one input merged)
   int64_t in_sn, in_sh, in_sw, in_sc;
   int64_t out_sn, out_sh, out_sw, out_sc;
   int64_t res_sn, res_sh, res_sw, res_sc;
@@ -41,6 +42,7 @@ static SpatialArgs spatial_args(const sw_op_desc& op) {
   a.act = (int)p[SP_ACT]; a.pre_relu = (int)p[SP_PRE_RELU]; a.has_res = (int)p[SP_HAS_RES];
   a.mode = (int)p[SP_POOL_MODE]; a.count_pad = (int)p[SP_COUNT_PAD];
   a.pad_b = (int)p[SP_PAD_BOTTOM]; a.pad_r = (int)p[SP_PAD_RIGHT];
+  a.mul = p[SP_POOL_MUL] > 0 ? (float)p[SP_POOL_MUL] : 1.f;
   a.in_sn = p[SP_IN_SN]; a.in_sh = p[SP_IN_SH]; a.in_sw = p[SP_IN_SW]; a.in_sc = p[SP_IN_SC];
   a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
   a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
@@ -149,6 +151,9 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
       div = (he - ih0) * (we - iw0);
     }
     scale(acc, div > 0 ? 1.f / (float)div : 0.f);
+    if (a.mul != 1.f) scale(acc, a.mul);  // power-of-two multiplier: exact, = summing the twins
+  } else if (a.mul != 1.f) {
+    scale(acc, a.mul);
   }
   if (a.has_res) {
     const float* rp = a.res + n * a.res_sn + p * a.res_sh + q * a.res_sw + c * a.res_sc;

@@ -47,7 +47,7 @@ enum KernelKind : int32_t {
 // epilogue, SP_PRE_RELU the first depthwise's input ReLU, SP_SPLIT_K the
 // cluster size = row bands per image)
 enum Sep2Param : int {
-  S2_MID = 35,      // channels between the two sepconvs
+  S2_MID = 36,      // channels between the two sepconvs
   S2_ACT1,          // activation after the first pointwise (+ folded BN)
   S2_DW_ACT1,       // activation after the first depthwise
   S2_DW_ACT2,       // activation after the second depthwise
@@ -147,7 +147,8 @@ enum SpatialParam : int {
   SP_OUT_SC,                           // output channel stride (1 = NHWC, H*W = NCHW output)
   SP_RES_SC,                           // residual channel stride (0 → 1)
   SP_KPAD,                             // K_CONV_TC: row stride of the pre-split weights
-  SP_DW_ACT                            // K_SEPCONV: activation between depthwise and pointwise
+  SP_DW_ACT,                           // K_SEPCONV: activation between depthwise and pointwise
+  SP_POOL_MUL                          // K_POOL: integer output multiplier (0 → 1): twin pools merged
 };
 // K_SEPCONV: PT_W / PT_BIAS = pointwise [K][C] / [K]; PT_WS = depthwise
 // weights [R][S][C]; PT_DW_BIAS = depthwise bias [C]; spatial params describe

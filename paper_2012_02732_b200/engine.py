@@ -44,13 +44,13 @@ EW_ADD, EW_MUL, EW_AFFINE, EW_COPY = 0, 1, 2, 3
 (SP_N, SP_H, SP_W, SP_C, SP_P, SP_Q, SP_K, SP_R, SP_S, SP_STRIDE_H, SP_STRIDE_W, SP_PAD_H,
  SP_PAD_W, SP_ACT, SP_PRE_RELU, SP_IN_SN, SP_IN_SH, SP_IN_SW, SP_IN_SC, SP_OUT_SN, SP_OUT_SH,
  SP_OUT_SW, SP_RES_SN, SP_RES_SH, SP_RES_SW, SP_HAS_RES, SP_POOL_MODE, SP_COUNT_PAD,
- SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC, SP_KPAD, SP_DW_ACT) = range(35)
+ SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC, SP_KPAD, SP_DW_ACT, SP_POOL_MUL) = range(36)
 PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS, PT_W_TC_HI, PT_W_TC_LO = range(8)
 PT_DW_BIAS = 6  # K_SEPCONV
 K_SEPCONV = 8
 K_SEP2 = 24  # fused NASNet separable block (csrc/kernels/sep2.cu)
 (S2_MID, S2_ACT1, S2_DW_ACT1, S2_DW_ACT2, S2_PRE_RELU2, S2_OFF_DW1, S2_OFF_PW1, S2_OFF_B1, S2_OFF_DB1,
- S2_OFF_DW2, S2_OFF_PW2, S2_OFF_B2, S2_OFF_DB2) = range(35, 48)
+ S2_OFF_DW2, S2_OFF_PW2, S2_OFF_B2, S2_OFF_DB2) = range(36, 49)
 TC_BK = 32  # K tile of the tcgen05 conv; its pre-split weights are padded to a multiple
 (EW_N, EW_H, EW_W, EW_C, EW_OP, EW_ACT, EW_A_SN, EW_A_SH, EW_A_SW, EW_A_SC, EW_B_SN, EW_B_SH,
  EW_B_SW, EW_B_SC, EW_C_SN, EW_C_SH, EW_C_SW, EW_C_SC, EW_O_SN, EW_O_SH, EW_O_SW, EW_O_SC,
@@ -288,6 +288,7 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 vals[SP_COUNT_PAD] = int(n.attrs["cip"])
                 vals[SP_PAD_BOTTOM] = ph
                 vals[SP_PAD_RIGHT] = pw
+                vals[SP_POOL_MUL] = int(n.attrs.get("mul", 1))
                 d.kind = K_POOL
             elif t.kind == "dwconv":
                 d.kind = K_DWCONV

@@ -480,10 +480,35 @@ def _fuse_sep_pairs(nodes, max_hw: int = 196):
     return [n for n in nodes if id(n) not in drop]
 
 
+def _merge_twin_pools(nodes):
+    """add(pool(x), pool'(x)) with two identical pooling ops on the same input
+    (NASNet normal cell: i3 = avg3(left) + avg3(left)) becomes ONE pool with an
+    output multiplier of 2 — exactly the sum in fp32 (doubling is exact)."""
+    users = _users(nodes)
+    drop = set()
+    for n in nodes:
+        if n.kind != "add" or len(n.inputs) != 2:
+            continue
+        a, b = n.inputs
+        if a is b or a.kind != "pool" or b.kind != "pool" or id(a) in drop or id(b) in drop:
+            continue
+        if a.inputs[0] is not b.inputs[0] or a.attrs != b.attrs or a.act != b.act or a.pre_relu != b.pre_relu:
+            continue
+        if a.residual is not None or b.residual is not None or len(users[id(a)]) != 1 or \
+                len(users[id(b)]) != 1:
+            continue
+        a.attrs = dict(a.attrs, mul=2)
+        _replace_uses(nodes, n, a)
+        drop.add(id(b))
+        drop.add(id(n))
+    return [n for n in nodes if id(n) not in drop]
+
+
 def optimize(nodes: list[INode], fuse_separable: bool = True, fuse_sep_pairs=False) -> list[INode]:
     out_node = nodes[-1]
     nodes = _drop_identities(nodes)
     nodes = _fold_bn(nodes)
+    nodes = _merge_twin_pools(nodes)
     nodes = _fold_residual_adds(nodes)
     nodes = _fold_acts(nodes, out_node)
     nodes = _pre_relu(nodes)

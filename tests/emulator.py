@@ -184,6 +184,8 @@ def run_op(mem: HostMemory, d):
                 else:
                     cnt = F.avg_pool2d(valid.double()[None, None], (R, S), (sh, sw))[0, 0] * (R * S)
                 y = (s / cnt.double().clamp(min=1)).float()
+            if p[E.SP_POOL_MUL] > 1:
+                y = y * float(p[E.SP_POOL_MUL])
         if p[E.SP_HAS_RES]:
             r = mem.gather(q[E.PT_RES], (Nb, K, P, Q),
                            (p[E.SP_RES_SN], p[E.SP_RES_SH], p[E.SP_RES_SW], p[E.SP_RES_SC] or 1))
