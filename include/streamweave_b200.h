@@ -231,6 +231,12 @@ int sw_engine_time_replay(sw_engine* e, int32_t slot, int32_t iters, double* out
 int sw_engine_launch_op(sw_engine* e, int64_t index);
 /* Eager run of all ops in the given order on one stream, host loop in C. */
 int sw_engine_run_eager(sw_engine* e, int64_t n, const int64_t* order);
+/* Framework (non-AoT) mode of a pre_run schedule: every LAUNCH / RECORD / WAIT
+ * issued now by the host on the engine's stream pool, no capture (the
+ * run-time-scheduling baseline of sim.py:69-80, multi-stream). */
+int sw_engine_run_schedule(sw_engine* e, int64_t n_streams, const int64_t* stream_len,
+                           const int32_t* op_kind, const int64_t* op_arg, int64_t n_order,
+                           const int64_t* order);
 int sw_engine_synchronize(sw_engine* e);
 /* Captured graph topology of a slot: node count and dependency edge count;
  * out_edges (capacity 2*cap) receives (from, to) node indices where node

@@ -99,6 +99,7 @@ PROTOTYPES = {
     "sw_engine_launch_op": (C.c_int, [C.c_void_p, i64]),
     "sw_engine_run_eager": (C.c_int, [C.c_void_p, i64, P64]),
     "sw_engine_synchronize": (C.c_int, [C.c_void_p]),
+    "sw_engine_run_schedule": (C.c_int, [C.c_void_p, i64, P64, P32, P64, i64, P64]),
     "sw_engine_graph_topology": (C.c_int, [C.c_void_p, i32, i64, P64, P32, P64, P64, P64]),
     "sw_engine_profile_ops": (C.c_int, [C.c_void_p, i64, P64, i32, C.POINTER(C.c_double)]),
     "sw_engine_stream": (C.c_int, [C.c_void_p, PU64]),

@@ -538,6 +538,53 @@ int sw_engine_run_eager(sw_engine* e, int64_t n, const int64_t* order) {
   return SW_OK;
 }
 
+// Framework mode on the device (sim.py:69-80 analogue): the same pre_run
+// schedule issued op by op by the host every iteration — LAUNCH on the
+// logical stream's CUDA stream, RECORD / WAIT as real cudaEventRecord /
+// cudaStreamWaitEvent — with no capture.  Forked from / joined back to the
+// launch stream like the captured graph.
+int sw_engine_run_schedule(sw_engine* e, int64_t n_streams, const int64_t* stream_len, const int32_t* op_kind,
+                           const int64_t* op_arg, int64_t n_order, const int64_t* order) {
+  int rc = ensure_streams(e, n_streams);
+  if (rc) return rc;
+  int64_t max_event = -1;
+  std::vector<int64_t> base(n_streams + 1, 0);
+  for (int64_t s = 0; s < n_streams; ++s) base[s + 1] = base[s] + stream_len[s];
+  for (int64_t k = 0; k < base[n_streams]; ++k)
+    if (op_kind[k] != SW_OP_LAUNCH) max_event = std::max(max_event, op_arg[k]);
+  rc = ensure_events(e, max_event + 1);
+  if (rc) return rc;
+  sw::g_launch_pdl = (e->flags & SW_ENGINE_PDL) != 0;
+  struct Reset {
+    ~Reset() { sw::g_launch_pdl = false; }
+  } reset;
+  CU(cudaEventRecord(e->fork, e->launch));
+  for (int64_t s = 0; s < n_streams; ++s) CU(cudaStreamWaitEvent(e->streams[s], e->fork, 0));
+  std::vector<int64_t> cursor(n_streams, 0);
+  for (int64_t i = 0; i < n_order; ++i) {
+    const int64_t s = order[i];
+    if (s < 0 || s >= n_streams || cursor[s] >= stream_len[s])
+      return sw::fail(SW_VALUE_ERROR, "order does not match the stream FIFOs");
+    const int64_t k = base[s] + cursor[s]++;
+    cudaStream_t st = e->streams[s];
+    if (op_kind[k] == SW_OP_LAUNCH) {
+      if (op_arg[k] < 0 || op_arg[k] >= (int64_t)e->ops.size())
+        return sw::fail(SW_GRAPH_ERROR, "schedule launches unknown task " + std::to_string(op_arg[k]));
+      rc = launch_task(e, e->ops[op_arg[k]], st);
+      if (rc) return rc;
+    } else if (op_kind[k] == SW_OP_RECORD) {
+      CU(cudaEventRecord(e->events[op_arg[k]], st));
+    } else {
+      CU(cudaStreamWaitEvent(st, e->events[op_arg[k]], 0));
+    }
+  }
+  for (int64_t s = 0; s < n_streams; ++s) {
+    CU(cudaEventRecord(e->joins[s], e->streams[s]));
+    CU(cudaStreamWaitEvent(e->launch, e->joins[s], 0));
+  }
+  return SW_OK;
+}
+
 int sw_engine_synchronize(sw_engine* e) {
   CU(cudaStreamSynchronize(e->launch));
   CU(cudaGetLastError());

@@ -723,6 +723,46 @@ class Engine:
             N.check(lib.sw_engine_run_eager(self._h, len(self.eager_order),
                                             N.ptr64(self.eager_order)))
 
+    def run_framework(self, multi: bool = True):
+        """Framework (non-AoT) mode: the pre_run schedule issued op by op now,
+        on the logical streams with real event record / wait (multi) or on one
+        stream (single) — the run-time-scheduling baseline (sim.py:69-80)."""
+        ts = self.schedule if multi else self.schedule_single
+        lens, kinds, args, order = schedule_arrays(ts)
+        N.check(N.lib().sw_engine_run_schedule(self._h, len(ts.streams), N.ptr64(lens), N.ptr32(kinds),
+                                               N.ptr64(args), len(ts.order), N.ptr64(order)))
+
+    def compare(self, iters: int = 50) -> dict:
+        """The reference's 4-mode matrix (compare.py:22-104) measured on the
+        device: (framework | replay) x (single | multi), device-resident input,
+        mean µs per iteration of host issue + execution (synchronised each
+        iteration), speed-ups against framework-single."""
+        lib = N.lib()
+        runs = {}
+        for mode, layout in (("framework", "single"), ("framework", "multi"),
+                             ("replay", "single"), ("replay", "multi")):
+            multi = layout == "multi"
+
+            def once():
+                if mode == "framework":
+                    self.run_framework(multi)
+                else:
+                    self.replay(multi=multi)
+                N.check(lib.sw_engine_synchronize(self._h))
+            for _ in range(3):
+                once()
+            t = time.perf_counter()
+            for _ in range(iters):
+                once()
+            runs[(mode, layout)] = (time.perf_counter() - t) / iters * 1e6
+        base = runs[("framework", "single")]
+        return {"modes": [{"mode": m, "layout": l, "us": round(v, 2),
+                           "num_streams": self.assignment.num_streams if l == "multi" else 1,
+                           "speedup_vs_baseline": round(base / v, 4)} for (m, l), v in runs.items()],
+                "stream_count": self.assignment.num_streams, "sync_count": len(self.plan),
+                "replay_multi_over_single": round(runs[("replay", "single")] / runs[("replay", "multi")], 4),
+                "replay_over_framework": round(runs[("framework", "multi")] / runs[("replay", "multi")], 4)}
+
     def time_replay(self, multi: bool = True, iters: int = 200, io: bool = False):
         slot = (SLOT_MULTI_IO if multi else SLOT_SINGLE_IO) if io else \
             (SLOT_MULTI if multi else SLOT_SINGLE)

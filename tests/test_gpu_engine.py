@@ -551,3 +551,24 @@ def test_fused_separable_block_kernel_parity():
     assert eng.program.stats().get("sep2", 0) > 0
     close(y, ref)
     eng.close()
+
+
+def test_compare_matrix_and_framework_mode():
+    """Measured 4-mode matrix (compare.py:22-104 on the device): the framework
+    modes run the same schedule op by op and give the replay's result."""
+    model, shape = build_model("nasnet_mobile")
+    x = example_input(shape)
+    eng = Engine(model, conv_impl="simt").prepare(x)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    y_replay = eng.device_output().clone()
+    for multi in (True, False):
+        eng.run_framework(multi)
+        eng.synchronize()
+        assert torch.equal(eng.device_output(), y_replay)
+    rep = eng.compare(iters=5)
+    assert [(m["mode"], m["layout"]) for m in rep["modes"]] == [
+        ("framework", "single"), ("framework", "multi"), ("replay", "single"), ("replay", "multi")]
+    assert rep["stream_count"] == eng.assignment.num_streams and rep["replay_multi_over_single"] > 1
+    eng.close()
