@@ -270,6 +270,22 @@ def run_ours(args, world, rank, local):
     eager = [eager_once() for _ in range(max(5, args.steps // 4))]
     eager_ms = 1e3 * sum(eager) / len(eager)
 
+    def framework_multi_once():
+        # framework mode, multi-stream: the schedule issued op by op with real
+        # event record / wait on the logical streams (sim.py:69-80 analogue)
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        eng.run_framework(multi=True)
+        eng.synchronize()
+        return time.perf_counter() - t
+
+    for _ in range(3):
+        framework_multi_once()
+    fw = [framework_multi_once() for _ in range(max(5, args.steps // 4))]
+    fw_multi_ms = 1e3 * sum(fw) / len(fw)
+
     # e2e through the public API: host tensor in (pinned host memory, as the
     # contract's e2e specifies; copied into the engine's pinned staging buffer
     # inside the call), host tensor out
@@ -361,6 +377,7 @@ def run_ours(args, world, rank, local):
                 "multi_stream_aot_us": round(ms * 1e3, 2),
                 "single_stream_aot_us": round(single_ms * 1e3, 2),
                 "eager_non_aot_us": round(eager_ms * 1e3, 2),
+                "framework_multi_stream_non_aot_us": round(fw_multi_ms * 1e3, 2),
                 ("multi_stream_aot_no_pdl_us" if eng.pdl else "multi_stream_aot_pdl_us"):
                     round(alt_ms * 1e3, 2),
                 "multi_over_single": round(single_ms / ms, 4),
