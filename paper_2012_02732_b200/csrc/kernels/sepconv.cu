@@ -588,8 +588,10 @@ constexpr SepCfg kSep[] = {{16, 32}, {8, 64}, {16, 64}, {32, 32}, {8, 32}, {32, 
 constexpr int kNumSep = sizeof(kSep) / sizeof(kSep[0]);
 // row-blocked depthwise variants (4 pixels per thread), after the TMA ones
 constexpr int kSepRowFirst = 11;
-constexpr SepCfg kSepRow[] = {{64, 32}, {128, 32}, {64, 64}};
-constexpr int kNumSepRow = 3;
+// (wide column tiles: the depthwise is recomputed once per column block, so
+// K up to 128 per block keeps that redundancy low for 88 / 176-channel layers)
+constexpr SepCfg kSepRow[] = {{64, 32}, {128, 32}, {64, 64}, {64, 128}, {32, 128}};
+constexpr int kNumSepRow = 5;
 constexpr int kSepSmemMax = 227 * 1024;
 }  // namespace
 
@@ -611,6 +613,8 @@ static cudaError_t launch_sep_v(int v, const SepArgs& a, dim3 grid, size_t smem,
     case 11: return launch_k(sepconv_kernel<KS, VEC, 64, 32, 2, 4, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
     case 12: return launch_k(sepconv_kernel<KS, VEC, 128, 32, 4, 4, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
     case 13: return launch_k(sepconv_kernel<KS, VEC, 64, 64, 4, 4, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 14: return launch_k(sepconv_kernel<KS, VEC, 64, 128, 4, 8, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
+    case 15: return launch_k(sepconv_kernel<KS, VEC, 32, 128, 2, 8, 4>, grid, dim3(SEP_THREADS), smem, st, 1, a);
     default: return launch_k(sepconv_kernel<KS, VEC, 16, 32, 1, 2>, grid, dim3(SEP_THREADS), smem, st, 1, a);
   }
 }
@@ -772,6 +776,10 @@ static void init_sep_ks() {
     cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 128, 32, 4, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSepSmemMax);
     cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 64, 64, 4, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSepSmemMax);
+    cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 64, 128, 4, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSepSmemMax);
+    cudaFuncSetAttribute(sepconv_kernel<KS, VEC, 32, 128, 2, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSepSmemMax);
   }
 }

@@ -88,7 +88,7 @@ SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (
              # TMA-staged kernel (one output row per CTA): BM pixels x BN channels
              6: (4, 32), 7: (8, 32), 8: (8, 64), 9: (16, 32), 10: (16, 64),
              # row-blocked depthwise (4 pixels per thread, large batches)
-             11: (64, 32), 12: (128, 32), 13: (64, 64)}
+             11: (64, 32), 12: (128, 32), 13: (64, 64), 14: (64, 128), 15: (32, 128)}
 SEP_TMA_FIRST = 6
 SEP_ROW_FIRST = 11
 

@@ -186,7 +186,7 @@ def test_direct_thin_conv(cin, cout, k, s, p, h, lead, relu):
     eng.close()
 
 
-@pytest.mark.parametrize("variant", [11, 12, 13])
+@pytest.mark.parametrize("variant", [11, 12, 13, 14, 15])
 @pytest.mark.parametrize("c,k,s,h,batch", [(44, 5, 1, 14, 3), (11, 7, 2, 23, 2), (32, 7, 2, 111, 2),
                                            (176, 3, 1, 7, 5), (24, 3, 2, 9, 3)])
 def test_sepconv_row_blocked_variants(variant, c, k, s, h, batch):
