@@ -651,6 +651,68 @@ class Engine:
                 self.tuning[t.tid] = best
         N.check(lib.sw_engine_synchronize(self._h))
 
+    def candidate_ctas(self, tid: int, kind: int, variant: int, split: int) -> int:
+        """CTAs a tuning candidate launches (the launchers' grid formulas)."""
+        p = self.ops[tid].params
+        M, K = p[SP_N] * p[SP_P] * p[SP_Q], p[SP_K]
+        cd = math.ceil
+        if kind == K_CONV:
+            if variant == 8:
+                return cd(K * 32 / 256)
+            if variant == 9:
+                return cd(M / 128)
+            bm, bn = PW_TILES[variant] if variant >= 16 else SIMT_TILES[variant]
+            return cd(M / bm) * cd(K / bn) * max(1, split)
+        if kind == K_CONV_TC:
+            return cd(M / 128) * cd(K / (variant % 1000)) * max(1, split)
+        if kind == K_SEPCONV:
+            bm, bn = SEP_TILES[variant]
+            if SEP_TMA_FIRST <= variant < SEP_ROW_FIRST:
+                rows = p[SP_N] * p[SP_P] * cd(p[SP_Q] / bm)
+                return rows * (split if split > 1 else cd(K / bn))
+            return cd(M / bm) * cd(K / bn)
+        if kind == K_SEP2:
+            return p[SP_N] * max(1, split)
+        return 1
+
+    def refine_graph(self, caps=(None, 592, 296, 148), iters: int = 100):
+        """Graph-level kernel selection: the per-task autotuner times every
+        candidate alone, but in the multi-stream replay kernels share the GPU.
+        For each cap on a kernel's CTA count, re-pick every tuned task's
+        fastest candidate within the cap (from the tuning log, no re-timing),
+        re-capture and time the whole replay; keep the best cap."""
+        lib = N.lib()
+        picks0 = {tid: (d.kind, d.variant, int(d.params[SP_SPLIT_K])) for tid, d in
+                  ((t.tid, self.ops[t.tid]) for t in self.program.tasks) if tid in self.tuning}
+        results = {}
+        best = None
+        for cap in caps:
+            for tid, log in self.tuning_log.items():
+                ok = [c for c in log if c[3] is not None and
+                      (cap is None or self.candidate_ctas(tid, c[0], c[1], c[2]) <= cap)]
+                kind, variant, split = picks0[tid] if not ok else min(ok, key=lambda c: c[3])[:3]
+                d = self.ops[tid]
+                d.kind, d.variant = kind, variant
+                d.params[SP_SPLIT_K] = split
+            N.check(lib.sw_engine_set_ops(self._h, len(self.program.tasks), self.ops))
+            self._capture(SLOT_MULTI, self.schedule, False)
+            self.replay(True)
+            self.synchronize()
+            us, _ = self.time_replay(True, iters)
+            results[cap] = us
+            if best is None or us < best[0]:
+                best = (us, cap, {tid: (d.kind, d.variant, int(d.params[SP_SPLIT_K]))
+                                  for tid, d in ((t, self.ops[t]) for t in picks0)})
+        for tid, (kind, variant, split) in best[2].items():
+            d = self.ops[tid]
+            d.kind, d.variant = kind, variant
+            d.params[SP_SPLIT_K] = split
+        N.check(lib.sw_engine_set_ops(self._h, len(self.program.tasks), self.ops))
+        self.recapture()
+        self.graph_tuning = {"replay_us_by_cta_cap": {str(k): round(v, 2) for k, v in results.items()},
+                             "chosen_cap": best[1]}
+        return self.graph_tuning
+
     @staticmethod
     def model_output_shape(prog: Program):
         o = prog.output_view.st
