@@ -240,8 +240,9 @@ int sw_engine_run_schedule(sw_engine* e, int64_t n_streams, const int64_t* strea
 int sw_engine_synchronize(sw_engine* e);
 /* Captured graph topology of a slot: node count and dependency edge count;
  * out_edges (capacity 2*cap) receives (from, to) node indices where node
- * index = position in cudaGraphGetNodes order; out_node_kind: 0 kernel,
- * 1 memcpy, 2 other; out_node_task: op index for kernel nodes else -1. */
+ * index = position in cudaGraphGetNodes order; out_node_kind: 0 task kernel,
+ * 1 memcpy, 2 other, 3 engine plumbing kernel (staging copy / L2 prefetch);
+ * out_node_task: op index for task kernel nodes else -1. */
 int sw_engine_graph_topology(sw_engine* e, int32_t slot, int64_t cap, int64_t* out_n_nodes,
                              int32_t* out_node_kind, int64_t* out_node_task,
                              int64_t* out_n_edges, int64_t* out_edges);
@@ -269,11 +270,16 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
  * replay, sw_engine_trace_read returns each task's start / end in µs from the
  * graph's start (the measured timeline behind a Chrome trace). */
 #define SW_ENGINE_TRACE 16u
+/* A root node on its own stream prefetches the range given to
+ * sw_engine_set_prefetch (the packed weights) into L2 at graph start. */
+#define SW_ENGINE_L2_PREFETCH 32u
 int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
 /* ---- training step (paper_2012_02732_b200/train.py) ---- */
 /* One more captured H2D copy in the with_io slots (labels next to images). */
 int sw_engine_add_input(sw_engine* e, uint64_t host, uint64_t dev, int64_t bytes);
+/* Device range warmed into L2 by SW_ENGINE_L2_PREFETCH captures. */
+int sw_engine_set_prefetch(sw_engine* e, uint64_t dev, int64_t bytes);
 /* Bind NCCL at run time (dlopen of `path`, or "libnccl.so.2" when NULL/empty). */
 int sw_nccl_load(const char* path);
 /* ncclGetUniqueId into a caller buffer of 128 bytes (rank 0 broadcasts it). */

@@ -115,6 +115,10 @@ struct sw_engine {
   // extra captured H2D copies (training: labels next to the images)
   std::vector<uint64_t> extra_host, extra_dev;
   std::vector<int64_t> extra_bytes;
+  uint64_t prefetch_ptr = 0;  // SW_ENGINE_L2_PREFETCH range
+  int64_t prefetch_bytes = 0;
+  cudaStream_t pf_stream = nullptr;
+  cudaEvent_t pf_join = nullptr;
   void* nccl_comm = nullptr;  // ncclComm_t of the data-parallel group (K_ALLREDUCE)
   // SW_ENGINE_TRACE: timing events around every task (measured Chrome trace)
   std::vector<cudaEvent_t> tr_start, tr_end;
@@ -251,6 +255,8 @@ int sw_engine_destroy(sw_engine* e) {
   for (auto s : e->streams) cudaStreamDestroy(s);
   for (auto ev : e->events) cudaEventDestroy(ev);
   for (auto ev : e->joins) cudaEventDestroy(ev);
+  if (e->pf_stream) cudaStreamDestroy(e->pf_stream);
+  if (e->pf_join) cudaEventDestroy(e->pf_join);
   for (auto ev : e->tr_start) cudaEventDestroy(ev);
   for (auto ev : e->tr_end) cudaEventDestroy(ev);
   if (e->tr0) cudaEventDestroy(e->tr0);
@@ -366,6 +372,15 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   }
   err = cudaEventRecord(e->fork, origin);
   if (err != cudaSuccess) return abort_capture(cuda_fail(err, "fork record"));
+  const bool prefetch = (e->flags & SW_ENGINE_L2_PREFETCH) && e->prefetch_bytes > 0 && e->pf_stream;
+  if (prefetch) {
+    err = cudaStreamWaitEvent(e->pf_stream, e->fork, 0);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "prefetch fork"));
+    err = (cudaError_t)sw::launch_l2_prefetch(reinterpret_cast<const void*>(e->prefetch_ptr), e->prefetch_bytes,
+                                               e->pf_stream);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "prefetch launch"));
+    last_node(e->pf_stream);
+  }
   for (int64_t s = 0; s < n_streams; ++s) {
     err = cudaStreamWaitEvent(e->streams[s], e->fork, 0);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "fork wait"));
@@ -403,6 +418,11 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "join record"));
     err = cudaStreamWaitEvent(origin, e->joins[s], 0);
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "join wait"));
+  }
+  if (prefetch) {
+    err = cudaEventRecord(e->pf_join, e->pf_stream);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(origin, e->pf_join, 0);
+    if (err != cudaSuccess) return abort_capture(cuda_fail(err, "prefetch join"));
   }
   if (with_io && e->out_bytes > 0) {
     err = kio ? (cudaError_t)sw::launch_io_copy(reinterpret_cast<void*>(e->host_out),
@@ -606,7 +626,8 @@ int sw_engine_graph_topology(sw_engine* e, int32_t slot, int64_t cap, int64_t* o
   for (size_t i = 0; i < nn; ++i) {
     cudaGraphNodeType t;
     CU(cudaGraphNodeGetType(nodes[i], &t));
-    out_node_kind[i] = t == cudaGraphNodeTypeKernel ? 0 : (t == cudaGraphNodeTypeMemcpy ? 1 : 2);
+    out_node_kind[i] = t == cudaGraphNodeTypeKernel ? (sl.io_nodes.count(nodes[i]) ? 3 : 0)
+                                                    : (t == cudaGraphNodeTypeMemcpy ? 1 : 2);
     auto it = sl.node_task.find(nodes[i]);
     out_node_task[i] = it == sl.node_task.end() ? -1 : it->second;
   }
@@ -668,6 +689,17 @@ int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* 
   cudaGraphExecDestroy(ex);
   if (ce != cudaSuccess) return cuda_fail(ce, "time_op replay");
   *out_us = (double)ms * 1000.0 / reps;
+  return SW_OK;
+}
+
+int sw_engine_set_prefetch(sw_engine* e, uint64_t dev, int64_t bytes) {
+  CU(cudaSetDevice(e->device));
+  if (!e->pf_stream) {
+    CU(cudaStreamCreateWithFlags(&e->pf_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&e->pf_join, cudaEventDisableTiming));
+  }
+  e->prefetch_ptr = dev;
+  e->prefetch_bytes = bytes;
   return SW_OK;
 }
 

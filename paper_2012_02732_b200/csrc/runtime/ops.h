@@ -176,6 +176,7 @@ int launch_conv(const sw_op_desc& op, void* stream);
 int launch_null(void* stream);  // diagnostic empty task
 int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream);  // staging copy as a kernel
 int set_io_copy_node(void* exec, void* node, void* dst, const void* src, int64_t bytes);  // re-point it
+int launch_l2_prefetch(const void* p, int64_t bytes, void* stream);  // warm L2 with the weights
 int launch_conv_pw(const sw_op_desc& op, int variant, void* stream);  // conv variants 16..21
 int launch_conv_tc(const sw_op_desc& op, void* stream);
 int launch_dwconv(const sw_op_desc& op, void* stream);

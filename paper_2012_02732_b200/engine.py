@@ -446,7 +446,7 @@ class Engine:
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
                  tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb",
-                 fuse_sep_pairs: bool = False):
+                 fuse_sep_pairs: bool = False, l2_prefetch: bool = True):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -462,6 +462,7 @@ class Engine:
             raise ValueError(f"arena must be 'hb' or 'reference', not {arena!r}")
         self.arena_mode = arena
         self.fuse_sep_pairs = fuse_sep_pairs
+        self.l2_prefetch = l2_prefetch
         self.tuning = {}
         self.tuning_log = {}
         self._h = None
@@ -550,6 +551,7 @@ class Engine:
                                      self.h_in.numel() * 4, self.h_out.data_ptr(),
                                      self.d_out_ptr, self.out_bytes))
         N.check(lib.sw_engine_set_flags(h, self._flags()))  # tuning sees the graph's PDL edges
+        N.check(lib.sw_engine_set_prefetch(h, self.weights.data_ptr(), self.weight_bytes))
         t3 = time.perf_counter()
         if self.conv_impl == "auto":
             self.d_in.copy_(ex.reshape(-1).to(dev))
@@ -572,7 +574,7 @@ class Engine:
 
     def _flags(self) -> int:
         """SW_ENGINE_PDL | SW_ENGINE_KERNEL_IO (include/streamweave_b200.h)."""
-        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0)
+        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0) | (32 if self.l2_prefetch else 0)
 
     def _tuning_signature(self):
         import hashlib
