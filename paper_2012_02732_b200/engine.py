@@ -446,7 +446,7 @@ class Engine:
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
                  tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb",
-                 fuse_sep_pairs: bool = False, l2_prefetch: bool = True):
+                 fuse_sep_pairs: bool = False, l2_prefetch: bool = False):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
