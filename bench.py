@@ -470,6 +470,13 @@ def other_configs(args, dev, hbm, bf16, flush, stream):
             eng.run_eager()
         eng.synchronize()
         eager_us = (time.perf_counter() - t) / 3 * 1e6
+        eng.run_framework(True)
+        eng.synchronize()
+        t = time.perf_counter()
+        for _ in range(5):
+            eng.run_framework(True)
+        eng.synchronize()
+        fw_us = (time.perf_counter() - t) / 5 * 1e6
         roof = eng.roofline_sum_us(hbm, bf16)
         fam_roof = None
         if batch > 1:
@@ -552,6 +559,13 @@ def train_configs(args, dev, world=1, rank=0):
             eng.run_eager()
         eng.synchronize()
         eager_us = (time.perf_counter() - t) / 3 * 1e6
+        eng.run_framework(True)
+        eng.synchronize()
+        t = time.perf_counter()
+        for _ in range(5):
+            eng.run_framework(True)
+        eng.synchronize()
+        fw_us = (time.perf_counter() - t) / 5 * 1e6
         for _ in range(2):
             eng.step(x, y)
         t = time.perf_counter()
@@ -561,6 +575,7 @@ def train_configs(args, dev, world=1, rank=0):
         rec = {"batch_per_gpu": 32, "gpus": world,
                "multi_stream_aot_us": round(multi_us, 2), "single_stream_aot_us": round(single_us, 2),
                "eager_non_aot_us": round(eager_us, 2),
+               "framework_multi_stream_non_aot_us": round(fw_us, 2),
                "images_per_s": round(world * 32 / (multi_us * 1e-6), 1),
                "e2e_images_per_s": round(world * 32 / (e2e_us * 1e-6), 1),
                "multi_over_single": round(single_us / multi_us, 4),

@@ -1176,6 +1176,14 @@ class TrainEngine:
     def synchronize(self):
         N.check(N.lib().sw_engine_synchronize(self._h))
 
+    def run_framework(self, multi: bool = True):
+        """Framework (non-AoT) mode of the training step: the pre_run schedule
+        issued op by op by the host on the logical streams (sim.py:69-80)."""
+        ts = self.schedule if multi else self.schedule_single
+        lens, kinds, args, order = schedule_arrays(ts)
+        N.check(N.lib().sw_engine_run_schedule(self._h, len(ts.streams), N.ptr64(lens), N.ptr32(kinds),
+                                               N.ptr64(args), len(ts.order), N.ptr64(order)))
+
     def device_loss(self) -> float:
         return float(self._dev_view(self.builder.loss, torch.float32)[0].item())
 

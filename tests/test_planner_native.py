@@ -154,3 +154,20 @@ def test_large_chain_is_fast():
     dt = time.perf_counter() - t
     assert f.num_streams == 1 and len(plan) == 0 and len(ts.streams[0]) == n
     assert dt < 2.0  # the reference needs ~2.8 s for assign_streams alone
+
+
+def test_cli_assign_matches_the_reference_bytes(tmp_path):
+    """`python -m paper_2012_02732_b200 assign graph.json` prints the
+    reference's assignment JSON (diamond golden case)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "tests", "golden", "planner_cases.json")) as fh:
+        cases = json.load(fh)["cases"]
+    case = next(c for c in cases if c.get("assign") and c.get("graph"))
+    gp = tmp_path / "g.json"
+    gp.write_text(case["graph"])
+    out = subprocess.run([sys.executable, "-m", "paper_2012_02732_b200", "assign", str(gp)], cwd=root,
+                         capture_output=True, text=True, check=True).stdout.strip()
+    assert out == case["assign"]
