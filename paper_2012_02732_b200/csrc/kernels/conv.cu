@@ -508,10 +508,12 @@ __global__ void __launch_bounds__(256) conv_skinny_kernel(ConvArgs a) {
   if (split > 1) {
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
-    if (cluster.block_rank() == 0 && lane < MB) {
-      float v = red[warp][lane];
-      for (int r = 1; r < split; ++r) v += cluster.map_shared_rank(&red[0][0], r)[warp * MB + lane];
-      red[warp][lane] = v;
+    if (cluster.block_rank() == 0) {
+      for (int m = lane; m < MB; m += 32) {
+        float v = red[warp][m];
+        for (int r = 1; r < split; ++r) v += cluster.map_shared_rank(&red[0][0], r)[warp * MB + m];
+        red[warp][m] = v;
+      }
     }
     cluster.sync();
     if (cluster.block_rank() != 0) return;
