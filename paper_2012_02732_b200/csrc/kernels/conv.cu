@@ -457,23 +457,30 @@ __global__ void __launch_bounds__(256) conv_skinny_kernel(ConvArgs a) {
   for (int ch = c0; ch < c1; ++ch) {
     const int k0 = ch * SK_KC;
     __syncthreads();
-    // stage the im2col rows of the M pixels for k in [k0, k0 + 128)
-    for (int e = threadIdx.x; e < MB * SK_KC; e += 256) {
-      const int m = e / SK_KC, kk = e % SK_KC;
+    // stage the im2col rows of the M pixels for k in [k0, k0 + 128): a thread
+    // owns one k (its (r, s, c) decoded once) and MB/2 pixels, all loads in
+    // flight before the stores (a serial gather loop was latency-bound)
+    {
+      const int kk = threadIdx.x % SK_KC, m0 = threadIdx.x / SK_KC;
       const int k = k0 + kk;
-      float v = 0.f;
-      if (m < a.M && k < a.Kdim) {
-        const int c = k % a.C, rs = k / a.C;
-        const int r = rs / a.S, s2 = rs % a.S;
-        const int q = m % a.Q, t = m / a.Q;
-        const int p = t % a.P, nb = t / a.P;
-        const int ih = p * a.sh - a.ph + r, iw = q * a.sw - a.pw + s2;
-        if ((unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W) {
-          v = __ldg(a.in + nb * a.in_sn + ih * a.in_sh + iw * a.in_sw + c * a.in_sc);
-          if (a.pre_relu) v = fmaxf(v, 0.f);
+      const bool kok = k < a.Kdim;
+      const int c = kok ? k % a.C : 0, rs = kok ? k / a.C : 0;
+      const int r = rs / a.S, s2 = rs % a.S;
+      float v[MB / 2];
+#pragma unroll
+      for (int j = 0; j < MB / 2; ++j) {
+        const int m = m0 + 2 * j;
+        v[j] = 0.f;
+        if (kok && m < a.M) {
+          const int q = m % a.Q, t = m / a.Q;
+          const int p = t % a.P, nb = t / a.P;
+          const int ih = p * a.sh - a.ph + r, iw = q * a.sw - a.pw + s2;
+          if ((unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W)
+            v[j] = __ldg(a.in + nb * a.in_sn + ih * a.in_sh + iw * a.in_sw + c * a.in_sc);
         }
       }
-      xs[m][kk] = v;
+#pragma unroll
+      for (int j = 0; j < MB / 2; ++j) xs[m0 + 2 * j][kk] = a.pre_relu ? fmaxf(v[j], 0.f) : v[j];
     }
     __syncthreads();
     float wv[SK_KC / 32];
