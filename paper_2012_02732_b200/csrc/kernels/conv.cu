@@ -420,124 +420,6 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   }
 }
 
-// Skinny implicit GEMM (variant 10): M <= 64 output pixels (batch-1 layers on
-// 7x7 maps), deep K.  Such layers stream their weights; a GEMM tile of >= 64
-// pixels is mostly padding and its split-K pipeline is latency-bound
-// (ResNet-50 layer4 3x3: 29 µs).  Here a CTA of 8 warps owns 8 output
-// channels (one per warp); the im2col rows of ALL M pixels for a 128-wide K
-// chunk are staged in shared memory once per CTA, each lane walks K with
-// coalesced weight loads and keeps MB pixel accumulators; a warp-shuffle tree
-// folds the lanes at the end.  Split-K over gridDim.y partitions, reduced
-// through a cluster (DSMEM) like the other conv kernels.
-constexpr int SK_KC = 128;
-
-template <int MB>
-__global__ void __launch_bounds__(256) conv_skinny_kernel(ConvArgs a) {
-  __shared__ __align__(16) float xs[MB][SK_KC + 1];
-  __shared__ float red[8][MB];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = blockIdx.x * 8 + warp;
-  const int split = a.split, z = blockIdx.z;
-  const int chunks = (a.Kdim + SK_KC - 1) / SK_KC;
-  const int per = (chunks + split - 1) / split;
-  const int c0 = z * per, c1 = min(chunks, c0 + per);
-  const float* wrow = a.w + (int64_t)min(n, a.K - 1) * a.Kdim;
-  // constants first: this lane's weights of the first chunk
-  float wpre[SK_KC / 32];
-#pragma unroll
-  for (int i = 0; i < SK_KC / 32; ++i) {
-    const int k = c0 * SK_KC + lane + 32 * i;
-    wpre[i] = (c0 < c1 && k < a.Kdim) ? __ldg(wrow + k) : 0.f;
-  }
-  pdl_trigger();
-  pdl_wait();
-  float acc[MB];
-#pragma unroll
-  for (int m = 0; m < MB; ++m) acc[m] = 0.f;
-  for (int ch = c0; ch < c1; ++ch) {
-    const int k0 = ch * SK_KC;
-    __syncthreads();
-    // stage the im2col rows of the M pixels for k in [k0, k0 + 128): a thread
-    // owns one k (its (r, s, c) decoded once) and MB/2 pixels, all loads in
-    // flight before the stores (a serial gather loop was latency-bound)
-    {
-      const int kk = threadIdx.x % SK_KC, m0 = threadIdx.x / SK_KC;
-      const int k = k0 + kk;
-      const bool kok = k < a.Kdim;
-      const int c = kok ? k % a.C : 0, rs = kok ? k / a.C : 0;
-      const int r = rs / a.S, s2 = rs % a.S;
-      float v[MB / 2];
-#pragma unroll
-      for (int j = 0; j < MB / 2; ++j) {
-        const int m = m0 + 2 * j;
-        v[j] = 0.f;
-        if (kok && m < a.M) {
-          const int q = m % a.Q, t = m / a.Q;
-          const int p = t % a.P, nb = t / a.P;
-          const int ih = p * a.sh - a.ph + r, iw = q * a.sw - a.pw + s2;
-          if ((unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W)
-            v[j] = __ldg(a.in + nb * a.in_sn + ih * a.in_sh + iw * a.in_sw + c * a.in_sc);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < MB / 2; ++j) xs[m0 + 2 * j][kk] = a.pre_relu ? fmaxf(v[j], 0.f) : v[j];
-    }
-    __syncthreads();
-    float wv[SK_KC / 32];
-#pragma unroll
-    for (int i = 0; i < SK_KC / 32; ++i) {
-      if (ch == c0) {
-        wv[i] = wpre[i];
-      } else {
-        const int k = k0 + lane + 32 * i;
-        wv[i] = k < a.Kdim ? __ldg(wrow + k) : 0.f;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < SK_KC / 32; ++i) {
-      const int kk = lane + 32 * i;
-#pragma unroll
-      for (int m = 0; m < MB; ++m) acc[m] = fmaf(wv[i], xs[m][kk], acc[m]);
-    }
-  }
-  // fold the 32 lanes of every pixel's partial sum
-#pragma unroll
-  for (int m = 0; m < MB; ++m) {
-    float v = acc[m];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    acc[m] = v;
-  }
-  // split-K: rank 0 of the cluster adds the other ranks' partials (DSMEM)
-  if (lane == 0)
-#pragma unroll
-    for (int m = 0; m < MB; ++m) red[warp][m] = acc[m];
-  if (split > 1) {
-    cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();
-    if (cluster.block_rank() == 0) {
-      for (int m = lane; m < MB; m += 32) {
-        float v = red[warp][m];
-        for (int r = 1; r < split; ++r) v += cluster.map_shared_rank(&red[0][0], r)[warp * MB + m];
-        red[warp][m] = v;
-      }
-    }
-    cluster.sync();
-    if (cluster.block_rank() != 0) return;
-  } else {
-    __syncwarp();
-  }
-  if (n >= a.K) return;
-  // epilogue: lane m writes pixel m of channel n
-  for (int m = lane; m < a.M && m < MB; m += 32) {
-    const int q = m % a.Q, t = m / a.Q;
-    const int p = t % a.P, nb = t / a.P;
-    float v = red[warp][m] + (a.bias ? a.bias[n] : 0.f);
-    if (a.has_res) v += a.res[nb * a.res_sn + p * a.res_sh + q * a.res_sw + n * a.res_sc];
-    a.out[nb * a.out_sn + p * a.out_sh + q * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
-  }
-}
-
 static size_t simt_smem_bytes(int bm, int bn) {
   const size_t tile = 8 * 16 * (size_t)(bm + 4) + 8 * 16 * (size_t)(bn + 4);  // STAGES * BK * (B? + PAD)
   const size_t part = (size_t)bm * bn;
@@ -545,9 +427,6 @@ static size_t simt_smem_bytes(int bm, int bn) {
 }
 
 void init_simt_kernels() {
-  cudaFuncSetAttribute(conv_skinny_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(conv_skinny_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(conv_skinny_kernel<64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_direct_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8 + 128 * (8 + 4)) * 4);
   cudaFuncSetAttribute(conv_direct_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16 + 128 * (16 + 4)) * 4);
   cudaFuncSetAttribute(conv_direct_kernel<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32 + 128 * (32 + 4)) * 4);
@@ -587,13 +466,6 @@ int launch_conv(const sw_op_desc& op, void* stream) {
                       : launch_k(conv_direct_kernel<16, 0>, grid, dim3(128), smem, st, 1, a));
     return (int)(k3 ? launch_k(conv_direct_kernel<32, 3>, grid, dim3(128), smem, st, 1, a)
                     : launch_k(conv_direct_kernel<32, 0>, grid, dim3(128), smem, st, 1, a));
-  }
-  if (op.variant == 10) {
-    if (a.M > 64 || a.split > 16) return (int)cudaErrorInvalidValue;
-    const dim3 grid((unsigned)cdiv(a.K, 8), 1, (unsigned)a.split);
-    if (a.M <= 16) return (int)launch_k(conv_skinny_kernel<16>, grid, dim3(256), 0, st, (unsigned)a.split, a);
-    if (a.M <= 32) return (int)launch_k(conv_skinny_kernel<32>, grid, dim3(256), 0, st, (unsigned)a.split, a);
-    return (int)launch_k(conv_skinny_kernel<64>, grid, dim3(256), 0, st, (unsigned)a.split, a);
   }
   if (op.variant >= 16) return launch_conv_pw(op, op.variant - 16, stream);  // conv1x1.cu (TMA)
   if (op.variant < 0 || op.variant >= kNumSimt) return (int)cudaErrorInvalidValue;

@@ -127,10 +127,6 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
         out.append((K_CONV, 8, 1))
     if K <= 32 and Kdim <= 576 and M >= 1024:
         out.append((K_CONV, 9, 1))  # direct thin-layer kernel (conv.cu conv_direct_kernel)
-    if M <= 64:  # skinny weight-streaming kernel (conv.cu conv_skinny_kernel), split-K clusters
-        for split in (1, 2, 4, 8, 16):
-            if math.ceil(Kdim / 128) >= split and math.ceil(K / 8) * split <= 8 * NUM_SMS:
-                out.append((K_CONV, 10, split))
     ksteps = math.ceil(Kdim / 16)
     for v, (bm, bn) in SIMT_TILES.items():
         ctas = math.ceil(M / bm) * math.ceil(K / bn)
@@ -667,8 +663,6 @@ class Engine:
                 return cd(K * 32 / 256)
             if variant == 9:
                 return cd(M / 128)
-            if variant == 10:
-                return cd(K / 8) * max(1, split)
             bm, bn = PW_TILES[variant] if variant >= 16 else SIMT_TILES[variant]
             return cd(M / bm) * cd(K / bn) * max(1, split)
         if kind == K_CONV_TC:

@@ -572,33 +572,3 @@ def test_compare_matrix_and_framework_mode():
         ("framework", "single"), ("framework", "multi"), ("replay", "single"), ("replay", "multi")]
     assert rep["stream_count"] == eng.assignment.num_streams and rep["replay_multi_over_single"] > 1
     eng.close()
-
-
-@pytest.mark.parametrize("cin,cout,k,s,p,h,batch,split", [
-    (512, 512, 3, 1, 1, 7, 1, 1), (512, 512, 3, 1, 1, 7, 1, 8),    # ResNet-50 layer4 3x3
-    (2048, 512, 1, 1, 0, 7, 1, 16), (1056, 176, 1, 1, 0, 7, 1, 4),  # 1x1 weight streaming
-    (11, 13, 5, 2, 2, 9, 2, 2),                                      # odd channels, padding, M=50
-])
-def test_skinny_conv(cin, cout, k, s, p, h, batch, split):
-    """conv variant 10 (skinny weight-streaming GEMM, M <= 64) forced, with
-    split-K clusters; the conv reads an NHWC activation with ReLU on load."""
-    from paper_2012_02732_b200 import _native as N
-    from paper_2012_02732_b200.engine import K_CONV, SLOT_MULTI, SP_SPLIT_K
-    torch.manual_seed(6)
-    m = nn.Sequential(nn.Conv2d(cin, cin, 1, bias=False), nn.ReLU(),
-                      Conv(cin, cout, k, s, p, bias=True, act=nn.ReLU(), bn=True)).eval()
-    x = torch.randn(batch, cin, h, h)
-    with torch.no_grad():
-        ref = m(x)
-    eng = Engine(m, conv_impl="simt").prepare(x)
-    t = len(eng.program.tasks) - 1
-    assert eng.ops[t].kind == K_CONV
-    eng.ops[t].variant = 10
-    eng.ops[t].params[SP_SPLIT_K] = split
-    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
-    eng._capture(SLOT_MULTI, eng.schedule, False)
-    eng.load_input_device(x)
-    eng.replay(multi=True)
-    eng.synchronize()
-    close(eng.device_output().cpu(), ref)
-    eng.close()
