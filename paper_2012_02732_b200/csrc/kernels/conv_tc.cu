@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   const int per = (ktiles + a.split - 1) / a.split;
   const int kt0 = blockIdx.z * per;
   const int iters = max(0, min(ktiles, kt0 + per) - kt0);
+  probe_begin();
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(smem_u32(&mbar[s]), 1);
@@ -249,8 +250,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)(TC_BM >> 4) << 24);
 
+  probe_pt(1);
   pdl_trigger();
   pdl_wait();
+  probe_pt(2);
 #pragma unroll 1
   for (int st = 0; st < S; ++st) {
     if (st < iters) issue(st, st);
@@ -261,6 +264,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     const int st = it % S;
     cp_wait<S - 2>();  // tile `it` landed (refills run one iteration behind)
     __syncthreads();
+    if (it == 0) probe_pt(3);
     // split the activation tile: hi = tf32(x) in place, lo = x - hi beside it
     {
       float4* hi = reinterpret_cast<float4*>(smem + st * L::STAGE);
@@ -309,6 +313,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     mbar_wait(smem_u32(&mbar[last % S]), (last / S) & 1);
   }
   tc_fence_after();
+  probe_pt(4);
 
   // TMEM → smem tile (rows = TMEM lanes) → one rolled epilogue loop, shared
   // with the split-K DSMEM reduction
@@ -329,8 +334,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     for (int j = 0; j < 16; j += 4)
       *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
+  probe_pt(5);
   cg::cluster_group cluster = cg::this_cluster();
   tile_epilogue<TC_BM, BN, TC_THREADS>(a.epi, part, m0, n0, a.split, cluster);
+  probe_pt(6);
 
   tc_fence_before();
   __syncthreads();
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)L::NCOLS)
                  : "memory");
   }
+  probe_end();
 }
 
 // ---------------------------------------------------------------------------
