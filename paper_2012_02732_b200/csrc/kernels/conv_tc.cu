@@ -106,6 +106,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr + 16));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
@@ -201,10 +220,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
 
   // cp.async of K tile `kt` (slice-relative) into stage `st`: A raw → A_hi slot,
   // W_hi / W_lo → B slots
-  auto issue = [&](int kt, int st) {
+  // part: 1 = activations (A), 2 = weights (B, constants), 3 = both
+  auto issue = [&](int kt, int st, int part) {
     const uint32_t stage = sbase + st * L::STAGE;
     const int k = (kt0 + kt) * TC_BK + chunk * 4;
-    if (a.vec) {
+    if (!(part & 1)) {
+      // weights only
+    } else if (a.vec) {
       const bool kin = k < a.Kdim;
       const int c = k % a.C;
       const int rs = k / a.C;
@@ -233,6 +255,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
         }
       }
     }
+    if (!(part & 2)) return;
     const uint32_t b_hi = stage + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
 #pragma unroll
     for (int i = 0; i < B_ROWS; ++i) {
@@ -250,13 +273,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)(TC_BM >> 4) << 24);
 
+  // the first stages' weights (constants) are requested before the PDL wait,
+  // the activations after it; stage s's cp.async group then holds A_s (and
+  // group 0 also every prologue B), so the per-stage waits stay correct
+#pragma unroll 1
+  for (int st = 0; st < S; ++st)
+    if (st < iters) issue(st, st, 2);
   probe_pt(1);
   pdl_trigger();
   pdl_wait();
   probe_pt(2);
 #pragma unroll 1
   for (int st = 0; st < S; ++st) {
-    if (st < iters) issue(st, st);
+    if (st < iters) issue(st, st, 1);
     cp_commit();
   }
 #pragma unroll 1
@@ -304,7 +333,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     if (it >= 1 && it - 1 + S < iters) {
       const int ps = (it - 1) % S;
       mbar_wait(smem_u32(&mbar[ps]), ((it - 1) / S) & 1);
-      issue(it - 1 + S, ps);
+      issue(it - 1 + S, ps, 3);
     }
     cp_commit();
   }
@@ -322,16 +351,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   float* part = reinterpret_cast<float*>(smem);  // [128][BN]; operands are dead now
   __syncthreads();
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    float v[16];
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    // two 16-column TMEM loads in flight per wait (BN >= 32)
+    float v[32];
     if (iters > 0) {
-      tmem_ld16(t_row + c0, v);
+      tmem_ld16x2(t_row + c0, v);
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
     }
 #pragma unroll
-    for (int j = 0; j < 16; j += 4)
+    for (int j = 0; j < 32; j += 4)
       *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
   probe_pt(5);
@@ -489,16 +519,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   float* part = reinterpret_cast<float*>(smem);
   __syncthreads();
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    float v[16];
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    // two 16-column TMEM loads in flight per wait (BN >= 32)
+    float v[32];
     if (iters > 0) {
-      tmem_ld16(t_row + c0, v);
+      tmem_ld16x2(t_row + c0, v);
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
     }
 #pragma unroll
-    for (int j = 0; j < 16; j += 4)
+    for (int j = 0; j < 32; j += 4)
       *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
   cg::cluster_group cluster = cg::this_cluster();
