@@ -278,6 +278,10 @@ int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 /* ---- training step (paper_2012_02732_b200/train.py) ---- */
 /* One more captured H2D copy in the with_io slots (labels next to images). */
 int sw_engine_add_input(sw_engine* e, uint64_t host, uint64_t dev, int64_t bytes);
+/* Per-task launch priority for subsequent captures / launches: one int32
+ * urgency level per op (0 = default, k > 0 = k steps above the default in the
+ * device's stream-priority range, clamped); n = 0 clears. */
+int sw_engine_set_priorities(sw_engine* e, int64_t n, const int32_t* prio);
 /* Device range warmed into L2 by SW_ENGINE_L2_PREFETCH captures. */
 int sw_engine_set_prefetch(sw_engine* e, uint64_t dev, int64_t bytes);
 /* Bind NCCL at run time (dlopen of `path`, or "libnccl.so.2" when NULL/empty). */

@@ -44,6 +44,9 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 // Engine-controlled launch flags (set around capture / eager launches).
 extern thread_local bool g_launch_pdl;
+// Per-task execution priority (cudaLaunchAttributePriority, 0 = default;
+// the engine raises the critical-path tasks of the schedule).
+extern thread_local int g_launch_priority;
 
 // Single launch path for every kernel: optional cluster (split-K along z)
 // and the PDL attribute.
@@ -55,8 +58,13 @@ inline cudaError_t launch_k(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t 
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   unsigned n = 0;
+  if (g_launch_priority != 0) {
+    attr[n].id = cudaLaunchAttributePriority;
+    attr[n].val.priority = g_launch_priority;
+    ++n;
+  }
   if (cluster_z > 1) {
     attr[n].id = cudaLaunchAttributeClusterDimension;
     attr[n].val.clusterDim.x = 1;

@@ -72,6 +72,7 @@ extern "C" int sw_probe_read(uint64_t* out) {
 
 namespace sw {
 thread_local bool g_launch_pdl = false;
+thread_local int g_launch_priority = 0;
 }
 
 namespace {
@@ -110,6 +111,7 @@ struct sw_engine {
   cudaEvent_t fork = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   std::vector<sw_op_desc> ops;
+  std::vector<int32_t> prio;  // per-task launch priority (sw_engine_set_priorities)
   uint64_t host_in = 0, dev_in = 0, host_out = 0, dev_out = 0;
   int64_t in_bytes = 0, out_bytes = 0;
   uint32_t flags = 0;  // SW_ENGINE_PDL | SW_ENGINE_NULL_KERNELS
@@ -164,7 +166,18 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
 
+int launch_task_impl(sw_engine* e, const sw_op_desc& op, cudaStream_t st);
+
+// priority of the task being launched: set around the kernel launcher
 int launch_task(sw_engine* e, const sw_op_desc& op, cudaStream_t st) {
+  const int64_t t = &op - e->ops.data();
+  sw::g_launch_priority = (t >= 0 && t < (int64_t)e->prio.size()) ? e->prio[t] : 0;
+  const int rc = launch_task_impl(e, op, st);
+  sw::g_launch_priority = 0;
+  return rc;
+}
+
+int launch_task_impl(sw_engine* e, const sw_op_desc& op, cudaStream_t st) {
   int rc = 0;
   switch (op.kind) {
     case sw::K_BN_STATS:
@@ -707,6 +720,16 @@ int sw_engine_set_prefetch(sw_engine* e, uint64_t dev, int64_t bytes) {
   }
   e->prefetch_ptr = dev;
   e->prefetch_bytes = bytes;
+  return SW_OK;
+}
+
+int sw_engine_set_priorities(sw_engine* e, int64_t n, const int32_t* prio) {
+  if (n != (int64_t)e->ops.size() && n != 0) return sw::fail(SW_VALUE_ERROR, "one priority per task");
+  int least = 0, greatest = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  // level k > 0 → k steps more urgent than the default, clamped to the device range
+  e->prio.resize(n);
+  for (int64_t i = 0; i < n; ++i) e->prio[i] = prio[i] > 0 ? std::max(greatest, least - prio[i]) : 0;
   return SW_OK;
 }
 

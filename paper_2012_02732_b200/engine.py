@@ -677,6 +677,36 @@ class Engine:
             return p[SP_N] * max(1, split)
         return 1
 
+    def critical_path_priorities(self, levels: int = 1, reps: int = 5):
+        """Raise the launch priority of the tasks on the schedule's critical
+        path (measured per-task durations, longest path through the DAG), so
+        the block scheduler serves them first when concurrent branches compete
+        for SMs.  `levels` = urgency steps given to zero-slack tasks."""
+        per = self.profile_tasks(reps=reps)
+        n = len(self.program.tasks)
+        preds = {t: set() for t in range(n)}
+        succs = {t: set() for t in range(n)}
+        for u, v in self.graph.edges:
+            preds[v].add(u)
+            succs[u].add(v)
+        order = [t.tid for t in self.program.tasks]  # fx order is topological
+        est = {}
+        for t in order:
+            est[t] = max((est[u] + per[u] for u in preds[t]), default=0.0)
+        total = max(est[t] + per[t] for t in order)
+        lft = {}
+        for t in reversed(order):
+            lft[t] = min((lft[v] - per[v] for v in succs[t]), default=total)
+        slack = {t: lft[t] - (est[t] + per[t]) for t in order}
+        prio = np.array([levels if slack[t] <= 0.05 * per[t] + 0.5 else 0 for t in range(n)], dtype=np.int32)
+        N.check(N.lib().sw_engine_set_priorities(self._h, n, N.ptr32(prio)))
+        self.recapture()
+        return {"critical_tasks": int((prio > 0).sum()), "critical_path_us": round(total, 2)}
+
+    def clear_priorities(self):
+        N.check(N.lib().sw_engine_set_priorities(self._h, 0, N.ptr32(np.zeros(1, dtype=np.int32))))
+        self.recapture()
+
     def refine_graph(self, caps=(None, 592, 296, 148), iters: int = 100):
         """Graph-level kernel selection: the per-task autotuner times every
         candidate alone, but in the multi-stream replay kernels share the GPU.
