@@ -689,7 +689,13 @@ class Engine:
         for u, v in self.graph.edges:
             preds[v].add(u)
             succs[u].add(v)
-        order = [t.tid for t in self.program.tasks]  # fx order is topological
+        indeg = {t: len(preds[t]) for t in range(n)}
+        order = [t for t in range(n) if indeg[t] == 0]
+        for t in order:  # Kahn; the list grows while it is walked
+            for v in succs[t]:
+                indeg[v] -= 1
+                if indeg[v] == 0:
+                    order.append(v)
         est = {}
         for t in order:
             est[t] = max((est[u] + per[u] for u in preds[t]), default=0.0)
