@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(256) io_copy_kernel(const float4* __restrict__
 static void io_geometry(int64_t bytes, int64_t* n16, int* tail, unsigned* blocks) {
   *n16 = bytes / 16;
   *tail = (int)((bytes % 16) / 4);
-  int64_t b = cdiv(*n16, 256 * 4);
+  int64_t b = cdiv(*n16, 256);  // one float4 per thread: PCIe reads spread over every SM
   if (b < 1) b = 1;
   if (b > 148 * 4) b = 148 * 4;
   *blocks = (unsigned)b;
@@ -348,14 +348,13 @@ int launch_l2_prefetch(const void* p, int64_t bytes, void* stream) {
 int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream) {
   if (bytes <= 0) return 0;
   if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return (int)cudaErrorMisalignedAddress;
-  const int64_t n16 = bytes / 16;
-  const int tail = (int)((bytes % 16) / 4);
+  int64_t n16;
+  int tail;
+  unsigned blocks;
+  io_geometry(bytes, &n16, &tail, &blocks);
   const float* st = reinterpret_cast<const float*>(src) + n16 * 4;
   float* dt = reinterpret_cast<float*>(dst) + n16 * 4;
-  int64_t blocks = cdiv(n16, 256 * 4);
-  if (blocks < 1) blocks = 1;
-  if (blocks > 148 * 4) blocks = 148 * 4;
-  return (int)launch_k(io_copy_kernel, dim3((unsigned)blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
+  return (int)launch_k(io_copy_kernel, dim3(blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1,
                        reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), n16, st, dt, tail);
 }
 

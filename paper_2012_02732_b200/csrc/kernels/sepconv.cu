@@ -10,7 +10,7 @@
 // depthwise tile per column block, a large BN the opposite):
 //   1. cp.async of the pointwise weights (stored [C][K]) the tile needs and of the whole
 //      depthwise filter, issued before the PDL wait (constants);
-//   2. depthwise for all C_in channels of the BM pixels into smem D[c][px]
+//   2. depthwise for all C_in channels of the BM pixels into smem D[px][c] (rows padded by 4 floats)
 //      (branch-free unrolled taps, 128-bit NHWC loads, filter from smem);
 //   3. pointwise GEMM D^T x W, TM x TN micro-tile per thread;
 //   4. shared float4 tile epilogue (bias, residual, activation, strided store).
@@ -108,8 +108,9 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   const int Cp = (a.C + SEP_BK - 1) / SEP_BK * SEP_BK;
   const int RR = KS ? KS : a.R;
   const int SS = KS ? KS : a.S;
-  float* D = smem;                  // [BM][Cp]   depthwise tile, channels contiguous
-  float* Bs = D + Cp * BM;          // [Cp][BN]   pointwise weights, columns contiguous
+  const int DS = Cp + 4;            // D row stride: 4 consecutive rows hit 4 distinct bank quads
+  float* D = smem;                  // [BM][DS]   depthwise tile, channels contiguous
+  float* Bs = D + DS * BM;          // [Cp][BN]   pointwise weights, columns contiguous
   float* Wd = Bs + Cp * BN;         // [RR*SS][Cp]
   const int tid = threadIdx.x;
   const int m0 = blockIdx.x * BM;
@@ -213,10 +214,10 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
 #pragma unroll
       for (int j = 0; j < PX; ++j) {
         if constexpr (VEC) {
-          *reinterpret_cast<float4*>(&D[(px0 + j) * Cp + c]) = make_float4(acc[j][0], acc[j][1 % V], acc[j][2 % V],
+          *reinterpret_cast<float4*>(&D[(px0 + j) * DS + c]) = make_float4(acc[j][0], acc[j][1 % V], acc[j][2 % V],
                                                                           acc[j][3 % V]);
         } else {
-          D[(px0 + j) * Cp + c] = acc[j][0];
+          D[(px0 + j) * DS + c] = acc[j][0];
         }
       }
     }
@@ -276,15 +277,21 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
       for (int j = 0; j < V; ++j) acc[j] = apply_act(acc[j] + (a.b_dw ? a.b_dw[c + j] : 0.f), a.dw_act);
     }
     if constexpr (VEC) {
-      *reinterpret_cast<float4*>(&D[px * Cp + c]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      *reinterpret_cast<float4*>(&D[px * DS + c]) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     } else {
-      D[px * Cp + c] = acc[0];
+      D[px * DS + c] = acc[0];
     }
   }
   __syncthreads();
   probe_pt(4);
 
-  // ---- pointwise GEMM: out[px][n] = sum_c D[c][px] * W[n][c] ----
+  // ---- pointwise GEMM: out[px][n] = sum_c D[px][c] * W[c][n] ----
+  // Thread (ty, tx) owns pixel rows ty + i * RS (interleaved, so the 4 row
+  // groups of a warp read 4 consecutive padded rows: conflict-free float4
+  // loads) and columns tx * TN + j.  Four channels per step: TM float4 loads
+  // of D and 4 rows of TN weights feed 4 * TM * TN FMAs (the scalar loop was
+  // shared-memory bound at batch 256: 20 wavefronts per 16 FMAs).
+  constexpr int RS = BM / TM;
   const int ty = tid / (BN / TN);
   const int tx = tid % (BN / TN);
   float o[TM][TN];
@@ -292,28 +299,42 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) o[i][j] = 0.f;
-  const float* at = D + ty * TM * Cp;
+  const float* at = D + ty * DS;
   const float* bt = Bs + tx * TN;
-#pragma unroll 4
-  for (int k = 0; k < Cp; ++k) {
-    float av[TM], bv[TN];
+#pragma unroll 2
+  for (int k = 0; k < Cp; k += 4) {
+    float4 av[TM];
 #pragma unroll
-    for (int i = 0; i < TM; ++i) av[i] = at[i * Cp + k];
+    for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const float4*>(&at[i * RS * DS + k]);
 #pragma unroll
-    for (int j = 0; j < TN; ++j) bv[j] = bt[k * BN + j];
+    for (int kk = 0; kk < 4; ++kk) {
+      float bv[TN];
+      if constexpr (TN % 4 == 0) {
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+        for (int j = 0; j < TN; j += 4) {
+          const float4 b4 = *reinterpret_cast<const float4*>(&bt[(k + kk) * BN + j]);
+          bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+        }
+      } else {
 #pragma unroll
-      for (int j = 0; j < TN; ++j) o[i][j] = fmaf(av[i], bv[j], o[i][j]);
+        for (int j = 0; j < TN; ++j) bv[j] = bt[(k + kk) * BN + j];
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const float a_ = kk == 0 ? av[i].x : kk == 1 ? av[i].y : kk == 2 ? av[i].z : av[i].w;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) o[i][j] = fmaf(a_, bv[j], o[i][j]);
+      }
+    }
   }
   __syncthreads();  // D / Bs reads done; reuse D as the output tile
   probe_pt(5);
 
-  float* part = D;  // [BM][BN] ≤ Cp*BM + Cp*BN floats
+  float* part = D;  // [BM][BN] ≤ DS*BM + Cp*BN floats
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) part[(ty * TM + i) * BN + tx * TN + j] = o[i][j];
+    for (int j = 0; j < TN; ++j) part[(ty + i * RS) * BN + tx * TN + j] = o[i][j];
   cg::cluster_group cluster = cg::this_cluster();
   tile_epilogue<BM, BN, SEP_THREADS>(a.epi, part, m0, n0, 1, cluster);
   probe_end();
@@ -597,7 +618,7 @@ constexpr int kSepSmemMax = 227 * 1024;
 
 static size_t sep_smem(int C, int R, int S, int bm, int bn) {
   const size_t cp = (size_t)(C + SEP_BK - 1) / SEP_BK * SEP_BK;
-  const size_t body = cp * bm + cp * bn + (size_t)R * S * cp;
+  const size_t body = (cp + 4) * bm + cp * bn + (size_t)R * S * cp;  // D rows padded by 4
   const size_t part = (size_t)bm * bn;  // epilogue tile reuses the same buffer
   return 4 * (body > part ? body : part);
 }

@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <dlfcn.h>
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
 
 #include <chrono>
 #include <cstdio>
@@ -76,6 +79,20 @@ thread_local int g_launch_priority = 0;
 }
 
 namespace {
+
+// SW_SEGV_TRACE=1: print the native stack of a segmentation fault (debugging aid)
+void segv_trace(int sig) {
+  void* fr[64];
+  const int n = backtrace(fr, 64);
+  backtrace_symbols_fd(fr, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+struct SegvTraceInit {
+  SegvTraceInit() {
+    if (getenv("SW_SEGV_TRACE")) signal(SIGSEGV, segv_trace);
+  }
+} segv_trace_init;
 
 constexpr int kSlots = 4;
 
@@ -170,8 +187,17 @@ int launch_task_impl(sw_engine* e, const sw_op_desc& op, cudaStream_t st);
 
 // priority of the task being launched: set around the kernel launcher
 int launch_task(sw_engine* e, const sw_op_desc& op, cudaStream_t st) {
-  const int64_t t = &op - e->ops.data();
-  sw::g_launch_priority = (t >= 0 && t < (int64_t)e->prio.size()) ? e->prio[t] : 0;
+  // `op` may be a caller-owned trial descriptor (sw_engine_time_op): compare
+  // addresses as integers (pointer subtraction across objects is undefined
+  // and was miscompiled into an unchecked load)
+  const uintptr_t base = reinterpret_cast<uintptr_t>(e->ops.data());
+  const uintptr_t at = reinterpret_cast<uintptr_t>(&op);
+  int prio = 0;
+  if (!e->prio.empty() && at >= base) {
+    const uintptr_t t = (at - base) / sizeof(sw_op_desc);
+    if (t < e->prio.size() && at == base + t * sizeof(sw_op_desc)) prio = e->prio[t];
+  }
+  sw::g_launch_priority = prio;
   const int rc = launch_task_impl(e, op, st);
   sw::g_launch_priority = 0;
   return rc;

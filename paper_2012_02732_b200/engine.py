@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass
 
@@ -163,7 +164,8 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
             if split > 1 and (ktiles // split < 1 or ctas * split > 2 * NUM_SMS):
                 continue
             out.append((K_CONV_TC, bn, split))
-            if pointwise:  # TMA-fed tcgen05 kernel (conv_tc.cu); refuses strided / unaligned layouts
+            # TMA-fed tcgen05 kernel (conv_tc.cu); refuses strided / unaligned layouts
+            if pointwise:
                 out.append((K_CONV_TC, 1000 + bn, split))
     return out
 
@@ -440,6 +442,8 @@ def roofline_us(t: Task, hbm_gbs: float, tflops: float) -> float:
 # Engine
 # ----------------------------------------------------------------------------
 
+_DEBUG_TUNE = bool(os.environ.get("SW_DEBUG_TUNE"))
+
 class Engine:
     """Nimble-style AoT engine around a static ``nn.Module`` (eval mode, fp32)."""
 
@@ -639,6 +643,8 @@ class Engine:
                 trial.kind = kind
                 trial.variant = variant
                 trial.params[SP_SPLIT_K] = split
+                if _DEBUG_TUNE:
+                    print(f"autotune task {t.tid} {t.name}: kind {kind} variant {variant} split {split}", flush=True)
                 rc = lib.sw_engine_time_op(self._h, C.byref(trial), reps, C.byref(us))
                 self.tuning_log.setdefault(t.tid, []).append(
                     (kind, variant, split, us.value if rc == 0 else None,

@@ -1,0 +1,72 @@
+// H2D staging microbenchmark: a kernel reading pinned host memory through its
+// UVA mapping (the engine's io_copy node) at several grid shapes vs DMA.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/io_bench tools/io_bench.cu && /tmp/io_bench
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+
+template <int U>
+__global__ void copy_k(const float4* __restrict__ s, float4* __restrict__ d, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = s[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < U; ++u) d[i + u * stride] = v[u];
+  }
+  for (; i < n; i += stride) d[i] = s[i];
+}
+
+template <int U>
+float run(const float4* h, float4* dd, int64_t n, int blocks, int threads, cudaStream_t st) {
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  for (int r = 0; r < 20; ++r) copy_k<U><<<blocks, threads, 0, st>>>(h, dd, n);
+  cudaStreamEndCapture(st, &g);
+  cudaGraphInstantiate(&ge, g, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int w = 0; w < 3; ++w) cudaGraphLaunch(ge, st);
+  cudaEventRecord(a, st);
+  for (int it = 0; it < 20; ++it) cudaGraphLaunch(ge, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  return ms * 1000.f / 400.f;
+}
+
+int main() {
+  const int64_t bytes = 602112, n = bytes / 16;
+  float4 *h, *dd;
+  cudaMallocHost(&h, bytes);
+  cudaMalloc(&dd, bytes);
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  const int grids[] = {37, 74, 148, 296, 592, 1184};
+  const int thr[] = {128, 256, 512};
+  for (int t : thr)
+    for (int gsz : grids) {
+      printf("threads %3d blocks %4d : U1 %6.2f us  U4 %6.2f us  U8 %6.2f us\n", t, gsz,
+             run<1>(h, dd, n, gsz, t, st), run<4>(h, dd, n, gsz, t, st), run<8>(h, dd, n, gsz, t, st));
+    }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int w = 0; w < 5; ++w) cudaMemcpyAsync(dd, h, bytes, cudaMemcpyHostToDevice, st);
+  cudaEventRecord(a, st);
+  for (int it = 0; it < 100; ++it) cudaMemcpyAsync(dd, h, bytes, cudaMemcpyHostToDevice, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("DMA cudaMemcpyAsync back-to-back: %.2f us per copy (%.1f GB/s)\n", ms * 10.f, bytes / (ms * 10.f) / 1e3);
+  printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
