@@ -102,13 +102,13 @@ __device__ __forceinline__ void dw_row_block(const SepArgs& a, const float* base
 }
 
 template <int KS, bool VEC, int BM, int BN, int TM, int TN, int PX = 1>
-__global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
+__global__ void __launch_bounds__(SEP_THREADS, PX > 1 ? 3 : 0) sepconv_kernel(SepArgs a) {
   static_assert((BM / TM) * (BN / TN) == SEP_THREADS, "256 threads");
   extern __shared__ __align__(16) float smem[];
   const int Cp = (a.C + SEP_BK - 1) / SEP_BK * SEP_BK;
   const int RR = KS ? KS : a.R;
   const int SS = KS ? KS : a.S;
-  const int DS = Cp + 4;            // D row stride: 4 consecutive rows hit 4 distinct bank quads
+  const int DS = PX > 1 ? Cp + 4 : Cp;  // D row stride (padded: 4 consecutive rows hit 4 distinct bank quads)
   float* D = smem;                  // [BM][DS]   depthwise tile, channels contiguous
   float* Bs = D + DS * BM;          // [Cp][BN]   pointwise weights, columns contiguous
   float* Wd = Bs + Cp * BN;         // [RR*SS][Cp]
@@ -286,12 +286,6 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   probe_pt(4);
 
   // ---- pointwise GEMM: out[px][n] = sum_c D[px][c] * W[c][n] ----
-  // Thread (ty, tx) owns pixel rows ty + i * RS (interleaved, so the 4 row
-  // groups of a warp read 4 consecutive padded rows: conflict-free float4
-  // loads) and columns tx * TN + j.  Four channels per step: TM float4 loads
-  // of D and 4 rows of TN weights feed 4 * TM * TN FMAs (the scalar loop was
-  // shared-memory bound at batch 256: 20 wavefronts per 16 FMAs).
-  constexpr int RS = BM / TM;
   const int ty = tid / (BN / TN);
   const int tx = tid % (BN / TN);
   float o[TM][TN];
@@ -299,32 +293,54 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) o[i][j] = 0.f;
-  const float* at = D + ty * DS;
   const float* bt = Bs + tx * TN;
+  // large tiles (PX > 1, batch >= 8): thread (ty, tx) owns pixel rows
+  // ty + i * RS (interleaved, so the 4 row groups of a warp read 4
+  // consecutive padded rows: conflict-free float4 loads); four channels per
+  // step feed 4 * TM * TN FMAs.  Small tiles (batch 1) keep the scalar loop
+  // over rows ty * TM + i, which measured faster there.
+  constexpr int RS = PX > 1 ? BM / TM : 1;
+  const int row0 = PX > 1 ? ty : ty * TM;
+  const float* at = D + row0 * DS;
+  if constexpr (PX > 1) {
 #pragma unroll 2
-  for (int k = 0; k < Cp; k += 4) {
-    float4 av[TM];
+    for (int k = 0; k < Cp; k += 4) {
+      float4 av[TM];
 #pragma unroll
-    for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const float4*>(&at[i * RS * DS + k]);
+      for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const float4*>(&at[i * RS * DS + k]);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      float bv[TN];
-      if constexpr (TN % 4 == 0) {
+      for (int kk = 0; kk < 4; ++kk) {
+        float bv[TN];
+        if constexpr (TN % 4 == 0) {
 #pragma unroll
-        for (int j = 0; j < TN; j += 4) {
-          const float4 b4 = *reinterpret_cast<const float4*>(&bt[(k + kk) * BN + j]);
-          bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+          for (int j = 0; j < TN; j += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(&bt[(k + kk) * BN + j]);
+            bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < TN; ++j) bv[j] = bt[(k + kk) * BN + j];
         }
-      } else {
 #pragma unroll
-        for (int j = 0; j < TN; ++j) bv[j] = bt[(k + kk) * BN + j];
+        for (int i = 0; i < TM; ++i) {
+          const float a_ = kk == 0 ? av[i].x : kk == 1 ? av[i].y : kk == 2 ? av[i].z : av[i].w;
+#pragma unroll
+          for (int j = 0; j < TN; ++j) o[i][j] = fmaf(a_, bv[j], o[i][j]);
+        }
       }
+    }
+  } else {
+#pragma unroll 4
+    for (int k = 0; k < Cp; ++k) {
+      float av[TM], bv[TN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const float a_ = kk == 0 ? av[i].x : kk == 1 ? av[i].y : kk == 2 ? av[i].z : av[i].w;
+      for (int i = 0; i < TM; ++i) av[i] = at[i * DS + k];
 #pragma unroll
-        for (int j = 0; j < TN; ++j) o[i][j] = fmaf(a_, bv[j], o[i][j]);
-      }
+      for (int j = 0; j < TN; ++j) bv[j] = bt[k * BN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) o[i][j] = fmaf(av[i], bv[j], o[i][j]);
     }
   }
   __syncthreads();  // D / Bs reads done; reuse D as the output tile
@@ -334,7 +350,7 @@ __global__ void __launch_bounds__(SEP_THREADS) sepconv_kernel(SepArgs a) {
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) part[(ty + i * RS) * BN + tx * TN + j] = o[i][j];
+    for (int j = 0; j < TN; ++j) part[(row0 + i * RS) * BN + tx * TN + j] = o[i][j];
   cg::cluster_group cluster = cg::this_cluster();
   tile_epilogue<BM, BN, SEP_THREADS>(a.epi, part, m0, n0, 1, cluster);
   probe_end();
