@@ -151,12 +151,12 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;  // fp32 per stage row = 8 chunks of 16 B = 4 MMA K-steps
 constexpr int TC_THREADS = 128;
 
-template <int BN>
+template <int BN, int SOVR = 0>
 struct TcSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 4;
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
-  static constexpr int STAGES = (BN <= 64) ? 4 : (BN == 128 ? 3 : 2);
+  static constexpr int STAGES = SOVR ? SOVR : (BN <= 64) ? 4 : (BN == 128 ? 3 : 2);
   static constexpr int OPER = STAGES * STAGE;
   static constexpr int PART = TC_BM * BN * 4;
   static constexpr int BODY = OPER > PART ? OPER : PART;
@@ -396,11 +396,13 @@ struct TcMaps {
   CUtensorMap a, bh, bl;
 };
 
-template <int BN>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// SOVR > 0: a shallower ring (SOVR stages) so that two CTAs share an SM and
+// one CTA's prologue / epilogue overlaps the other's TMA stream (large M).
+template <int BN, int SOVR = 0>
+__global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
     conv_tc_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                        const __grid_constant__ CUtensorMap tbl, TcArgs a) {
-  using L = TcSmem<BN>;
+  using L = TcSmem<BN, SOVR>;
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BODY);
@@ -576,7 +578,7 @@ static TcArgs tc_args(const sw_op_desc& op) {
 }
 
 // variant = N tile (32, 64, 128, 256); SP_SPLIT_K = cluster split along K.
-template <int BN>
+template <int BN, int SOVR = 0>
 static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st) {
   // 1x1 / stride 1 / no padding on 16-B aligned NHWC rows only
   if (a.R != 1 || a.S != 1 || a.sh != 1 || a.sw != 1 || a.ph != 0 || a.pw != 0 || !a.vec)
@@ -597,7 +599,7 @@ static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st)
     if (!encode_tmap_f32(&tbl, a.w_lo, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), (unsigned)cdiv(a.K, BN), (unsigned)a.split);
-  return (int)launch_k(conv_tc_tma_kernel<BN>, grid, dim3(TC_THREADS), (size_t)TcSmem<BN>::TOTAL, st,
+  return (int)launch_k(conv_tc_tma_kernel<BN, SOVR>, grid, dim3(TC_THREADS), (size_t)TcSmem<BN, SOVR>::TOTAL, st,
                        (unsigned)a.split, ta, tbh, tbl, a);
 }
 
@@ -612,6 +614,9 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
     case 1064: return launch_tc_tma<64>(a, op, st);
     case 1128: return launch_tc_tma<128>(a, op, st);
     case 1256: return launch_tc_tma<256>(a, op, st);
+    // 2000 + BN: two stages, two CTAs per SM
+    case 2032: return launch_tc_tma<32, 2>(a, op, st);
+    case 2064: return launch_tc_tma<64, 2>(a, op, st);
     default: break;
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), 1, (unsigned)a.split);
@@ -639,6 +644,10 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
 
 // Pre-set the dynamic smem limits outside any stream capture.
 void init_tc_kernels() {
+  cudaFuncSetAttribute(conv_tc_tma_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32, 2>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<32, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<64, 2>::TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_kernel<64, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32>::TOTAL);
   cudaFuncSetAttribute(conv_tc_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32>::TOTAL);
