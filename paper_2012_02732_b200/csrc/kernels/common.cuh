@@ -103,10 +103,12 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 
-template <int BM, int BN, int NT, typename Cluster>
+// PS = row stride of the tile in floats (BN, or BN + 4 where the producer
+// writes one row per lane: the padding makes those float4 stores conflict-free)
+template <int BM, int BN, int NT, int PS = BN, typename Cluster>
 __device__ __forceinline__ void tile_epilogue(const Epi& ep, const float* part, int m0, int n0, int split,
                                               Cluster& cluster) {
-  static_assert(BN % 4 == 0, "channel groups of 4");
+  static_assert(BN % 4 == 0 && PS % 4 == 0, "channel groups of 4");
   constexpr int GPR = BN / 4;  // groups per row
   constexpr int G = BM * GPR;
   int g0 = 0, g1 = G, nr = 1;
@@ -124,14 +126,15 @@ __device__ __forceinline__ void tile_epilogue(const Epi& ep, const float* part, 
     const int m = m0 + g / GPR, n = n0 + (g % GPR) * 4;
     if (m >= ep.M || n >= ep.K) continue;
     float4 v;
+    const int gi = PS == BN ? g : (g / GPR) * (PS / 4) + g % GPR;  // float4 index in the tile
     if (nr == 1) {
-      v = reinterpret_cast<const float4*>(part)[g];
+      v = reinterpret_cast<const float4*>(part)[gi];
     } else {
       v = make_float4(0.f, 0.f, 0.f, 0.f);
       float4 t[16];  // up to 16 ranks (non-portable cluster size)
 #pragma unroll
       for (int r = 0; r < 16; ++r)
-        if (r < nr) t[r] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, r))[g];
+        if (r < nr) t[r] = reinterpret_cast<const float4*>(cluster.map_shared_rank(part, r))[gi];
 #pragma unroll
       for (int r = 0; r < 16; ++r)
         if (r < nr) v = f4add(v, t[r]);

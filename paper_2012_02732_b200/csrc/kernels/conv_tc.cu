@@ -158,7 +158,8 @@ struct TcSmem {
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
   static constexpr int STAGES = SOVR ? SOVR : (BN <= 64) ? 4 : (BN == 128 ? 3 : 2);
   static constexpr int OPER = STAGES * STAGE;
-  static constexpr int PART = TC_BM * BN * 4;
+  static constexpr int PS = BN + 4;  // epilogue tile row stride (floats): conflict-free row-per-lane stores
+  static constexpr int PART = TC_BM * PS * 4;
   static constexpr int BODY = OPER > PART ? OPER : PART;
   static constexpr int TOTAL = BODY + 128;  // + mbarriers + tmem slot
   static constexpr int NCOLS = BN < 32 ? 32 : BN;
@@ -362,11 +363,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < 32; j += 4)
-      *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      *reinterpret_cast<float4*>(&part[row * L::PS + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
   probe_pt(5);
   cg::cluster_group cluster = cg::this_cluster();
-  tile_epilogue<TC_BM, BN, TC_THREADS>(a.epi, part, m0, n0, a.split, cluster);
+  tile_epilogue<TC_BM, BN, TC_THREADS, L::PS>(a.epi, part, m0, n0, a.split, cluster);
   probe_pt(6);
 
   tc_fence_before();
@@ -532,10 +533,10 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
     }
 #pragma unroll
     for (int j = 0; j < 32; j += 4)
-      *reinterpret_cast<float4*>(&part[row * BN + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      *reinterpret_cast<float4*>(&part[row * L::PS + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
   }
   cg::cluster_group cluster = cg::this_cluster();
-  tile_epilogue<TC_BM, BN, TC_THREADS>(a.epi, part, m0, n0, a.split, cluster);
+  tile_epilogue<TC_BM, BN, TC_THREADS, L::PS>(a.epi, part, m0, n0, a.split, cluster);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
