@@ -23,6 +23,8 @@
 //    every CTA of a batch-1 layer starts on a cold SM.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "tma.cuh"
 
@@ -162,6 +164,9 @@ struct TcSmem {
   static constexpr int PART = TC_BM * PS * 4;
   static constexpr int BODY = OPER > PART ? OPER : PART;
   static constexpr int TOTAL = BODY + 128;  // + mbarriers + tmem slot
+  // persistent kernel: the epilogue tile sits past the ring (loads stay in flight)
+  static constexpr int P_BODY = OPER + PART;
+  static constexpr int P_TOTAL = P_BODY + 128;
   static constexpr int NCOLS = BN < 32 ? 32 : BN;
 };
 
@@ -545,6 +550,155 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent form of the TMA 1x1 kernel (variants 3000 + BN, split 1, large
+// M): a CTA walks M tiles blockIdx.x, blockIdx.x + gridDim.x, ... and the
+// stage ring runs over the flattened (tile, k-tile) sequence, so the loads of
+// the next tile are in flight while this tile's accumulator is drained
+// (ncu at bs256: the one-tile kernel spends 32 % of its stalls waiting for
+// the first stages of every tile, with nothing else resident to overlap).
+// ---------------------------------------------------------------------------
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    conv_tc_tma_persistent_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
+                                  const __grid_constant__ CUtensorMap tbl, TcArgs a) {
+  using L = TcSmem<BN, BN == 128 ? 2 : 0>;  // 2 x 64 KB ring + 66 KB tile for BN = 128
+  constexpr int S = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::P_BODY);
+  uint64_t* done = full + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + S);
+  const uint32_t sbase = smem_u32(smem);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int n0 = blockIdx.y * BN;
+  const int iters = (a.Kdim + TC_BK - 1) / TC_BK;  // k-tiles per M tile
+  const int mtiles = (a.M + TC_BM - 1) / TC_BM;
+  const int ntl = mtiles > (int)blockIdx.x ? (mtiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = ntl * iters;  // flattened (tile, k-tile) sequence of this CTA
+  constexpr uint32_t A_TX = L::A_BYTES, B_TX = 2 * L::B_BYTES;
+
+  if (tid == 0) {
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tbh);
+    prefetch_tmap(&tbl);
+    for (int st = 0; st < S; ++st) {
+      mbar_init(smem_u32(&full[st]), 1);
+      mbar_init(smem_u32(&done[st]), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)L::NCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto load_b = [&](int q, int st) {
+    const uint32_t stage = sbase + st * L::STAGE;
+    const int kc = (q % iters) * (TC_BK / 4);
+    const uint32_t bar = smem_u32(&full[st]);
+    tma_load_3d(stage + 2 * L::A_BYTES, &tbh, 0, n0, kc, bar);
+    tma_load_3d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, 0, n0, kc, bar);
+  };
+  auto load_a = [&](int q, int st) {
+    const uint32_t stage = sbase + st * L::STAGE;
+    const int m0 = ((int)blockIdx.x + (q / iters) * (int)gridDim.x) * TC_BM;
+    tma_load_3d(stage, &ta, 0, m0, (q % iters) * (TC_BK / 4), smem_u32(&full[st]));
+  };
+  if (tid == 0) {
+    for (int st = 0; st < S && st < total; ++st) {
+      mbar_expect_tx(smem_u32(&full[st]), A_TX + B_TX);
+      load_b(st, st);
+    }
+  }
+  pdl_trigger();
+  pdl_wait();
+  if (tid == 0)
+    for (int st = 0; st < S && st < total; ++st) load_a(st, st);
+
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                         ((uint32_t)(TC_BM >> 4) << 24);
+  const int row = warp * 32 + lane;
+  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  float* part = reinterpret_cast<float*>(smem + S * L::STAGE);  // past the ring: loads stay in flight
+  cg::cluster_group cluster = cg::this_cluster();
+#pragma unroll 1
+  for (int q = 0; q < total; ++q) {
+    const int st = q % S;
+    const int kt = q % iters;
+    mbar_wait(smem_u32(&full[st]), (q / S) & 1);
+    {
+      float4* hi = reinterpret_cast<float4*>(smem + st * L::STAGE);
+      float4* lo = reinterpret_cast<float4*>(smem + st * L::STAGE + L::A_BYTES);
+#pragma unroll 2
+      for (int i = tid; i < L::A_BYTES / 16; i += TC_THREADS) {
+        float4 x = hi[i];
+        if (a.pre_relu) {
+          x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+        }
+        const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+        hi[i] = h;
+        lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t a_hi = sbase + st * L::STAGE, a_lo = a_hi + L::A_BYTES;
+      const uint32_t b_hi = a_hi + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
+      constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
+#pragma unroll
+      for (int ks = 0; ks < TC_BK / 8; ++ks) {
+        const uint64_t ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
+        const uint64_t al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
+        const uint64_t bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
+        const uint64_t bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+        mma_tf32(tmem, ah, bh, idesc, (kt | ks) ? 1u : 0u);
+        mma_tf32(tmem, ah, bl, idesc, 1u);
+        mma_tf32(tmem, al, bh, idesc, 1u);
+      }
+      mma_commit(smem_u32(&done[st]));
+      if (q >= 1 && q - 1 + S < total) {  // refill the stage the previous MMAs released
+        const int ps = (q - 1) % S;
+        mbar_wait(smem_u32(&done[ps]), ((q - 1) / S) & 1);
+        mbar_expect_tx(smem_u32(&full[ps]), A_TX + B_TX);
+        load_b(q - 1 + S, ps);
+        load_a(q - 1 + S, ps);
+      }
+    }
+    if (kt == iters - 1) {  // tile complete: drain the accumulator while the next tile's stages load
+      mbar_wait(smem_u32(&done[st]), (q / S) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld16x2(t_row + c0, v);
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(&part[row * L::PS + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+      tc_fence_before();
+      const int m0 = ((int)blockIdx.x + (q / iters) * (int)gridDim.x) * TC_BM;
+      tile_epilogue<TC_BM, BN, TC_THREADS, L::PS>(a.epi, part, m0, n0, 1, cluster);
+      __syncthreads();  // part is rewritten by the next tile; the next MMAs overwrite TMEM
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)L::NCOLS)
+                 : "memory");
+  }
+}
+
 static TcArgs tc_args(const sw_op_desc& op) {
   const int64_t* p = op.params;
   TcArgs a;
@@ -579,7 +733,7 @@ static TcArgs tc_args(const sw_op_desc& op) {
 }
 
 // variant = N tile (32, 64, 128, 256); SP_SPLIT_K = cluster split along K.
-template <int BN, int SOVR = 0>
+template <int BN, int SOVR = 0, bool PERSIST = false>
 static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st) {
   // 1x1 / stride 1 / no padding on 16-B aligned NHWC rows only
   if (a.R != 1 || a.S != 1 || a.sh != 1 || a.sw != 1 || a.ph != 0 || a.pw != 0 || !a.vec)
@@ -598,6 +752,14 @@ static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st)
     const uint32_t box[3] = {4, (uint32_t)BN, TC_BK / 4};
     if (!encode_tmap_f32(&tbh, a.w_hi, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
     if (!encode_tmap_f32(&tbl, a.w_lo, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
+  }
+  if constexpr (PERSIST) {
+    if (a.split != 1) return (int)cudaErrorInvalidValue;
+    using LP = TcSmem<BN, BN == 128 ? 2 : 0>;
+    const int64_t ntn = cdiv(a.K, BN), mt = cdiv(a.M, TC_BM);
+    const int64_t gx = std::min<int64_t>(mt, std::max<int64_t>(1, 148 / ntn));
+    return (int)launch_k(conv_tc_tma_persistent_kernel<BN>, dim3((unsigned)gx, (unsigned)ntn, 1), dim3(TC_THREADS),
+                         (size_t)LP::P_TOTAL, st, 1u, ta, tbh, tbl, a);
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), (unsigned)cdiv(a.K, BN), (unsigned)a.split);
   return (int)launch_k(conv_tc_tma_kernel<BN, SOVR>, grid, dim3(TC_THREADS), (size_t)TcSmem<BN, SOVR>::TOTAL, st,
@@ -618,6 +780,10 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
     // 2000 + BN: two stages, two CTAs per SM
     case 2032: return launch_tc_tma<32, 2>(a, op, st);
     case 2064: return launch_tc_tma<64, 2>(a, op, st);
+    // 3000 + BN: persistent tile loop (split 1)
+    case 3032: return launch_tc_tma<32, 0, true>(a, op, st);
+    case 3064: return launch_tc_tma<64, 0, true>(a, op, st);
+    case 3128: return launch_tc_tma<128, 0, true>(a, op, st);
     default: break;
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), 1, (unsigned)a.split);
@@ -645,6 +811,12 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
 
 // Pre-set the dynamic smem limits outside any stream capture.
 void init_tc_kernels() {
+  cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       TcSmem<32>::P_TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       TcSmem<64>::P_TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       TcSmem<128, 2>::P_TOTAL);
   cudaFuncSetAttribute(conv_tc_tma_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32, 2>::TOTAL);
   cudaFuncSetAttribute(conv_tc_tma_kernel<32, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(conv_tc_tma_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<64, 2>::TOTAL);

@@ -100,6 +100,35 @@ def test_tcgen05_tiles_and_splits(bn, split):
     eng.close()
 
 
+@pytest.mark.parametrize("bn", [32, 64, 128])
+@pytest.mark.parametrize("cin,cout,hw,batch,pre", [(264, 88, 28, 8, True), (44, 200, 17, 20, False), (64, 64, 56, 8, False),
+                                                   (40, 1000, 9, 3, True)])
+def test_tcgen05_tma_persistent(bn, cin, cout, hw, batch, pre):
+    """Persistent TMA tcgen05 1x1 conv (variants 3000 + N tile): several M
+    tiles per CTA, ragged last tile, ragged N / K, pre-ReLU, fused BN bias."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
+    torch.manual_seed(4)
+    m = Conv(cin, cout, 1, 1, 0, bias=False, act=None, bn=True).eval()
+    lead = [nn.Conv2d(cin, cin, 1, bias=False)] + ([nn.ReLU()] if pre else [])
+    m = nn.Sequential(*lead, m).eval()
+    x = torch.randn(batch, cin, hw, hw)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="tc").prepare(x)
+    last = eng.ops[len(eng.program.tasks) - 1]
+    assert last.kind == K_CONV_TC
+    last.variant = 3000 + bn
+    last.params[SP_SPLIT_K] = 1
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 @pytest.mark.parametrize("bn", [32, 64, 128, 256, 1032, 1064])
 @pytest.mark.parametrize("split", [1, 2, 8, 16])
 @pytest.mark.parametrize("cin,cout,hw,batch,pre", [(264, 88, 28, 2, True), (1056, 200, 7, 1, False),
