@@ -82,6 +82,14 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
 
+// K-major SWIZZLE_128B operand (TMA box = 32 fp32 x rows, 1024-B aligned):
+// 8-row groups 1024 B apart (SBO), layout type 2 in bits 61-63; a K step of 8
+// tf32 advances the start address by 32 B inside the swizzle atom.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -558,7 +566,7 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
 // (ncu at bs256: the one-tile kernel spends 32 % of its stalls waiting for
 // the first stages of every tile, with nothing else resident to overlap).
 // ---------------------------------------------------------------------------
-template <int BN>
+template <int BN, bool SWZ = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_tma_persistent_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                                   const __grid_constant__ CUtensorMap tbl, TcArgs a) {
@@ -602,15 +610,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   auto load_b = [&](int q, int st) {
     const uint32_t stage = sbase + st * L::STAGE;
-    const int kc = (q % iters) * (TC_BK / 4);
     const uint32_t bar = smem_u32(&full[st]);
-    tma_load_3d(stage + 2 * L::A_BYTES, &tbh, 0, n0, kc, bar);
-    tma_load_3d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, 0, n0, kc, bar);
+    if constexpr (SWZ) {  // 2-D maps (k, row), 128-B rows swizzled
+      tma_load_2d(stage + 2 * L::A_BYTES, &tbh, (q % iters) * TC_BK, n0, bar);
+      tma_load_2d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, (q % iters) * TC_BK, n0, bar);
+    } else {
+      const int kc = (q % iters) * (TC_BK / 4);
+      tma_load_3d(stage + 2 * L::A_BYTES, &tbh, 0, n0, kc, bar);
+      tma_load_3d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, 0, n0, kc, bar);
+    }
   };
   auto load_a = [&](int q, int st) {
     const uint32_t stage = sbase + st * L::STAGE;
     const int m0 = ((int)blockIdx.x + (q / iters) * (int)gridDim.x) * TC_BM;
-    tma_load_3d(stage, &ta, 0, m0, (q % iters) * (TC_BK / 4), smem_u32(&full[st]));
+    if constexpr (SWZ)
+      tma_load_2d(stage, &ta, (q % iters) * TC_BK, m0, smem_u32(&full[st]));
+    else
+      tma_load_3d(stage, &ta, 0, m0, (q % iters) * (TC_BK / 4), smem_u32(&full[st]));
   };
   if (tid == 0) {
     for (int st = 0; st < S && st < total; ++st) {
@@ -657,10 +673,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
 #pragma unroll
       for (int ks = 0; ks < TC_BK / 8; ++ks) {
-        const uint64_t ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
-        const uint64_t al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
-        const uint64_t bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
-        const uint64_t bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+        uint64_t ah, al, bh, bl;
+        if constexpr (SWZ) {
+          ah = make_desc_sw128(a_hi + ks * 32);
+          al = make_desc_sw128(a_lo + ks * 32);
+          bh = make_desc_sw128(b_hi + ks * 32);
+          bl = make_desc_sw128(b_lo + ks * 32);
+        } else {
+          ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
+          al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
+          bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
+          bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+        }
         mma_tf32(tmem, ah, bh, idesc, (kt | ks) ? 1u : 0u);
         mma_tf32(tmem, ah, bl, idesc, 1u);
         mma_tf32(tmem, al, bh, idesc, 1u);
@@ -733,13 +757,25 @@ static TcArgs tc_args(const sw_op_desc& op) {
 }
 
 // variant = N tile (32, 64, 128, 256); SP_SPLIT_K = cluster split along K.
-template <int BN, int SOVR = 0, bool PERSIST = false>
+template <int BN, int SOVR = 0, bool PERSIST = false, bool SWZ = false>
 static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st) {
   // 1x1 / stride 1 / no padding on 16-B aligned NHWC rows only
   if (a.R != 1 || a.S != 1 || a.sh != 1 || a.sw != 1 || a.ph != 0 || a.pw != 0 || !a.vec)
     return (int)cudaErrorInvalidValue;
   if (a.in_sn != (int64_t)a.H * a.W * a.in_sw || a.in_sh != (int64_t)a.W * a.in_sw) return (int)cudaErrorInvalidValue;
   CUtensorMap ta, tbh, tbl;
+  if constexpr (SWZ) {  // 2-D (k, row) maps, box 32 fp32 x rows, 128-B swizzle
+    const uint64_t da[2] = {(uint64_t)a.C, (uint64_t)a.M};
+    const uint64_t sa[1] = {(uint64_t)a.in_sw * 4};
+    const uint32_t ba[2] = {TC_BK, TC_BM};
+    const uint64_t db[2] = {(uint64_t)a.Kpad, (uint64_t)a.K};
+    const uint64_t sb[1] = {(uint64_t)a.Kpad * 4};
+    const uint32_t bb[2] = {TC_BK, (uint32_t)BN};
+    if (!encode_tmap_f32(&ta, a.in, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_tmap_f32(&tbh, a.w_hi, 2, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_tmap_f32(&tbl, a.w_lo, 2, db, sb, bb, CU_TENSOR_MAP_SWIZZLE_128B))
+      return (int)cudaErrorInvalidValue;
+  } else {
   {  // activations: (4 floats, M rows, C/4 chunks)
     const uint64_t dims[3] = {4, (uint64_t)a.M, (uint64_t)(a.C / 4)};
     const uint64_t str[2] = {(uint64_t)a.in_sw * 4, 16};
@@ -753,12 +789,13 @@ static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st)
     if (!encode_tmap_f32(&tbh, a.w_hi, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
     if (!encode_tmap_f32(&tbl, a.w_lo, 3, dims, str, box)) return (int)cudaErrorInvalidValue;
   }
+  }
   if constexpr (PERSIST) {
     if (a.split != 1) return (int)cudaErrorInvalidValue;
     using LP = TcSmem<BN, BN == 128 ? 2 : 0>;
     const int64_t ntn = cdiv(a.K, BN), mt = cdiv(a.M, TC_BM);
     const int64_t gx = std::min<int64_t>(mt, std::max<int64_t>(1, 148 / ntn));
-    return (int)launch_k(conv_tc_tma_persistent_kernel<BN>, dim3((unsigned)gx, (unsigned)ntn, 1), dim3(TC_THREADS),
+    return (int)launch_k(conv_tc_tma_persistent_kernel<BN, SWZ>, dim3((unsigned)gx, (unsigned)ntn, 1), dim3(TC_THREADS),
                          (size_t)LP::P_TOTAL, st, 1u, ta, tbh, tbl, a);
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), (unsigned)cdiv(a.K, BN), (unsigned)a.split);
@@ -784,6 +821,10 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
     case 3032: return launch_tc_tma<32, 0, true>(a, op, st);
     case 3064: return launch_tc_tma<64, 0, true>(a, op, st);
     case 3128: return launch_tc_tma<128, 0, true>(a, op, st);
+    // 4000 + BN: persistent, 128-B swizzled operands (full-row TMA boxes)
+    case 4032: return launch_tc_tma<32, 0, true, true>(a, op, st);
+    case 4064: return launch_tc_tma<64, 0, true, true>(a, op, st);
+    case 4128: return launch_tc_tma<128, 0, true, true>(a, op, st);
     default: break;
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), 1, (unsigned)a.split);
@@ -816,6 +857,12 @@ void init_tc_kernels() {
   cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        TcSmem<64>::P_TOTAL);
   cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       TcSmem<128, 2>::P_TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       TcSmem<32>::P_TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       TcSmem<64>::P_TOTAL);
+  cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        TcSmem<128, 2>::P_TOTAL);
   cudaFuncSetAttribute(conv_tc_tma_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32, 2>::TOTAL);
   cudaFuncSetAttribute(conv_tc_tma_kernel<32, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

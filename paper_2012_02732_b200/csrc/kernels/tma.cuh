@@ -109,7 +109,8 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
 // layout breaks a TMA rule (16-B aligned base / strides, box ≤ 256, inner box
 // bytes % 16) so the caller can refuse the variant.
 inline bool encode_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                            const uint64_t* strides_bytes, const uint32_t* box) {
+                            const uint64_t* strides_bytes, const uint32_t* box,
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -133,7 +134,7 @@ inline bool encode_tmap_f32(CUtensorMap* m, const void* base, int rank, const ui
   }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), d, s, b, e,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

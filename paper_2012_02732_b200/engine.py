@@ -169,8 +169,9 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
                 out.append((K_CONV_TC, 1000 + bn, split))
                 if bn <= 64 and M >= 4096:  # two-stage ring, two CTAs per SM (large M)
                     out.append((K_CONV_TC, 2000 + bn, split))
-                if bn <= 128 and split == 1 and M >= 4096:  # persistent tile loop
+                if bn <= 128 and split == 1 and M >= 4096:  # persistent tile loop (+ 128-B swizzle)
                     out.append((K_CONV_TC, 3000 + bn, 1))
+                    out.append((K_CONV_TC, 4000 + bn, 1))
     return out
 
 

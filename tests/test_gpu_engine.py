@@ -100,11 +100,12 @@ def test_tcgen05_tiles_and_splits(bn, split):
     eng.close()
 
 
-@pytest.mark.parametrize("bn", [32, 64, 128])
+@pytest.mark.parametrize("bn", [32, 64, 128, 1032, 1064, 1128])
 @pytest.mark.parametrize("cin,cout,hw,batch,pre", [(264, 88, 28, 8, True), (44, 200, 17, 20, False), (64, 64, 56, 8, False),
                                                    (40, 1000, 9, 3, True)])
 def test_tcgen05_tma_persistent(bn, cin, cout, hw, batch, pre):
-    """Persistent TMA tcgen05 1x1 conv (variants 3000 + N tile): several M
+    """Persistent TMA tcgen05 1x1 conv (variants 3000 + N tile; 4000 + N tile
+    with 128-B swizzled operands): several M
     tiles per CTA, ragged last tile, ragged N / K, pre-ReLU, fused BN bias."""
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
