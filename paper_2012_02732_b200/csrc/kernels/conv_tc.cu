@@ -412,7 +412,7 @@ struct TcMaps {
 
 // SOVR > 0: a shallower ring (SOVR stages) so that two CTAs share an SM and
 // one CTA's prologue / epilogue overlaps the other's TMA stream (large M).
-template <int BN, int SOVR = 0>
+template <int BN, int SOVR = 0, bool SWZ = false>
 __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
     conv_tc_tma_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                        const __grid_constant__ CUtensorMap tbl, TcArgs a) {
@@ -457,14 +457,22 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
 
   auto load_b = [&](int kt, int st) {
     const uint32_t stage = sbase + st * L::STAGE;
-    const int kc = (kt0 + kt) * (TC_BK / 4);
     const uint32_t bar = smem_u32(&full[st]);
-    tma_load_3d(stage + 2 * L::A_BYTES, &tbh, 0, n0, kc, bar);
-    tma_load_3d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, 0, n0, kc, bar);
+    if constexpr (SWZ) {
+      tma_load_2d(stage + 2 * L::A_BYTES, &tbh, (kt0 + kt) * TC_BK, n0, bar);
+      tma_load_2d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, (kt0 + kt) * TC_BK, n0, bar);
+    } else {
+      const int kc = (kt0 + kt) * (TC_BK / 4);
+      tma_load_3d(stage + 2 * L::A_BYTES, &tbh, 0, n0, kc, bar);
+      tma_load_3d(stage + 2 * L::A_BYTES + L::B_BYTES, &tbl, 0, n0, kc, bar);
+    }
   };
   auto load_a = [&](int kt, int st) {
     const uint32_t stage = sbase + st * L::STAGE;
-    tma_load_3d(stage, &ta, 0, m0, (kt0 + kt) * (TC_BK / 4), smem_u32(&full[st]));
+    if constexpr (SWZ)
+      tma_load_2d(stage, &ta, (kt0 + kt) * TC_BK, m0, smem_u32(&full[st]));
+    else
+      tma_load_3d(stage, &ta, 0, m0, (kt0 + kt) * (TC_BK / 4), smem_u32(&full[st]));
   };
   if (tid == 0) {
     for (int st = 0; st < S && st < iters; ++st) {
@@ -506,10 +514,18 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
       constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
 #pragma unroll
       for (int ks = 0; ks < TC_BK / 8; ++ks) {
-        const uint64_t ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
-        const uint64_t al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
-        const uint64_t bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
-        const uint64_t bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+        uint64_t ah, al, bh, bl;
+        if constexpr (SWZ) {
+          ah = make_desc_sw128(a_hi + ks * 32);
+          al = make_desc_sw128(a_lo + ks * 32);
+          bh = make_desc_sw128(b_hi + ks * 32);
+          bl = make_desc_sw128(b_lo + ks * 32);
+        } else {
+          ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
+          al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
+          bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
+          bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+        }
         mma_tf32(tmem, ah, bh, idesc, (it | ks) ? 1u : 0u);
         mma_tf32(tmem, ah, bl, idesc, 1u);
         mma_tf32(tmem, al, bh, idesc, 1u);
@@ -799,7 +815,7 @@ static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st)
                          (size_t)LP::P_TOTAL, st, 1u, ta, tbh, tbl, a);
   }
   dim3 grid((unsigned)cdiv(a.M, TC_BM), (unsigned)cdiv(a.K, BN), (unsigned)a.split);
-  return (int)launch_k(conv_tc_tma_kernel<BN, SOVR>, grid, dim3(TC_THREADS), (size_t)TcSmem<BN, SOVR>::TOTAL, st,
+  return (int)launch_k(conv_tc_tma_kernel<BN, SOVR, SWZ>, grid, dim3(TC_THREADS), (size_t)TcSmem<BN, SOVR>::TOTAL, st,
                        (unsigned)a.split, ta, tbh, tbl, a);
 }
 
@@ -821,6 +837,11 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
     case 3032: return launch_tc_tma<32, 0, true>(a, op, st);
     case 3064: return launch_tc_tma<64, 0, true>(a, op, st);
     case 3128: return launch_tc_tma<128, 0, true>(a, op, st);
+    // 5000 + BN: one tile per CTA (split-K clusters), 128-B swizzled operands
+    case 5032: return launch_tc_tma<32, 0, false, true>(a, op, st);
+    case 5064: return launch_tc_tma<64, 0, false, true>(a, op, st);
+    case 5128: return launch_tc_tma<128, 0, false, true>(a, op, st);
+    case 5256: return launch_tc_tma<256, 0, false, true>(a, op, st);
     // 4000 + BN: persistent, 128-B swizzled operands (full-row TMA boxes)
     case 4032: return launch_tc_tma<32, 0, true, true>(a, op, st);
     case 4064: return launch_tc_tma<64, 0, true, true>(a, op, st);
@@ -852,6 +873,15 @@ int launch_conv_tc(const sw_op_desc& op, void* stream) {
 
 // Pre-set the dynamic smem limits outside any stream capture.
 void init_tc_kernels() {
+#define SW_TC_SWZ_ATTR(BN_)                                                                                  \
+  cudaFuncSetAttribute(conv_tc_tma_kernel<BN_, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                       TcSmem<BN_>::TOTAL);                                                                  \
+  cudaFuncSetAttribute(conv_tc_tma_kernel<BN_, 0, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  SW_TC_SWZ_ATTR(32)
+  SW_TC_SWZ_ATTR(64)
+  SW_TC_SWZ_ATTR(128)
+  SW_TC_SWZ_ATTR(256)
+#undef SW_TC_SWZ_ATTR
   cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        TcSmem<32>::P_TOTAL);
   cudaFuncSetAttribute(conv_tc_tma_persistent_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,

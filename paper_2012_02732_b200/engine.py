@@ -167,6 +167,7 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
             # TMA-fed tcgen05 kernel (conv_tc.cu); refuses strided / unaligned layouts
             if pointwise:
                 out.append((K_CONV_TC, 1000 + bn, split))
+                out.append((K_CONV_TC, 5000 + bn, split))  # 128-B swizzled operands
                 if bn <= 64 and M >= 4096:  # two-stage ring, two CTAs per SM (large M)
                     out.append((K_CONV_TC, 2000 + bn, split))
                 if bn <= 128 and split == 1 and M >= 4096:  # persistent tile loop (+ 128-B swizzle)

@@ -119,7 +119,8 @@ def test_fused_separable_blocks_emulated(programs):
 def test_conv_candidates_tcgen05_variants():
     """Autotune candidate rules (engine.conv_candidates): the large-M 1x1
     variants (two-stage 2000 + N, persistent 3000 + N, swizzled 4000 + N) are
-    offered only for pointwise convs with M >= 4096, persistent ones only at
+    offered only for pointwise convs with M >= 4096 (5000 + N, swizzled one
+    tile per CTA, for any pointwise conv), persistent ones only at
     split 1; k x k convs never get TMA variants; tiny M gets the GEMV."""
     from paper_2012_02732_b200.engine import K_CONV, K_CONV_TC, conv_candidates
     big = conv_candidates(200704, 88, 264, 1, 1, (0, 0))
@@ -129,7 +130,8 @@ def test_conv_candidates_tcgen05_variants():
     assert all(s == 1 for v, s in tc if v >= 3000)
     assert {(2032, 1), (2064, 1)} <= tc and not any(v in (2128, 2256) for v, _ in tc)
     small = conv_candidates(196, 88, 528, 1, 1, (0, 0))
-    assert not any(k == K_CONV_TC and v >= 2000 for k, v, _ in small)
+    assert not any(k == K_CONV_TC and 2000 <= v < 5000 for k, v, _ in small)
+    assert any(k == K_CONV_TC and v >= 5000 for k, v, _ in small)  # swizzled one-tile variants: any M
     kxk = conv_candidates(200704, 64, 576, 3, 3, (1, 1))
     assert not any(k == K_CONV_TC and v >= 1000 for k, v, _ in kxk)
     gemv = conv_candidates(1, 1000, 1056, 1, 1, (0, 0))

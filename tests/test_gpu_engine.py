@@ -130,13 +130,14 @@ def test_tcgen05_tma_persistent(bn, cin, cout, hw, batch, pre):
     eng.close()
 
 
-@pytest.mark.parametrize("bn", [32, 64, 128, 256, 1032, 1064])
+@pytest.mark.parametrize("bn", [32, 64, 128, 256, 1032, 1064, 4032, 4064, 4128, 4256])
 @pytest.mark.parametrize("split", [1, 2, 8, 16])
 @pytest.mark.parametrize("cin,cout,hw,batch,pre", [(264, 88, 28, 2, True), (1056, 200, 7, 1, False),
                                                    (44, 1000, 9, 3, True)])
 def test_tcgen05_tma_pointwise(bn, split, cin, cout, hw, batch, pre):
     """TMA-fed tcgen05 1x1 conv (variants 1000 + N tile; 2000 + N tile = the
-    two-stage, two-CTAs-per-SM ring): every N tile and split-K cluster size,
+    two-stage, two-CTAs-per-SM ring; 5000 + N tile = 128-B swizzled operands):
+    every N tile and split-K cluster size,
     ragged M / N / K, pre-ReLU on load, fused BN bias."""
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
