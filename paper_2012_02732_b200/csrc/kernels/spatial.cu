@@ -97,15 +97,17 @@ __global__ void __launch_bounds__(256) spatial_kernel(SpatialArgs a, int64_t tot
   using T = typename V::T;
   pdl_trigger();
   pdl_wait();
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int CG = a.C / VEC;
-  int cg = (int)(idx % CG);
-  int64_t t = idx / CG;
-  int q = (int)(t % a.Q);
-  t /= a.Q;
-  int p = (int)(t % a.P);
-  int n = (int)(t / a.P);
+  // 32-bit index math (the launcher guarantees total < 2^31): the int64
+  // div / mod chain was ~500 instructions per thread, most of a bs256 pool
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int64_t)idx >= total) return;
+  const uint32_t CG = (uint32_t)(a.C / VEC);
+  const int cg = (int)(idx % CG);
+  uint32_t t = idx / CG;
+  const int q = (int)(t % (uint32_t)a.Q);
+  t /= (uint32_t)a.Q;
+  const int p = (int)(t % (uint32_t)a.P);
+  const int n = (int)(t / (uint32_t)a.P);
   int c = cg * VEC;
   const float* base = a.in + n * a.in_sn + c * a.in_sc;
   const int ih0 = p * a.sh - a.ph, iw0 = q * a.sw - a.pw;
@@ -203,6 +205,7 @@ static int launch_spatial(const sw_op_desc& op, void* stream) {
   bool v4 = can_vec4(a, op, KIND == 0);
   int64_t total = (int64_t)a.N * a.P * a.Q * (v4 ? a.C / 4 : a.C);
   if (total == 0) return 0;
+  if (total >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;  // 32-bit index math in the kernel
   int blocks = (int)cdiv(total, 256);
   const int ks = (a.R == a.S && (a.R == 1 || a.R == 3 || a.R == 5 || a.R == 7)) ? a.R : 0;
   if (v4)
