@@ -67,6 +67,35 @@ int main() {
   float ms;
   cudaEventElapsedTime(&ms, a, b);
   printf("DMA cudaMemcpyAsync back-to-back: %.2f us per copy (%.1f GB/s)\n", ms * 10.f, bytes / (ms * 10.f) / 1e3);
+  // single-shot latency (one copy, idle GPU before and after)
+  for (int gsz : {37, 148, 592}) {
+    float tot = 0.f;
+    for (int it = 0; it < 50; ++it) {
+      cudaStreamSynchronize(st);
+      cudaEventRecord(a, st);
+      copy_k<1><<<gsz, 256, 0, st>>>(h, dd, n);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float m1;
+      cudaEventElapsedTime(&m1, a, b);
+      tot += m1;
+    }
+    printf("single-shot kernel copy, %d blocks: %.2f us\n", gsz, tot * 1000.f / 50);
+  }
+  {
+    float tot = 0.f;
+    for (int it = 0; it < 50; ++it) {
+      cudaStreamSynchronize(st);
+      cudaEventRecord(a, st);
+      cudaMemcpyAsync(dd, h, bytes, cudaMemcpyHostToDevice, st);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float m1;
+      cudaEventElapsedTime(&m1, a, b);
+      tot += m1;
+    }
+    printf("single-shot DMA copy: %.2f us\n", tot * 1000.f / 50);
+  }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
