@@ -42,6 +42,25 @@ float run(const float4* h, float4* dd, int64_t n, int blocks, int threads, cudaS
   return ms * 1000.f / 400.f;
 }
 
+// stem-conv access pattern straight from pinned host memory (UVA): NCHW 3 x 224 x 224,
+// 3x3 stride 2, one thread per output pixel summing its 27 taps (reads only)
+__global__ void stem_read_k(const float* __restrict__ x, float* __restrict__ y, int H, int W, int P, int Q) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P * Q) return;
+  const int p = i / Q, q = i % Q;
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int h = 2 * p + r, w = 2 * q + s;
+        if (h < H && w < W) acc += x[(c * H + h) * W + w];
+      }
+  y[i] = acc;
+}
+
 int main() {
   const int64_t bytes = 602112, n = bytes / 16;
   float4 *h, *dd;
@@ -95,6 +114,24 @@ int main() {
       tot += m1;
     }
     printf("single-shot DMA copy: %.2f us\n", tot * 1000.f / 50);
+  }
+  for (int dev_src = 0; dev_src < 2; ++dev_src) {
+    const float* src = dev_src ? reinterpret_cast<const float*>(dd) : reinterpret_cast<const float*>(h);
+    float* yo = nullptr;
+    cudaMalloc(&yo, 111 * 111 * 4);
+    float tot = 0.f;
+    for (int it = 0; it < 50; ++it) {
+      cudaStreamSynchronize(st);
+      cudaEventRecord(a, st);
+      stem_read_k<<<(111 * 111 + 255) / 256, 256, 0, st>>>(src, yo, 224, 224, 111, 111);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float m1;
+      cudaEventElapsedTime(&m1, a, b);
+      tot += m1;
+    }
+    printf("stem-pattern read from %s: %.2f us\n", dev_src ? "device (HBM/L2)" : "pinned host (UVA)", tot * 1000.f / 50);
+    cudaFree(yo);
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
