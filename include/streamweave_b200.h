@@ -221,6 +221,12 @@ int sw_engine_replay(sw_engine* e, int32_t slot);
  * staging buffer, replay a with_io slot, wait, copy the staged output to
  * host_out (out_bytes).  Either pointer may be NULL (staging used as is). */
 int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_out);
+
+/* n requests back to back through device-resident slot `slot` (pipelined:
+ * request i+1's H2D overlaps request i's replay; staging is double-buffered).
+ * host_in[i] / host_out[i]: in_bytes / out_bytes host buffers (pinned for
+ * overlap).  Results equal n sw_engine_infer calls. */
+int sw_engine_infer_stream(sw_engine* e, int32_t slot, int64_t n, const uint64_t* host_in, const uint64_t* host_out);
 /* Replay and wait; returns host wall time of the launch call in ns. */
 int sw_engine_replay_sync(sw_engine* e, int32_t slot, int64_t* out_launch_ns);
 /* Time `iters` replays with cudaEvents on the launch stream → mean µs,

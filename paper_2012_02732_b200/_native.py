@@ -108,6 +108,7 @@ PROTOTYPES = {
     "sw_engine_add_input": (C.c_int, [C.c_void_p, u64, u64, i64]),
     "sw_engine_set_prefetch": (C.c_int, [C.c_void_p, u64, i64]),
     "sw_engine_set_priorities": (C.c_int, [C.c_void_p, i64, P32]),
+    "sw_engine_infer_stream": (C.c_int, [C.c_void_p, C.c_int32, i64, P64, P64]),
     "sw_nccl_load": (C.c_int, [C.c_char_p]),
     "sw_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "sw_engine_nccl_init": (C.c_int, [C.c_void_p, i32, i32, C.c_char_p]),

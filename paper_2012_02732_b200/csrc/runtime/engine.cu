@@ -130,6 +130,11 @@ struct sw_engine {
   std::vector<sw_op_desc> ops;
   std::vector<int32_t> prio;  // per-task launch priority (sw_engine_set_priorities)
   uint64_t host_in = 0, dev_in = 0, host_out = 0, dev_out = 0;
+  // request pipelining (sw_engine_infer_stream): double-buffered device
+  // staging of the inputs, filled on a copy stream under the running replay
+  void* stage[2] = {nullptr, nullptr};
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   int64_t in_bytes = 0, out_bytes = 0;
   uint32_t flags = 0;  // SW_ENGINE_PDL | SW_ENGINE_NULL_KERNELS
   Slot slots[kSlots];
@@ -297,6 +302,12 @@ int sw_engine_destroy(sw_engine* e) {
   for (auto ev : e->events) cudaEventDestroy(ev);
   for (auto ev : e->joins) cudaEventDestroy(ev);
   if (e->pf_stream) cudaStreamDestroy(e->pf_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (e->stage[i]) cudaFree(e->stage[i]);
+    if (e->ev_h2d[i]) cudaEventDestroy(e->ev_h2d[i]);
+    if (e->ev_done[i]) cudaEventDestroy(e->ev_done[i]);
+  }
+  if (e->cstream) cudaStreamDestroy(e->cstream);
   if (e->pf_join) cudaEventDestroy(e->pf_join);
   for (auto ev : e->tr_start) cudaEventDestroy(ev);
   for (auto ev : e->tr_end) cudaEventDestroy(ev);
@@ -558,6 +569,49 @@ int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_
   if (q != cudaSuccess) return cuda_fail(q, "cudaStreamQuery");
   if (host_out && reinterpret_cast<uint64_t>(host_out) != e->host_out)
     std::memcpy(host_out, reinterpret_cast<const void*>(e->host_out), (size_t)e->out_bytes);
+  return SW_OK;
+}
+
+// n requests back to back through a device-resident slot (no staging nodes):
+// request i+1's H2D runs on a copy stream into the other staging buffer while
+// request i replays; each replay starts with a device-to-device copy of its
+// staged input into the arena's input storage and ends with the D2H of its
+// output.  Same results as n calls of sw_engine_infer; throughput, not latency.
+int sw_engine_infer_stream(sw_engine* e, int32_t slot, int64_t n, const uint64_t* host_in, const uint64_t* host_out) {
+  if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
+  if (e->slots[slot].io_in) return sw::fail(SW_VALUE_ERROR, "infer_stream needs a device-resident slot");
+  if (n <= 0) return SW_OK;
+  CU(cudaSetDevice(e->device));
+  if (!e->cstream) {
+    CU(cudaStreamCreateWithFlags(&e->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaMalloc(&e->stage[i], (size_t)e->in_bytes));
+      CU(cudaEventCreateWithFlags(&e->ev_h2d[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&e->ev_done[i], cudaEventDisableTiming));
+    }
+  }
+  const size_t ib = (size_t)e->in_bytes, ob = (size_t)e->out_bytes;
+  CU(cudaMemcpyAsync(e->stage[0], reinterpret_cast<const void*>(host_in[0]), ib, cudaMemcpyHostToDevice, e->cstream));
+  CU(cudaEventRecord(e->ev_h2d[0], e->cstream));
+  for (int64_t i = 0; i < n; ++i) {
+    const int b = (int)(i & 1), nb = b ^ 1;
+    if (i + 1 < n) {  // stage the next request into the other buffer (freed by replay i - 1)
+      if (i >= 1) CU(cudaStreamWaitEvent(e->cstream, e->ev_done[nb], 0));
+      CU(cudaMemcpyAsync(e->stage[nb], reinterpret_cast<const void*>(host_in[i + 1]), ib, cudaMemcpyHostToDevice,
+                         e->cstream));
+      CU(cudaEventRecord(e->ev_h2d[nb], e->cstream));
+    }
+    CU(cudaStreamWaitEvent(e->launch, e->ev_h2d[b], 0));
+    CU(cudaMemcpyAsync(reinterpret_cast<void*>(e->dev_in), e->stage[b], ib, cudaMemcpyDeviceToDevice, e->launch));
+    CU(cudaEventRecord(e->ev_done[b], e->launch));
+    CU(cudaGraphLaunch(e->slots[slot].exec, e->launch));
+    CU(cudaMemcpyAsync(reinterpret_cast<void*>(host_out[i]), reinterpret_cast<const void*>(e->dev_out), ob,
+                       cudaMemcpyDeviceToHost, e->launch));
+  }
+  cudaError_t q;
+  while ((q = cudaStreamQuery(e->launch)) == cudaErrorNotReady) {
+  }
+  if (q != cudaSuccess) return cuda_fail(q, "cudaStreamQuery");
   return SW_OK;
 }
 

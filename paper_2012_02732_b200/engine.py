@@ -805,6 +805,30 @@ class Engine:
         N.check(N.lib().sw_engine_infer(self._h, slot, None, out.data_ptr()))
         return out
 
+    def infer_stream(self, xs, outs=None) -> list:
+        """End-to-end inference of a stream of requests (public serving API):
+        one C call runs them back to back through the device-resident
+        captured graph, staging request i+1 (H2D on a copy stream, double
+        buffered) while request i replays, each output copied back after its
+        replay.  Results equal [engine(x) for x in xs]; pass pinned inputs
+        (and `outs`) for the copies to overlap."""
+        xs = [x.detach() for x in xs]
+        if not xs:
+            return []
+        if not self.prepared:
+            self.prepare(xs[0])
+        for x in xs:
+            if not (x.device.type == "cpu" and x.dtype == torch.float32 and x.is_contiguous()
+                    and x.numel() == self.h_in.numel()):
+                raise ValueError("infer_stream: contiguous fp32 host tensors of the prepared input size")
+        if outs is None:
+            outs = [torch.empty(self.out_shape, dtype=torch.float32, pin_memory=True) for _ in xs]
+        hi = np.array([x.data_ptr() for x in xs], dtype=np.int64)
+        ho = np.array([o.data_ptr() for o in outs], dtype=np.int64)
+        slot = SLOT_MULTI if self.multi_stream else SLOT_SINGLE
+        N.check(N.lib().sw_engine_infer_stream(self._h, slot, len(xs), N.ptr64(hi), N.ptr64(ho)))
+        return outs
+
     def load_input_device(self, x: torch.Tensor):
         """Place a batch in the device input buffer (for device-resident replay)."""
         self.d_in.copy_(x.detach().reshape(-1).to(self.d_in.device, torch.float32))
