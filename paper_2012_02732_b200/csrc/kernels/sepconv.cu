@@ -102,7 +102,7 @@ __device__ __forceinline__ void dw_row_block(const SepArgs& a, const float* base
 }
 
 template <int KS, bool VEC, int BM, int BN, int TM, int TN, int PX = 1>
-__global__ void __launch_bounds__(SEP_THREADS, PX > 1 ? 3 : 0) sepconv_kernel(SepArgs a) {
+__global__ void __launch_bounds__(SEP_THREADS, PX > 1 ? 4 : 0) sepconv_kernel(SepArgs a) {
   static_assert((BM / TM) * (BN / TN) == SEP_THREADS, "256 threads");
   extern __shared__ __align__(16) float smem[];
   const int Cp = (a.C + SEP_BK - 1) / SEP_BK * SEP_BK;
