@@ -270,6 +270,18 @@ constexpr int kNumSimt = sizeof(kSimt) / sizeof(kSimt[0]);
 // accumulators in registers, the filter sits in shared memory as [rsc][K]
 // (warp-uniform broadcast reads), and each pixel's outputs leave as one
 // contiguous run (float4 when the layout allows).
+// Dense pointwise layer with few input channels: the CTA's 128 input pixel
+// rows are one contiguous block, staged into shared memory by coalesced
+// float4 loads (a thread reading its own 128-B pixel row made every load
+// instruction touch 32 lines).  Row stride DX floats, DX / 4 odd: the per-row
+// float4 reads of a warp are conflict-free.
+__host__ __device__ inline bool direct_stage_in(const ConvArgs& a) {
+  return a.R == 1 && a.S == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.in_sc == 1 &&
+         (a.C & 3) == 0 && a.C <= 32 && a.in_sw == a.C && a.in_sh == (int64_t)a.W * a.C &&
+         a.in_sn == (int64_t)a.H * a.W * a.C && (reinterpret_cast<uintptr_t>(a.in) & 15) == 0;
+}
+__host__ __device__ inline int direct_stage_ld(int C) { return ((C / 4 + 1) & 1) ? C + 4 : C + 8; }
+
 template <int KB, int KS>
 __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   extern __shared__ float wsm[];  // [Kdim][KB] + bias[KB]
@@ -325,6 +337,35 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
             acc[4 * k4 + 3] = fmaf(xv, w.w, acc[4 * k4 + 3]);
           }
         }
+    }
+  } else if (direct_stage_in(a)) {
+    float* xs = bsm + KB + 128 * (KB + 4);  // [128][DX], past the epilogue tile
+    const int DX = direct_stage_ld(a.C);
+    const int c4n = a.C / 4;
+    for (int e = tid; e < 128 * c4n; e += 128) {
+      const int px = e / c4n, ch = e - px * c4n;
+      const int mm = min(m0 + px, a.M - 1);
+      float4 v = __ldg(reinterpret_cast<const float4*>(a.in + (int64_t)mm * a.C) + ch);
+      if (a.pre_relu) {
+        v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+      }
+      *reinterpret_cast<float4*>(&xs[px * DX + ch * 4]) = v;
+    }
+    __syncthreads();
+    const float* xr = xs + tid * DX;
+#pragma unroll 4
+    for (int c = 0; c < a.C; c += 4) {
+      const float4 x = *reinterpret_cast<const float4*>(xr + c);
+      const float4* w4 = reinterpret_cast<const float4*>(wsm + c * KB);
+      constexpr int G = KB / 4;
+#pragma unroll
+      for (int k4 = 0; k4 < G; ++k4) {
+        const float4 w0 = w4[k4], w1 = w4[G + k4], w2 = w4[2 * G + k4], w3 = w4[3 * G + k4];
+        acc[4 * k4] = fmaf(x.x, w0.x, fmaf(x.y, w1.x, fmaf(x.z, w2.x, fmaf(x.w, w3.x, acc[4 * k4]))));
+        acc[4 * k4 + 1] = fmaf(x.x, w0.y, fmaf(x.y, w1.y, fmaf(x.z, w2.y, fmaf(x.w, w3.y, acc[4 * k4 + 1]))));
+        acc[4 * k4 + 2] = fmaf(x.x, w0.z, fmaf(x.y, w1.z, fmaf(x.z, w2.z, fmaf(x.w, w3.z, acc[4 * k4 + 2]))));
+        acc[4 * k4 + 3] = fmaf(x.x, w0.w, fmaf(x.y, w1.w, fmaf(x.z, w2.w, fmaf(x.w, w3.w, acc[4 * k4 + 3]))));
+      }
     }
   } else {
 #pragma unroll 1
@@ -427,12 +468,12 @@ static size_t simt_smem_bytes(int bm, int bn) {
 }
 
 void init_simt_kernels() {
-  cudaFuncSetAttribute(conv_direct_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8 + 128 * (8 + 4)) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16 + 128 * (16 + 4)) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32 + 128 * (32 + 4)) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8 + 128 * (8 + 4)) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16 + 128 * (16 + 4)) * 4);
-  cudaFuncSetAttribute(conv_direct_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32 + 128 * (32 + 4)) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8 + 128 * (8 + 4) + 128 * 72) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16 + 128 * (16 + 4) + 128 * 72) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32 + 128 * (32 + 4) + 128 * 72) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 8 + 8 + 128 * (8 + 4) + 128 * 72) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 16 + 16 + 128 * (16 + 4) + 128 * 72) * 4);
+  cudaFuncSetAttribute(conv_direct_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (576 * 32 + 32 + 128 * (32 + 4) + 128 * 72) * 4);
   for (int i = 0; i < kNumSimt; ++i)
     for (int j = 0; j < 2; ++j)
     {
@@ -455,7 +496,8 @@ int launch_conv(const sw_op_desc& op, void* stream) {
   if (op.variant == 9) {
     if (a.K > 32 || a.Kdim > 576 || a.split != 1) return (int)cudaErrorInvalidValue;
     const int kb = a.K <= 8 ? 8 : (a.K <= 16 ? 16 : 32);
-    const size_t smem = ((size_t)a.Kdim * kb + kb + 128 * (size_t)(kb + 4)) * sizeof(float);
+    size_t smem = ((size_t)a.Kdim * kb + kb + 128 * (size_t)(kb + 4)) * sizeof(float);
+    if (direct_stage_in(a)) smem += 128 * (size_t)direct_stage_ld(a.C) * sizeof(float);
     const dim3 grid((unsigned)cdiv(a.M, 128));
     const bool k3 = a.R == 3 && a.S == 3;
     if (kb == 8)

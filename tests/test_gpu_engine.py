@@ -192,6 +192,7 @@ def test_depthwise(c, k, s, p, h):
     (3, 32, 3, 2, 0, 45, False, False),    # NASNet conv0 shape: NCHW image, scalar channel loads
     (32, 11, 1, 1, 0, 37, True, True),     # stem conv_1x1: odd K, scalar stores, ReLU on load
     (44, 24, 1, 1, 0, 28, True, False),    # float4 loads and stores
+    (32, 8, 1, 1, 0, 19, True, False),     # staged input rows, ragged last CTA, no pre-ReLU
     (11, 13, 5, 2, 2, 23, True, True),     # odd everything, padding
 ])
 def test_direct_thin_conv(cin, cout, k, s, p, h, lead, relu):
