@@ -263,6 +263,10 @@ int sw_engine_stream(sw_engine* e, uint64_t* out_stream);
 /* Kernel selection support: device time (µs, mean of `reps` back-to-back
  * launches after one warm-up) of an op descriptor that is not in the table. */
 int sw_engine_time_op(sw_engine* e, const sw_op_desc* op, int32_t reps, double* out_us);
+/* Kernel selection support: launch an op descriptor that is not in the table
+ * once on the launch stream and wait for it (the autotuner checks a timed
+ * winner's output against a reference candidate's before keeping it). */
+int sw_engine_run_op(sw_engine* e, const sw_op_desc* op);
 /* Engine flags for subsequent captures / eager launches:
  * SW_ENGINE_PDL = programmatic dependent launch on same-stream kernel edges. */
 #define SW_ENGINE_PDL 1u

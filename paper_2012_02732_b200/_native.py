@@ -104,6 +104,7 @@ PROTOTYPES = {
     "sw_engine_profile_ops": (C.c_int, [C.c_void_p, i64, P64, i32, C.POINTER(C.c_double)]),
     "sw_engine_stream": (C.c_int, [C.c_void_p, PU64]),
     "sw_engine_time_op": (C.c_int, [C.c_void_p, C.POINTER(OpDesc), i32, C.POINTER(C.c_double)]),
+    "sw_engine_run_op": (C.c_int, [C.c_void_p, C.POINTER(OpDesc)]),
     "sw_engine_set_flags": (C.c_int, [C.c_void_p, C.c_uint32]),
     "sw_engine_add_input": (C.c_int, [C.c_void_p, u64, u64, i64]),
     "sw_engine_set_prefetch": (C.c_int, [C.c_void_p, u64, i64]),

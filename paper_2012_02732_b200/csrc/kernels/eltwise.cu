@@ -121,11 +121,8 @@ int launch_eltwise(const sw_op_desc& d, void* stream) {
   int64_t total = (int64_t)e.N * e.H * e.W * (v4 ? e.C / 4 : e.C);
   if (total == 0) return 0;
   int blocks = (int)cdiv(total, 256);
-  if (v4)
-    launch_k(ew_vec4_kernel, dim3(blocks), dim3(256), 0, st, 1, e, total);
-  else
-    launch_k(ew_scalar_kernel, dim3(blocks), dim3(256), 0, st, 1, e, total);
-  return (int)cudaGetLastError();
+  if (v4) return (int)launch_k(ew_vec4_kernel, dim3(blocks), dim3(256), 0, st, 1, e, total);
+  return (int)launch_k(ew_scalar_kernel, dim3(blocks), dim3(256), 0, st, 1, e, total);
 }
 
 // Global average pool: out[n, c] = mean_hw(relu?(a[n, h, w, c])).
@@ -195,12 +192,10 @@ int launch_global_pool(const sw_op_desc& d, void* stream) {
                   aligned16(d.ptrs[EP_A]);
   if (v4) {
     int64_t warps = (int64_t)e.N * (e.C / 4);
-    launch_k(global_pool_vec4_kernel, dim3((unsigned)cdiv(warps * 32, 256)), dim3(256), 0, st, 1, e);
-  } else {
-    dim3 grid((unsigned)cdiv(e.C, 128), (unsigned)e.N);
-    launch_k(global_pool_kernel, grid, dim3(128), 0, st, 1, e);
+    return (int)launch_k(global_pool_vec4_kernel, dim3((unsigned)cdiv(warps * 32, 256)), dim3(256), 0, st, 1, e);
   }
-  return (int)cudaGetLastError();
+  dim3 grid((unsigned)cdiv(e.C, 128), (unsigned)e.N);
+  return (int)launch_k(global_pool_kernel, grid, dim3(128), 0, st, 1, e);
 }
 
 }  // namespace sw
@@ -254,8 +249,8 @@ int launch_concat(const sw_op_desc& d, void* stream) {
   a.out = reinterpret_cast<float*>(d.ptrs[7]);
   int64_t total = (int64_t)a.N * a.hw * a.ctot;
   if (total == 0) return 0;
-  launch_k(concat_kernel, dim3((unsigned)cdiv(total, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 1, a, total);
-  return (int)cudaGetLastError();
+  return (int)launch_k(concat_kernel, dim3((unsigned)cdiv(total, 256)), dim3(256), 0,
+                       reinterpret_cast<cudaStream_t>(stream), 1, a, total);
 }
 
 // Diagnostic (SW_ENGINE_NULL_KERNELS): an empty task with the same PDL
@@ -342,7 +337,7 @@ int launch_l2_prefetch(const void* p, int64_t bytes, void* stream) {
   if (blocks > 148 * 2) blocks = 148 * 2;
   l2_prefetch_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const char*>(p), lines);
-  return (int)cudaGetLastError();
+  return (int)cudaPeekAtLastError();
 }
 
 int launch_io_copy(void* dst, const void* src, int64_t bytes, void* stream) {

@@ -188,13 +188,13 @@ static bool can_vec4(const SpatialArgs& a, const sw_op_desc& op, bool has_w) {
 // taps fully unrolled for the kernel sizes the networks use: all k*k loads of
 // a thread are in flight together (one memory round trip per output)
 template <int KIND, int VEC>
-static void launch_ks(int ks, int blocks, cudaStream_t st, const SpatialArgs& a, int64_t total) {
+static cudaError_t launch_ks(int ks, int blocks, cudaStream_t st, const SpatialArgs& a, int64_t total) {
   switch (ks) {
-    case 1: launch_k(spatial_kernel<KIND, VEC, 1>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
-    case 3: launch_k(spatial_kernel<KIND, VEC, 3>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
-    case 5: launch_k(spatial_kernel<KIND, VEC, 5>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
-    case 7: launch_k(spatial_kernel<KIND, VEC, 7>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
-    default: launch_k(spatial_kernel<KIND, VEC, 0>, dim3(blocks), dim3(256), 0, st, 1, a, total); break;
+    case 1: return launch_k(spatial_kernel<KIND, VEC, 1>, dim3(blocks), dim3(256), 0, st, 1, a, total);
+    case 3: return launch_k(spatial_kernel<KIND, VEC, 3>, dim3(blocks), dim3(256), 0, st, 1, a, total);
+    case 5: return launch_k(spatial_kernel<KIND, VEC, 5>, dim3(blocks), dim3(256), 0, st, 1, a, total);
+    case 7: return launch_k(spatial_kernel<KIND, VEC, 7>, dim3(blocks), dim3(256), 0, st, 1, a, total);
+    default: return launch_k(spatial_kernel<KIND, VEC, 0>, dim3(blocks), dim3(256), 0, st, 1, a, total);
   }
 }
 
@@ -208,11 +208,7 @@ static int launch_spatial(const sw_op_desc& op, void* stream) {
   if (total >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;  // 32-bit index math in the kernel
   int blocks = (int)cdiv(total, 256);
   const int ks = (a.R == a.S && (a.R == 1 || a.R == 3 || a.R == 5 || a.R == 7)) ? a.R : 0;
-  if (v4)
-    launch_ks<KIND, 4>(ks, blocks, st, a, total);
-  else
-    launch_ks<KIND, 1>(ks, blocks, st, a, total);
-  return (int)cudaGetLastError();
+  return (int)(v4 ? launch_ks<KIND, 4>(ks, blocks, st, a, total) : launch_ks<KIND, 1>(ks, blocks, st, a, total));
 }
 
 int launch_dwconv(const sw_op_desc& op, void* stream) { return launch_spatial<0>(op, stream); }

@@ -938,6 +938,7 @@ int launch_train(const sw_op_desc& d, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t* p = d.params;
   const uint64_t* q = d.ptrs;
+  cudaError_t err = cudaSuccess;  // the launch's own status (never a stale error of an earlier call)
   switch (d.kind) {
     case K_BN_STATS:
     case K_BN_BWD_REDUCE: {
@@ -947,7 +948,7 @@ int launch_train(const sw_op_desc& d, void* stream) {
         a.stats = reinterpret_cast<float*>(q[1]);
         a.running = reinterpret_cast<float*>(q[2]);
         a.ws = reinterpret_cast<double*>(q[7]);
-        launch_k(bn_reduce_kernel<0>, dim3(a.grid, (unsigned)cdiv(a.C, chan_tile((int)a.C))), dim3(kNT), 0, st, 1, a);
+        err = launch_k(bn_reduce_kernel<0>, dim3(a.grid, (unsigned)cdiv(a.C, chan_tile((int)a.C))), dim3(kNT), 0, st, 1, a);
       } else {
         a.dout = reinterpret_cast<const float*>(q[0]);
         a.y = reinterpret_cast<const float*>(q[1]);
@@ -955,7 +956,7 @@ int launch_train(const sw_op_desc& d, void* stream) {
         a.gamma = reinterpret_cast<const float*>(q[3]);
         a.dgamma = reinterpret_cast<float*>(q[4]);
         a.ws = reinterpret_cast<double*>(q[7]);
-        launch_k(bn_reduce_kernel<1>, dim3(a.grid, (unsigned)cdiv(a.C, chan_tile((int)a.C))), dim3(kNT), 0, st, 1, a);
+        err = launch_k(bn_reduce_kernel<1>, dim3(a.grid, (unsigned)cdiv(a.C, chan_tile((int)a.C))), dim3(kNT), 0, st, 1, a);
       }
       break;
     }
@@ -1008,7 +1009,7 @@ int launch_train(const sw_op_desc& d, void* stream) {
       a.gamma = reinterpret_cast<const float*>(q[2]);
       a.res = reinterpret_cast<const float*>(q[3]);
       a.out = reinterpret_cast<float*>(q[4]);
-      launch_k(bn_apply_kernel, dim3(elementwise_grid(a.M * a.C / 4)), dim3(kNT), 0, st, 1, a);
+      err = launch_k(bn_apply_kernel, dim3(elementwise_grid(a.M * a.C / 4)), dim3(kNT), 0, st, 1, a);
       break;
     }
     case K_BN_BWD_APPLY: {
@@ -1020,7 +1021,7 @@ int launch_train(const sw_op_desc& d, void* stream) {
       a.dgamma = reinterpret_cast<float*>(q[4]);
       a.res = reinterpret_cast<const float*>(q[5]);
       a.out = reinterpret_cast<float*>(q[6]);
-      launch_k(bn_bwd_apply_kernel, dim3(elementwise_grid(a.M * a.C)), dim3(kNT), 0, st, 1, a);
+      err = launch_k(bn_bwd_apply_kernel, dim3(elementwise_grid(a.M * a.C)), dim3(kNT), 0, st, 1, a);
       break;
     }
     case K_DW_DGRAD: {
@@ -1033,9 +1034,9 @@ int launch_train(const sw_op_desc& d, void* stream) {
                       (!a.has_res || aligned16(q[4]));
       const int64_t work = (int64_t)a.N * a.H * a.W * (v4 ? a.C / 4 : a.C);
       if (v4)
-        launch_k(dw_dgrad_kernel<4>, dim3(elementwise_grid(work)), dim3(kNT), 0, st, 1, a);
+        err = launch_k(dw_dgrad_kernel<4>, dim3(elementwise_grid(work)), dim3(kNT), 0, st, 1, a);
       else
-        launch_k(dw_dgrad_kernel<1>, dim3(elementwise_grid(work)), dim3(kNT), 0, st, 1, a);
+        err = launch_k(dw_dgrad_kernel<1>, dim3(elementwise_grid(work)), dim3(kNT), 0, st, 1, a);
       break;
     }
     case K_DW_WGRAD: {
@@ -1048,9 +1049,9 @@ int launch_train(const sw_op_desc& d, void* stream) {
       const int TC = chan_tile(a.C), RL = kNT / TC;
       const size_t smem = RL > 1 ? (size_t)RL * a.R * a.S * TC * sizeof(float) : 0;
       if (a.R == 3)
-        launch_k(dw_wgrad_kernel<3>, dim3(a.grid, (unsigned)cdiv(a.C, TC)), dim3(kNT), smem, st, 1, a);
+        err = launch_k(dw_wgrad_kernel<3>, dim3(a.grid, (unsigned)cdiv(a.C, TC)), dim3(kNT), smem, st, 1, a);
       else if (a.R == 5)
-        launch_k(dw_wgrad_kernel<5>, dim3(a.grid, (unsigned)cdiv(a.C, TC)), dim3(kNT), smem, st, 1, a);
+        err = launch_k(dw_wgrad_kernel<5>, dim3(a.grid, (unsigned)cdiv(a.C, TC)), dim3(kNT), smem, st, 1, a);
       else
         return (int)cudaErrorInvalidValue;
       break;
@@ -1092,22 +1093,22 @@ int launch_train(const sw_op_desc& d, void* stream) {
       g.partials_only = (int)p[GM_PARTIALS_ONLY];
       if (g.split > 1 && !g.ws) return (int)cudaErrorInvalidValue;
       if (d.kind == K_GEMM_REDUCE) {
-        launch_k(gemm_reduce_kernel, dim3((unsigned)cdiv(g.M * g.N, 32)), dim3(kNT), 0, st, 1, g);
+        err = launch_k(gemm_reduce_kernel, dim3((unsigned)cdiv(g.M * g.N, 32)), dim3(kNT), 0, st, 1, g);
         break;
       }
       dim3 grid((unsigned)cdiv(g.N, GBN), (unsigned)cdiv(g.M, GBM), (unsigned)g.split);
-      launch_k(gemm_kernel, grid, dim3(kNT), 0, st, 1, g);
+      err = launch_k(gemm_kernel, grid, dim3(kNT), 0, st, 1, g);
       break;
     }
     case K_XENT:
-      launch_k(xent_kernel, dim3(1), dim3(kNT), 0, st, 1, reinterpret_cast<const float*>(q[0]),
+      err = launch_k(xent_kernel, dim3(1), dim3(kNT), 0, st, 1, reinterpret_cast<const float*>(q[0]),
                reinterpret_cast<const int*>(q[1]), reinterpret_cast<float*>(q[2]),
                reinterpret_cast<float*>(q[3]), (int)p[0], (int)p[1], (int64_t)p[2]);
       break;
     case K_SGD: {
       if (!aligned16(q[0]) || !aligned16(q[1]) || !aligned16(q[2])) return (int)cudaErrorMisalignedAddress;
       const int64_t n = p[0];
-      launch_k(sgd_kernel, dim3(elementwise_grid(n / 4 + 1)), dim3(kNT), 0, st, 1, reinterpret_cast<float*>(q[0]),
+      err = launch_k(sgd_kernel, dim3(elementwise_grid(n / 4 + 1)), dim3(kNT), 0, st, 1, reinterpret_cast<float*>(q[0]),
                reinterpret_cast<const float*>(q[1]), reinterpret_cast<float*>(q[2]), n,
                bits_f((int)p[1]), bits_f((int)p[2]), bits_f((int)p[3]));
       break;
@@ -1128,18 +1129,18 @@ int launch_train(const sw_op_desc& d, void* stream) {
       a.out = reinterpret_cast<float*>(q[4]);
       a.zs = reinterpret_cast<const float*>(q[5]);
       const int64_t work = a.mode == 2 ? a.N * a.C * 32 : a.N * a.HW * a.C;
-      launch_k(ew_bwd_kernel, dim3((unsigned)cdiv(work, kNT)), dim3(kNT), 0, st, 1, a);
+      err = launch_k(ew_bwd_kernel, dim3((unsigned)cdiv(work, kNT)), dim3(kNT), 0, st, 1, a);
       break;
     }
     case K_TRANSPOSE: {
       const int rows = (int)p[0], cols = (int)p[1];
-      launch_k(transpose_kernel, dim3((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32)), dim3(kNT), 0, st, 1,
+      err = launch_k(transpose_kernel, dim3((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32)), dim3(kNT), 0, st, 1,
                reinterpret_cast<const float*>(q[0]), reinterpret_cast<float*>(q[1]), rows, cols);
       break;
     }
     default: return (int)cudaErrorInvalidValue;
   }
-  return (int)cudaGetLastError();
+  return (int)err;
 }
 
 }  // namespace sw

@@ -104,6 +104,7 @@ struct Slot {
   cudaGraphNode_t io_in = nullptr, io_out = nullptr;  // the main input / output staging nodes
   bool io_in_custom = false, io_out_custom = false;  // re-pointed at a caller buffer
   const void* io_in_ptr = nullptr;                    // the caller buffer it points at
+  bool with_io = false;                               // captured with host staging copies
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -112,6 +113,7 @@ struct Slot {
     node_task.clear();
     io_nodes.clear();
     io_in = io_out = nullptr;
+    with_io = false;
     io_in_custom = io_out_custom = false;
     io_in_ptr = nullptr;
   }
@@ -344,6 +346,7 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
   CU(cudaSetDevice(e->device));
   Slot& sl = e->slots[slot];
   sl.reset();
+  sl.with_io = with_io != 0;
   int rc = ensure_streams(e, n_streams);
   if (rc) return rc;
   int64_t max_event = -1;
@@ -579,7 +582,8 @@ int sw_engine_infer(sw_engine* e, int32_t slot, const void* host_in, void* host_
 // output.  Same results as n calls of sw_engine_infer; throughput, not latency.
 int sw_engine_infer_stream(sw_engine* e, int32_t slot, int64_t n, const uint64_t* host_in, const uint64_t* host_out) {
   if (slot < 0 || slot >= kSlots || !e->slots[slot].exec) return sw::fail(SW_VALUE_ERROR, "slot not captured");
-  if (e->slots[slot].io_in) return sw::fail(SW_VALUE_ERROR, "infer_stream needs a device-resident slot");
+  if (e->slots[slot].with_io) return sw::fail(SW_VALUE_ERROR, "infer_stream needs a device-resident slot");
+  if (n > 0 && (!host_in || !host_out)) return sw::fail(SW_VALUE_ERROR, "infer_stream: null buffer list");
   if (n <= 0) return SW_OK;
   CU(cudaSetDevice(e->device));
   if (!e->cstream) {
@@ -752,6 +756,14 @@ int sw_engine_profile_ops(sw_engine* e, int64_t n, const int64_t* order, int32_t
     int rc = sw_engine_time_op(e, &e->ops[order[i]], reps, &out_us[i]);
     if (rc) return rc;
   }
+  return SW_OK;
+}
+
+int sw_engine_run_op(sw_engine* e, const sw_op_desc* op) {
+  CU(cudaStreamSynchronize(e->launch));
+  int rc = launch_task(e, *op, e->launch);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(e->launch));
   return SW_OK;
 }
 

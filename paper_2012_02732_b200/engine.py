@@ -620,10 +620,42 @@ class Engine:
         with open(self.tuning_cache, "w") as fh:
             json.dump({"signature": self._signature, "picks": picks}, fh)
 
-    def _autotune(self, reps: int = 5):
-        """Time every conv task's candidate kernels in isolation; keep the fastest."""
+    def _out_tensor(self, t: Task) -> torch.Tensor:
+        """Device view of task t's output channel slice inside the arena."""
+        v = t.out
+        st = v.st
+        off = self.base_map[st.sid] - self.arena.data_ptr()
+        flat = self.arena[off: off + st.nbytes].view(torch.float32)
+        if st.nchw:
+            return flat.view(st.n, st.c, st.h, st.w)[:, v.c_off: v.c_off + v.c]
+        return flat.view(st.n, st.h, st.w, st.c)[..., v.c_off: v.c_off + v.c]
+
+    def _reference_candidate(self, t: Task, d) -> tuple[int, int, int] | None:
+        """The candidate a timed winner is checked against: the SIMT
+        implicit GEMM (heuristic tile) for convs, the plain tile variant 0
+        for fused sepconvs; None for kernels with a single implementation."""
+        p = d.params
+        if t.kind == "conv":
+            M = p[SP_N] * p[SP_P] * p[SP_Q]
+            v, split = pick_conv_variant(M, p[SP_K], p[SP_R] * p[SP_S] * p[SP_C], p[SP_R], p[SP_S],
+                                         (p[SP_PAD_H], p[SP_PAD_W]), (p[SP_STRIDE_H], p[SP_STRIDE_W]))
+            return (K_CONV, v, split)
+        if t.kind == "sepconv":
+            return (K_SEPCONV, 0, 1)
+        return None
+
+    def _autotune(self, reps: int = 5, rtol: float = 1e-4):
+        """Time every conv task's candidate kernels in isolation; keep the
+        fastest whose output matches the reference candidate's on the same
+        (seeded random) arena contents: |winner − ref| ≤ rtol · max(1, max|ref|).
+        A candidate that returns success but computes something else is
+        logged and skipped, never picked (tuning_rejected)."""
         lib = N.lib()
         us = C.c_double()
+        gen = torch.Generator(device=self.arena.device).manual_seed(1234)
+        words = self.arena.numel() // 4
+        self.arena[: 4 * words].view(torch.float32).normal_(generator=gen)
+        self.tuning_rejected = {}
         for t in self.program.tasks:
             if t.kind not in ("conv", "sepconv", "sep2"):
                 continue
@@ -632,7 +664,6 @@ class Engine:
             M = p[SP_N] * p[SP_P] * p[SP_Q]
             K = p[SP_K]
             Kdim = p[SP_R] * p[SP_S] * p[SP_C]
-            best = None
             trial = N.OpDesc()
             C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
             if t.kind == "sep2":
@@ -645,6 +676,7 @@ class Engine:
                           if SEP_TMA_FIRST <= v < SEP_ROW_FIRST and 2 <= math.ceil(K / bn) <= 8]
             else:
                 cands = conv_candidates(M, K, Kdim, p[SP_R], p[SP_S], (p[SP_PAD_H], p[SP_PAD_W]))
+            timed = []
             for kind, variant, split in cands:
                 trial.kind = kind
                 trial.variant = variant
@@ -655,10 +687,30 @@ class Engine:
                 self.tuning_log.setdefault(t.tid, []).append(
                     (kind, variant, split, us.value if rc == 0 else None,
                      None if rc == 0 else lib.sw_last_error().decode()))
-                if rc != 0:
-                    continue
-                if best is None or us.value < best[0]:
-                    best = (us.value, kind, variant, split)
+                if rc == 0:
+                    timed.append((us.value, kind, variant, split))
+            timed.sort()
+            ref_cand = self._reference_candidate(t, d)
+            ref_out = None
+            if ref_cand is not None and timed:
+                trial.kind, trial.variant = ref_cand[0], ref_cand[1]
+                trial.params[SP_SPLIT_K] = ref_cand[2]
+                N.check(lib.sw_engine_run_op(self._h, C.byref(trial)))
+                ref_out = self._out_tensor(t).clone()
+                tol = rtol * max(1.0, ref_out.abs().max().item())
+            best = None
+            for cand in timed:
+                if ref_out is not None and cand[1:] != ref_cand:
+                    trial.kind, trial.variant = cand[1], cand[2]
+                    trial.params[SP_SPLIT_K] = cand[3]
+                    self._out_tensor(t).fill_(float("nan"))
+                    N.check(lib.sw_engine_run_op(self._h, C.byref(trial)))
+                    err = (self._out_tensor(t) - ref_out).abs().max().item()
+                    if not err <= tol:  # NaN-safe
+                        self.tuning_rejected.setdefault(t.tid, []).append((cand[1:], err))
+                        continue
+                best = cand
+                break
             if best is not None:
                 d.kind, d.variant = best[1], best[2]
                 d.params[SP_SPLIT_K] = best[3]
@@ -823,6 +875,16 @@ class Engine:
                 raise ValueError("infer_stream: contiguous fp32 host tensors of the prepared input size")
         if outs is None:
             outs = [torch.empty(self.out_shape, dtype=torch.float32, pin_memory=True) for _ in xs]
+        else:
+            outs = list(outs)
+            if len(outs) != len(xs):
+                raise ValueError(f"infer_stream: {len(outs)} output buffers for {len(xs)} requests")
+            n_out = math.prod(self.out_shape)
+            for o in outs:
+                if not (isinstance(o, torch.Tensor) and o.device.type == "cpu" and o.dtype == torch.float32
+                        and o.is_contiguous() and o.numel() == n_out):
+                    raise ValueError("infer_stream: outs must be contiguous fp32 host tensors of "
+                                     f"{n_out} elements ({self.out_shape})")
         hi = np.array([x.data_ptr() for x in xs], dtype=np.int64)
         ho = np.array([o.data_ptr() for o in outs], dtype=np.int64)
         slot = SLOT_MULTI if self.multi_stream else SLOT_SINGLE

@@ -83,7 +83,8 @@ def test_lowered_ops_emulated_match_cpu_forward(programs, name, fuse):
         ref = model(x)
     y, prog, ops = emulate(model, x, fuse=fuse)
     assert y.shape == ref.shape
-    torch.testing.assert_close(y, ref, rtol=1e-4, atol=1e-5 * max(1.0, ref.abs().max().item()))
+    # BN folding re-rounds every layer: ~1e-5 abs on O(1) logits after 50+ layers
+    torch.testing.assert_close(y, ref, rtol=1e-4, atol=1e-4)
 
 
 def test_single_stream_emulation_equals_multi(programs):

@@ -171,3 +171,19 @@ def test_cli_assign_matches_the_reference_bytes(tmp_path):
     out = subprocess.run([sys.executable, "-m", "paper_2012_02732_b200", "assign", str(gp)], cwd=root,
                          capture_output=True, text=True, check=True).stdout.strip()
     assert out == case["assign"]
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="CPU-only host behaviour")
+def test_engine_without_gpu_raises_cuda_error():
+    """No CPU fallback: on a host without a CUDA device the engine's prepare
+    and call raise CudaError (the C ABI's SW_CUDA_ERROR class) and nothing
+    is computed on the CPU."""
+    from paper_2012_02732_b200.engine import Engine
+    from paper_2012_02732_b200.networks import InceptionCell, example_input
+    model = InceptionCell().eval()
+    x = example_input((1, 3, 32, 32))
+    with pytest.raises(sw.CudaError):
+        Engine(model).prepare(x)
+    with pytest.raises(sw.CudaError):
+        Engine(model)(x)
+    assert sw.CudaError.__mro__[1] is sw.StreamWeaveError
