@@ -19,11 +19,11 @@
  * bound to one device and is not re-entrant.
  *
  * Reference interfaces replaced (file:line under /root/reference/pkg/src/streamweave):
- *   graph.py:209   validate_graph            -> sw_plan_validate
- *   graph.py:298   topological_order         -> sw_plan_topological_order
- *   graph.py:349   transitive_closure        -> sw_plan_transitive_closure
- *   graph.py:373   minimum_equivalent_graph  -> sw_plan_minimum_equivalent_graph
- *   graph.py:389   critical_path_time        -> sw_plan_critical_path_time
+ *   graph.py:111   validate_graph            -> sw_plan_validate
+ *   graph.py:200   topological_order         -> sw_plan_topological_order
+ *   graph.py:251   transitive_closure        -> sw_plan_transitive_closure
+ *   graph.py:275   minimum_equivalent_graph  -> sw_plan_minimum_equivalent_graph
+ *   graph.py:291   critical_path_time        -> sw_plan_critical_path_time
  *   assign.py:82   maximum_matching          -> sw_plan_maximum_matching
  *   assign.py:105  validate_matching         -> sw_plan_assignment_from_matching (checks)
  *   assign.py:138  assignment_from_matching  -> sw_plan_assignment_from_matching
@@ -32,9 +32,9 @@
  *   assign.py:212  plan_is_safe              -> sw_plan_plan_is_safe
  *   assign.py:233  assign_streams            -> sw_plan_assign_streams
  *   assign.py:243  fold_streams              -> sw_plan_fold_streams
- *   schedule.py:352 pre_run                  -> sw_plan_pre_run
- *   schedule.py:417 reserve_arena            -> sw_plan_reserve_arena
- *   sim.py:256/261 simulate / run_framework_mode -> sw_plan_simulate
+ *   schedule.py:53 pre_run                  -> sw_plan_pre_run
+ *   schedule.py:118 reserve_arena            -> sw_plan_reserve_arena
+ *   sim.py:64/69 simulate / run_framework_mode -> sw_plan_simulate
  *   (the CUDA Stream Capture / Graph Launch step the
  *    package abstracted into TaskSchedule)   -> sw_engine_capture / sw_engine_replay
  */
@@ -80,7 +80,7 @@ const char* sw_last_error(void);
 /* Library version string. */
 const char* sw_version(void);
 
-/* A task graph (graph.py:163-206: CompGraph / TaskNode / MemEvent), in the
+/* A task graph (graph.py:57-108: CompGraph / TaskNode / MemEvent), in the
  * caller's node order and edge order (the reference semantics depend on both). */
 typedef struct sw_graph_view {
   int64_t n_nodes;
@@ -158,7 +158,7 @@ typedef struct sw_schedule_out {
 int sw_plan_pre_run(const sw_graph_view* g, const sw_assignment_view* f, int64_t n_plan,
                     const int64_t* plan, sw_schedule_out* out);
 
-/* First-fit over a linear trace (schedule.py:417-454). Keys are caller
+/* First-fit over a linear trace (schedule.py:118-155). Keys are caller
  * integers; out_offset[i] is written for alloc events; on a key error
  * *out_bad_event is the failing event index (for the caller's message). */
 int sw_plan_reserve_arena(int64_t n_events, const int64_t* keys, const int32_t* kinds,

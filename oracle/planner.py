@@ -32,14 +32,14 @@ class OracleError(Exception):
 
 
 def build(nodes, edges):
-    """CompGraph.build: nodes sorted by id (stable), edges sorted (graph.py:170-175)."""
+    """CompGraph.build: nodes sorted by id (stable), edges sorted (graph.py:73-77)."""
     nodes = sorted(((int(n[0]), int(n[1]), int(n[2]), tuple(n[3])) for n in nodes),
                    key=lambda t: t[0])
     return nodes, sorted((int(u), int(v)) for u, v in edges)
 
 
 def graph_from_obj(doc):
-    """Plain graph from the reference JSON document shape (graph.py:423-447)."""
+    """Plain graph from the reference JSON document shape (graph.py:325-349)."""
     nodes = []
     for it in doc.get("nodes", []):
         mem = []
@@ -63,7 +63,7 @@ def _succ(nodes, edges):
 # --- graph.py ---------------------------------------------------------------
 
 def validate(nodes, edges):
-    """validate_graph (graph.py:209-234) incl. _validate_mem (:237-252)."""
+    """validate_graph (graph.py:111-136) incl. _validate_mem (:237-252)."""
     ids = set()
     for nid, _d, _q, mem in nodes:
         if nid in ids:
@@ -102,7 +102,7 @@ def validate(nodes, edges):
 
 
 def find_cycle(nodes, edges):
-    """Three-colour DFS, roots ascending, witness [v..v] (graph.py:264-295)."""
+    """Three-colour DFS, roots ascending, witness [v..v] (graph.py:166-197)."""
     succ = _succ(nodes, edges)
     state = {n[0]: 0 for n in nodes}
     up = {}
@@ -134,7 +134,7 @@ def find_cycle(nodes, edges):
 
 
 def topo(nodes, edges):
-    """Min-heap Kahn order (graph.py:298-317)."""
+    """Min-heap Kahn order (graph.py:200-219)."""
     succ = _succ(nodes, edges)
     indeg = {n[0]: 0 for n in nodes}
     for _, v in edges:
@@ -155,7 +155,7 @@ def topo(nodes, edges):
 
 
 def closure(nodes, edges):
-    """Reachability rows by id rank, reverse topo accumulation (graph.py:349-359).
+    """Reachability rows by id rank, reverse topo accumulation (graph.py:251-261).
 
     Returns (rank, rows) where rows[rank[u]] is a Python-int bitmask.
     """
@@ -177,7 +177,7 @@ def reaches(cl, u, v):
 
 
 def meg(nodes, edges, cl=None):
-    """Minimum equivalent graph: keep (u,v) unless a sibling succ reaches v (graph.py:373-386)."""
+    """Minimum equivalent graph: keep (u,v) unless a sibling succ reaches v (graph.py:275-288)."""
     cl = cl or closure(nodes, edges)
     succ = _succ(nodes, edges)
     kept = [(u, v) for u, v in edges
@@ -186,7 +186,7 @@ def meg(nodes, edges, cl=None):
 
 
 def critical_path(nodes, edges):
-    """Longest duration path (graph.py:389-399)."""
+    """Longest duration path (graph.py:291-301)."""
     if not nodes:
         return 0
     dur = {n[0]: n[1] for n in nodes}
@@ -379,7 +379,7 @@ def assignment_json(nodes, edges, stream_of, plan, meg_edges):
 # --- schedule.py ------------------------------------------------------------
 
 def first_fit(live, size):
-    """_first_fit (schedule.py:447-454 region: lowest gap among sorted live blocks)."""
+    """_first_fit (schedule.py:148-155 region: lowest gap among sorted live blocks)."""
     off = 0
     for start, length in sorted(live):
         if off + size <= start:
@@ -389,7 +389,7 @@ def first_fit(live, size):
 
 
 def arena(trace):
-    """reserve_arena (schedule.py:417-444): trace of (key, kind, arg)."""
+    """reserve_arena (schedule.py:118-145): trace of (key, kind, arg)."""
     live, placed, total = {}, {}, 0
     for key, kind, arg in trace:
         if kind == "alloc":
@@ -410,7 +410,7 @@ def arena(trace):
 
 
 def pre_run(nodes, edges, stream_of, plan):
-    """pre_run (schedule.py:352-414).
+    """pre_run (schedule.py:53-115).
 
     Returns dict(streams=[[(kind, arg)]], events, arena_total, blocks,
     task_args, order).
@@ -462,7 +462,7 @@ def pre_run(nodes, edges, stream_of, plan):
 
 
 def schedule_json(s):
-    """schedule_to_json (schedule.py:473-487)."""
+    """schedule_to_json (schedule.py:174-188)."""
     doc = {
         "streams": [[{k: a} for k, a in fifo] for fifo in s["streams"]],
         "events": s["events"],
@@ -475,7 +475,7 @@ def schedule_json(s):
 
 
 def graph_json(nodes, edges, labels=None):
-    """graph_to_json (graph.py:404-420) for nodes without labels unless given."""
+    """graph_to_json (graph.py:306-322) for nodes without labels unless given."""
     out = []
     for nid, d, q, mem in nodes:
         item = {"id": nid}

@@ -1,6 +1,6 @@
 """Happens-before-aware device arena (hard part H3).
 
-The reference arena (`reserve_arena`, schedule.py:417-454) is first-fit over
+The reference arena (`reserve_arena`, schedule.py:118-155) is first-fit over
 the *linear* capture trace: a block freed by task X may be handed to a task Y
 that runs concurrently with X on another stream — a race on a GPU.
 The engine therefore used it only in its "never free" form (every activation

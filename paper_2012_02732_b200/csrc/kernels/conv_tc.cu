@@ -145,7 +145,21 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// Round-to-nearest TF32 (cvt.rna): the 3xTF32 split x = hi + lo with
+// hi = rn(x), lo = rn(x - hi) leaves an unbiased residual <= 2^-22 |x|.
+// (A truncating split leaves a residual up to 2^-20 |x| with the sign of x,
+// so the dropped parts of every product shrink it the same way and a dot
+// product of non-negative activations inherits a coherent ~1e-6 relative
+// bias per layer.)
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void split_tf32(float4 x, float4& h, float4& l) {
+  h = make_float4(tf32_rn(x.x), tf32_rn(x.y), tf32_rn(x.z), tf32_rn(x.w));
+  l = make_float4(tf32_rn(x.x - h.x), tf32_rn(x.y - h.y), tf32_rn(x.z - h.z), tf32_rn(x.w - h.w));
+}
 
 __device__ __forceinline__ void tc_epilogue_store(const TcArgs& a, int m, int n, float v) {
   const int q = m % a.Q;
@@ -161,7 +175,7 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;  // fp32 per stage row = 8 chunks of 16 B = 4 MMA K-steps
 constexpr int TC_THREADS = 128;
 
-template <int BN, int SOVR = 0>
+template <int BN, int SOVR = 0, int CPS = (SOVR ? 2 : 1)>  // CPS: CTAs resident per SM
 struct TcSmem {
   static constexpr int A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 4;
@@ -175,8 +189,111 @@ struct TcSmem {
   // persistent kernel: the epilogue tile sits past the ring (loads stay in flight)
   static constexpr int P_BODY = OPER + PART;
   static constexpr int P_TOTAL = P_BODY + 128;
-  static constexpr int NCOLS = BN < 32 ? 32 : BN;
+  // Accumulation precision.  The tensor pipe's fp32 accumulation truncates,
+  // so one TMEM accumulator over a long K drifts toward zero
+  // (tools/tc_precision.cu: 25x the FFMA rms error at K = 4096).
+  //  * PROMO (BN <= 128): every K tile's 3xTF32 products go into a fresh TMEM
+  //    accumulator (ping-pong pair); while the tensor pipe works on tile i
+  //    the threads add tile i-1's accumulator into fp32 registers
+  //    (round-to-nearest), so no TMEM chain is longer than 12 MMAs — more
+  //    accurate than a sequential FFMA dot product.
+  //  * BN = 256 (no room for 256 register accumulators): ACC accumulators for
+  //    the hi·hi products (K tile kt goes to kt % ACC) + one for the hi·lo +
+  //    lo·hi corrections, summed in fp32 by the epilogue.
+  static constexpr bool PROMO = BN <= 128;
+  static constexpr int COLS_CTA = CPS > 1 ? 256 : 512;
+  static constexpr int ACC = (COLS_CTA / (BN < 32 ? 32 : BN)) - 1 > 0 ? (COLS_CTA / (BN < 32 ? 32 : BN)) - 1 : 1;
+  static constexpr int NCOLS = PROMO ? (2 * BN < 32 ? 32 : 2 * BN) : COLS_CTA;
 };
+
+// Issue the 3xTF32 MMAs of one K tile (ksteps of 8): hi·hi into accumulator
+// kt % ACC, hi·lo + lo·hi into the correction accumulator (column ACC*BN).
+template <int ACC, int BN>
+__device__ __forceinline__ void mma_ktile_3xtf32(uint32_t tmem, int kt, const uint64_t (&ah)[4],
+                                                 const uint64_t (&al)[4], const uint64_t (&bh)[4],
+                                                 const uint64_t (&bl)[4], uint32_t idesc) {
+  const uint32_t dh = tmem + (uint32_t)((kt % ACC) * BN);
+  const uint32_t dc = tmem + (uint32_t)(ACC * BN);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    mma_tf32(dh, ah[ks], bh[ks], idesc, (kt >= ACC || ks) ? 1u : 0u);
+    mma_tf32(dc, ah[ks], bl[ks], idesc, (kt | ks) ? 1u : 0u);
+    mma_tf32(dc, al[ks], bh[ks], idesc, 1u);
+  }
+}
+
+// PROMO: all 12 MMAs of one K tile into one fresh accumulator `d`.
+__device__ __forceinline__ void mma_ktile_fresh(uint32_t d, const uint64_t (&ah)[4], const uint64_t (&al)[4],
+                                                const uint64_t (&bh)[4], const uint64_t (&bl)[4], uint32_t idesc) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    mma_tf32(d, ah[ks], bh[ks], idesc, ks ? 1u : 0u);
+    mma_tf32(d, ah[ks], bl[ks], idesc, 1u);
+    mma_tf32(d, al[ks], bh[ks], idesc, 1u);
+  }
+}
+
+template <int ACC, int BN, bool PROMO>
+__device__ __forceinline__ void mma_ktile(uint32_t tmem, int kt, const uint64_t (&ah)[4], const uint64_t (&al)[4],
+                                          const uint64_t (&bh)[4], const uint64_t (&bl)[4], uint32_t idesc) {
+  if constexpr (PROMO)
+    mma_ktile_fresh(tmem + (uint32_t)((kt & 1) * BN), ah, al, bh, bl, idesc);
+  else
+    mma_ktile_3xtf32<ACC, BN>(tmem, kt, ah, al, bh, bl, idesc);
+}
+
+// PROMO: racc += this warp's TMEM lanes of the accumulator at column `col`.
+template <int BN>
+__device__ __forceinline__ void tmem_promote(uint32_t t_row, uint32_t col, float (&racc)[BN]) {
+#pragma unroll
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    float v[32];
+    tmem_ld16x2(t_row + col + (uint32_t)c0, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) racc[c0 + j] += v[j];
+  }
+}
+
+// 32 accumulator columns [c0, c0 + 32) of this warp's TMEM lanes, summed over
+// the nacc used hi·hi accumulators and the correction accumulator.
+template <int ACC, int BN>
+__device__ __forceinline__ void tmem_sum32(uint32_t t_row, int c0, int nacc, float (&v)[32]) {
+  tmem_ld16x2(t_row + (uint32_t)(ACC * BN + c0), v);
+#pragma unroll 1
+  for (int r = 0; r < nacc; ++r) {
+    float w[32];
+    tmem_ld16x2(t_row + (uint32_t)(r * BN + c0), w);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += w[j];
+  }
+}
+
+
+// End of a tile: the fp32 result rows → the smem tile `part` [128][PS]
+// (PROMO: the register accumulators; else the TMEM accumulator sum).
+template <class L, int BN>
+__device__ __forceinline__ void drain_to_part(uint32_t t_row, int row, int iters, const float (&racc)[L::PROMO ? BN : 1],
+                                              float* part) {
+  if constexpr (L::PROMO) {
+#pragma unroll
+    for (int j = 0; j < BN; j += 4)
+      *reinterpret_cast<float4*>(&part[row * L::PS + j]) = make_float4(racc[j], racc[j + 1], racc[j + 2], racc[j + 3]);
+  } else {
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      if (iters > 0) {
+        tmem_sum32<L::ACC, BN>(t_row, c0, min(iters, L::ACC), v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(&part[row * L::PS + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  }
+}
 
 }  // namespace
 
@@ -215,6 +332,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int row = warp * 32 + lane;
+  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  float racc[L::PROMO ? BN : 1];
+#pragma unroll
+  for (int j = 0; j < (L::PROMO ? BN : 1); ++j) racc[j] = 0.f;
 
   // Loader mapping: thread owns 16-byte K chunk (tid % 8) of rows tid/8 + 16*i.
   const int chunk = tid & 7;
@@ -318,9 +440,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
         if (a.pre_relu) {
           x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
         }
-        const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+        float4 h, l;
+        split_tf32(x, h, l);
         hi[i] = h;
-        lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        lo[i] = l;
       }
     }
     fence_proxy_async();
@@ -330,16 +453,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
       const uint32_t a_hi = sbase + st * L::STAGE, a_lo = a_hi + L::A_BYTES;
       const uint32_t b_hi = a_hi + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
       constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
+      uint64_t ah[4], al[4], bh[4], bl[4];
 #pragma unroll
       for (int ks = 0; ks < TC_BK / 8; ++ks) {
-        const uint64_t ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
-        const uint64_t al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
-        const uint64_t bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
-        const uint64_t bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
-        mma_tf32(tmem, ah, bh, idesc, (it | ks) ? 1u : 0u);
-        mma_tf32(tmem, ah, bl, idesc, 1u);
-        mma_tf32(tmem, al, bh, idesc, 1u);
+        ah[ks] = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
+        al[ks] = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
+        bh[ks] = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
+        bl[ks] = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
       }
+      mma_ktile<L::ACC, BN, L::PROMO>(tmem, it, ah, al, bh, bl, idesc);
       mma_commit(smem_u32(&mbar[st]));
     }
     // refill the stage of the PREVIOUS tile (its MMAs have had a whole
@@ -350,34 +472,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(TcArgs a) {
       issue(it - 1 + S, ps, 3);
     }
     cp_commit();
+    if constexpr (L::PROMO) {  // tile it-1's accumulator → registers while tile it's MMAs run
+      if (it >= 1) {
+        mbar_wait(smem_u32(&mbar[(it - 1) % S]), ((it - 1) / S) & 1);
+        tc_fence_after();
+        tmem_promote<BN>(t_row, (uint32_t)(((it - 1) & 1) * BN), racc);
+        tc_fence_before();
+      }
+    }
   }
   if (iters > 0) {
     const int last = iters - 1;
     mbar_wait(smem_u32(&mbar[last % S]), (last / S) & 1);
+    tc_fence_after();
+    if constexpr (L::PROMO) tmem_promote<BN>(t_row, (uint32_t)((last & 1) * BN), racc);
   }
   tc_fence_after();
   probe_pt(4);
 
-  // TMEM → smem tile (rows = TMEM lanes) → one rolled epilogue loop, shared
-  // with the split-K DSMEM reduction
-  const int row = warp * 32 + lane;
-  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  // accumulators → smem tile (rows = TMEM lanes) → one rolled epilogue loop,
+  // shared with the split-K DSMEM reduction
   float* part = reinterpret_cast<float*>(smem);  // [128][BN]; operands are dead now
   __syncthreads();
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    // two 16-column TMEM loads in flight per wait (BN >= 32)
-    float v[32];
-    if (iters > 0) {
-      tmem_ld16x2(t_row + c0, v);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; j += 4)
-      *reinterpret_cast<float4*>(&part[row * L::PS + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-  }
+  drain_to_part<L, BN>(t_row, row, iters, racc, part);
   probe_pt(5);
   cg::cluster_group cluster = cg::this_cluster();
   tile_epilogue<TC_BM, BN, TC_THREADS, L::PS>(a.epi, part, m0, n0, a.split, cluster);
@@ -454,6 +571,11 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int row = warp * 32 + lane;
+  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  float racc[L::PROMO ? BN : 1];
+#pragma unroll
+  for (int j = 0; j < (L::PROMO ? BN : 1); ++j) racc[j] = 0.f;
 
   auto load_b = [&](int kt, int st) {
     const uint32_t stage = sbase + st * L::STAGE;
@@ -500,9 +622,10 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
         if (a.pre_relu) {
           x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
         }
-        const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+        float4 h, l;
+        split_tf32(x, h, l);
         hi[i] = h;
-        lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        lo[i] = l;
       }
     }
     fence_proxy_async();
@@ -512,24 +635,22 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
       const uint32_t a_hi = sbase + st * L::STAGE, a_lo = a_hi + L::A_BYTES;
       const uint32_t b_hi = a_hi + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
       constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
+      uint64_t ah[4], al[4], bh[4], bl[4];
 #pragma unroll
       for (int ks = 0; ks < TC_BK / 8; ++ks) {
-        uint64_t ah, al, bh, bl;
         if constexpr (SWZ) {
-          ah = make_desc_sw128(a_hi + ks * 32);
-          al = make_desc_sw128(a_lo + ks * 32);
-          bh = make_desc_sw128(b_hi + ks * 32);
-          bl = make_desc_sw128(b_lo + ks * 32);
+          ah[ks] = make_desc_sw128(a_hi + ks * 32);
+          al[ks] = make_desc_sw128(a_lo + ks * 32);
+          bh[ks] = make_desc_sw128(b_hi + ks * 32);
+          bl[ks] = make_desc_sw128(b_lo + ks * 32);
         } else {
-          ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
-          al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
-          bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
-          bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+          ah[ks] = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
+          al[ks] = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
+          bh[ks] = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
+          bl[ks] = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
         }
-        mma_tf32(tmem, ah, bh, idesc, (it | ks) ? 1u : 0u);
-        mma_tf32(tmem, ah, bl, idesc, 1u);
-        mma_tf32(tmem, al, bh, idesc, 1u);
       }
+      mma_ktile<L::ACC, BN, L::PROMO>(tmem, it, ah, al, bh, bl, idesc);
       mma_commit(smem_u32(&done[st]));
       // refill the stage the PREVIOUS tile's MMAs are releasing
       if (it >= 1 && it - 1 + S < iters) {
@@ -540,30 +661,25 @@ __global__ void __launch_bounds__(TC_THREADS, SOVR ? 2 : 1)
         load_a(it - 1 + S, ps);
       }
     }
+    if constexpr (L::PROMO) {  // tile it-1's accumulator → registers while tile it's MMAs run
+      if (it >= 1) {
+        mbar_wait(smem_u32(&done[(it - 1) % S]), ((it - 1) / S) & 1);
+        tc_fence_after();
+        tmem_promote<BN>(t_row, (uint32_t)(((it - 1) & 1) * BN), racc);
+        tc_fence_before();
+      }
+    }
   }
   if (iters > 0) {
     const int last = iters - 1;
     mbar_wait(smem_u32(&done[last % S]), (last / S) & 1);
+    tc_fence_after();
+    if constexpr (L::PROMO) tmem_promote<BN>(t_row, (uint32_t)((last & 1) * BN), racc);
   }
   tc_fence_after();
-  const int row = warp * 32 + lane;
-  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
   float* part = reinterpret_cast<float*>(smem);
   __syncthreads();
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    // two 16-column TMEM loads in flight per wait (BN >= 32)
-    float v[32];
-    if (iters > 0) {
-      tmem_ld16x2(t_row + c0, v);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < 32; j += 4)
-      *reinterpret_cast<float4*>(&part[row * L::PS + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-  }
+  drain_to_part<L, BN>(t_row, row, iters, racc, part);
   cg::cluster_group cluster = cg::this_cluster();
   tile_epilogue<TC_BM, BN, TC_THREADS, L::PS>(a.epi, part, m0, n0, a.split, cluster);
   tc_fence_before();
@@ -586,7 +702,7 @@ template <int BN, bool SWZ = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     conv_tc_tma_persistent_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                                   const __grid_constant__ CUtensorMap tbl, TcArgs a) {
-  using L = TcSmem<BN, BN == 128 ? 2 : 0>;  // 2 x 64 KB ring + 66 KB tile for BN = 128
+  using L = TcSmem<BN, BN == 128 ? 2 : 0, 1>;  // 2 x 64 KB ring + 66 KB tile for BN = 128
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::P_BODY);
@@ -661,6 +777,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
   float* part = reinterpret_cast<float*>(smem + S * L::STAGE);  // past the ring: loads stay in flight
   cg::cluster_group cluster = cg::this_cluster();
+  float racc[BN];
+#pragma unroll
+  for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+  auto flush_tile = [&](int qq) {  // registers → part → epilogue; restart the accumulation
+    drain_to_part<L, BN>(t_row, row, iters, racc, part);
+#pragma unroll
+    for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+    const int m0 = ((int)blockIdx.x + (qq / iters) * (int)gridDim.x) * TC_BM;
+    tile_epilogue<TC_BM, BN, TC_THREADS, L::PS>(a.epi, part, m0, n0, 1, cluster);
+    __syncthreads();  // part is rewritten by the next tile
+  };
 #pragma unroll 1
   for (int q = 0; q < total; ++q) {
     const int st = q % S;
@@ -675,9 +802,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (a.pre_relu) {
           x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
         }
-        const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+        float4 h, l;
+        split_tf32(x, h, l);
         hi[i] = h;
-        lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        lo[i] = l;
       }
     }
     fence_proxy_async();
@@ -687,24 +815,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t a_hi = sbase + st * L::STAGE, a_lo = a_hi + L::A_BYTES;
       const uint32_t b_hi = a_hi + 2 * L::A_BYTES, b_lo = b_hi + L::B_BYTES;
       constexpr uint32_t LBO_A = TC_BM * 16, LBO_B = BN * 16, SBO = 128;
+      uint64_t ah[4], al[4], bh[4], bl[4];
 #pragma unroll
       for (int ks = 0; ks < TC_BK / 8; ++ks) {
-        uint64_t ah, al, bh, bl;
         if constexpr (SWZ) {
-          ah = make_desc_sw128(a_hi + ks * 32);
-          al = make_desc_sw128(a_lo + ks * 32);
-          bh = make_desc_sw128(b_hi + ks * 32);
-          bl = make_desc_sw128(b_lo + ks * 32);
+          ah[ks] = make_desc_sw128(a_hi + ks * 32);
+          al[ks] = make_desc_sw128(a_lo + ks * 32);
+          bh[ks] = make_desc_sw128(b_hi + ks * 32);
+          bl[ks] = make_desc_sw128(b_lo + ks * 32);
         } else {
-          ah = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
-          al = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
-          bh = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
-          bl = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
+          ah[ks] = make_desc(a_hi + ks * 2 * LBO_A, LBO_A, SBO);
+          al[ks] = make_desc(a_lo + ks * 2 * LBO_A, LBO_A, SBO);
+          bh[ks] = make_desc(b_hi + ks * 2 * LBO_B, LBO_B, SBO);
+          bl[ks] = make_desc(b_lo + ks * 2 * LBO_B, LBO_B, SBO);
         }
-        mma_tf32(tmem, ah, bh, idesc, (kt | ks) ? 1u : 0u);
-        mma_tf32(tmem, ah, bl, idesc, 1u);
-        mma_tf32(tmem, al, bh, idesc, 1u);
       }
+      mma_ktile<L::ACC, BN, L::PROMO>(tmem, L::PROMO ? q : kt, ah, al, bh, bl, idesc);
       mma_commit(smem_u32(&done[st]));
       if (q >= 1 && q - 1 + S < total) {  // refill the stage the previous MMAs released
         const int ps = (q - 1) % S;
@@ -714,22 +840,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         load_a(q - 1 + S, ps);
       }
     }
-    if (kt == iters - 1) {  // tile complete: drain the accumulator while the next tile's stages load
-      mbar_wait(smem_u32(&done[st]), (q / S) & 1);
+    // PROMO: k-tile q-1's accumulator → registers while k-tile q's MMAs run;
+    // a finished tile goes through the epilogue right after its last k-tile
+    static_assert(L::PROMO, "persistent kernel: BN <= 128");
+    if (q >= 1) {
+      mbar_wait(smem_u32(&done[(q - 1) % S]), ((q - 1) / S) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld16x2(t_row + c0, v);
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4*>(&part[row * L::PS + c0 + j]) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-      }
+      tmem_promote<BN>(t_row, (uint32_t)(((q - 1) & 1) * BN), racc);
       tc_fence_before();
-      const int m0 = ((int)blockIdx.x + (q / iters) * (int)gridDim.x) * TC_BM;
-      tile_epilogue<TC_BM, BN, TC_THREADS, L::PS>(a.epi, part, m0, n0, 1, cluster);
-      __syncthreads();  // part is rewritten by the next tile; the next MMAs overwrite TMEM
+      if ((q - 1) % iters == iters - 1) flush_tile(q - 1);
     }
+  }
+  if (total > 0) {
+    mbar_wait(smem_u32(&done[(total - 1) % S]), ((total - 1) / S) & 1);
+    tc_fence_after();
+    tmem_promote<BN>(t_row, (uint32_t)(((total - 1) & 1) * BN), racc);
+    flush_tile(total - 1);
   }
   tc_fence_before();
   __syncthreads();

@@ -64,7 +64,7 @@ Graph Graph::from_view(const sw_graph_view* v) {
 }
 
 // Dense view: ranks by ascending id, successor lists in edge order
-// (graph.py:187-197 builds adjacency by appending in edge order).
+// (graph.py:89-99 builds adjacency by appending in edge order).
 int Graph::index(std::string* missing_key) {
   sorted_ids = ids;
   std::sort(sorted_ids.begin(), sorted_ids.end());
@@ -96,7 +96,7 @@ int Graph::index(std::string* missing_key) {
   return SW_OK;
 }
 
-// graph.py:264-295 — iterative three-colour DFS, roots ascending, successors
+// graph.py:166-197 — iterative three-colour DFS, roots ascending, successors
 // in edge order; witness = path from the re-entered node back to itself.
 bool Graph::find_cycle(std::vector<int64_t>* witness) const {
   const int64_t N = (int64_t)sorted_ids.size();
@@ -150,7 +150,7 @@ static std::string cycle_str(const std::vector<int64_t>& c) {
   return s;
 }
 
-// graph.py:298-317 — Kahn with a min-heap of ready ids (rank order == id order).
+// graph.py:200-219 — Kahn with a min-heap of ready ids (rank order == id order).
 int Graph::topo(std::vector<int64_t>* order_ranks) const {
   const int64_t N = (int64_t)sorted_ids.size();
   std::vector<int64_t> indeg(N, 0);
@@ -176,7 +176,7 @@ int Graph::topo(std::vector<int64_t>* order_ranks) const {
   return SW_OK;
 }
 
-// graph.py:349-359 — rows[rank u] = OR over succ v of (rows[v] | bit v),
+// graph.py:251-261 — rows[rank u] = OR over succ v of (rows[v] | bit v),
 // filled in reverse topological order.
 int Graph::closure(const std::vector<int64_t>& order_ranks) {
   const int64_t N = (int64_t)sorted_ids.size();
@@ -194,7 +194,7 @@ int Graph::closure(const std::vector<int64_t>& order_ranks) {
   return SW_OK;
 }
 
-// graph.py:209-252 — validation order: per node (dup id, then mem), per edge
+// graph.py:111-154 — validation order: per node (dup id, then mem), per edge
 // (self loop, dangling), duplicate edge, cycle.
 int validate(const Graph& g) {
   std::unordered_set<int64_t> seen;
@@ -254,7 +254,7 @@ int prepare(Graph& g, bool do_validate, bool need_closure) {
   return SW_OK;
 }
 
-// graph.py:373-386 — keep (u,v) iff no other direct successor w of u reaches v.
+// graph.py:275-288 — keep (u,v) iff no other direct successor w of u reaches v.
 std::vector<std::pair<int64_t, int64_t>> meg_edges(const Graph& g) {
   std::vector<std::pair<int64_t, int64_t>> kept;
   for (size_t k = 0; k < g.edges.size(); ++k) {
@@ -548,7 +548,7 @@ int fold_streams(const Graph& g, const Assign& f, int64_t max_streams, std::vect
   return SW_OK;
 }
 
-// schedule.py:417-454 — first fit over a linear trace.
+// schedule.py:118-155 — first fit over a linear trace.
 int reserve_arena(int64_t n, const int64_t* keys, const int32_t* kinds, const int64_t* sizes, int64_t* out_offset,
                   int64_t* total_out, int64_t* bad) {
   std::map<int64_t, std::pair<int64_t, int64_t>> live;   // key -> (offset, size)
@@ -594,7 +594,7 @@ int reserve_arena(int64_t n, const int64_t* keys, const int32_t* kinds, const in
   return SW_OK;
 }
 
-// schedule.py:352-414
+// schedule.py:53-115
 int pre_run(Graph& g, const Assign& f, const std::vector<std::pair<int64_t, int64_t>>& plan, sw_schedule_out* out) {
   int rc = g.index(nullptr);
   if (rc) return fail(SW_KEY_ERROR, g_last_error);
@@ -721,7 +721,7 @@ int pre_run(Graph& g, const Assign& f, const std::vector<std::pair<int64_t, int6
   return SW_OK;
 }
 
-// graph.py:389-399
+// graph.py:291-301
 int critical_path(Graph& g, int64_t* out) {
   int rc = prepare(g, false, false);
   if (rc) return rc;

@@ -1,5 +1,5 @@
 // Integer-time multi-stream device simulator — native restatement of the
-// reference's semantic model (sim.py:256-426).  It is not the executor (the
+// reference's semantic model (sim.py:64-234).  It is not the executor (the
 // CUDA graph is); it is kept so the drop-in API still answers simulate /
 // run_framework_mode / compare_modes, and so measured kernel durations can be
 // fed back into the reference's replay semantics.
@@ -23,7 +23,7 @@ int simulate(const Graph& g, int64_t n_streams, const int64_t* stream_len, const
              const int64_t* op_arg, int64_t n_order, const int64_t* order, const sw_sim_config* cfg,
              int64_t* makespan, int64_t* active, std::unordered_map<int64_t, std::pair<int64_t, int64_t>>* intervals,
              std::vector<std::pair<int64_t, int64_t>>* fire_log) {
-  // sim.py:276-293 — schedule must launch known tasks; capacity admission.
+  // sim.py:84-101 — schedule must launch known tasks; capacity admission.
   std::unordered_map<int64_t, int64_t> duration, demand;
   std::unordered_map<int64_t, std::vector<int64_t>> preds;
   for (int64_t i = 0; i < g.n; ++i) {
@@ -49,7 +49,7 @@ int simulate(const Graph& g, int64_t n_streams, const int64_t* stream_len, const
                                               std::to_string(g.dem[i]) + " of capacity " +
                                               std::to_string(cfg->capacity));
 
-  // replay_order (schedule.py:457-464)
+  // replay_order (schedule.py:158-165)
   std::vector<std::pair<int64_t, int64_t>> flat;  // (stream, global op index)
   std::vector<int64_t> cursor(n_streams, 0);
   for (int64_t i = 0; i < n_order; ++i) {
@@ -70,7 +70,7 @@ int simulate(const Graph& g, int64_t n_streams, const int64_t* stream_len, const
   int64_t host = 0;
   size_t sub = 0;
 
-  auto pump = [&]() -> bool {  // sim.py:310-326
+  auto pump = [&]() -> bool {  // sim.py:118-134
     bool changed = false;
     while (sub < flat.size()) {
       int64_t s = flat[sub].first, k = flat[sub].second;
@@ -94,13 +94,13 @@ int simulate(const Graph& g, int64_t n_streams, const int64_t* stream_len, const
     }
     return changed;
   };
-  auto available = [&](int64_t now) {  // sim.py:328-330
+  auto available = [&](int64_t now) {  // sim.py:136-138
     int64_t used = 0;
     for (auto& r : running)
       if (r.first > now) used += r.second;
     return cfg->capacity - used;
   };
-  auto wave = [&](int64_t now) -> bool {  // sim.py:332-363
+  auto wave = [&](int64_t now) -> bool {  // sim.py:140-171
     bool changed = false;
     for (int64_t s = 0; s < n_streams; ++s) {
       while (qpos[s] < queues[s].size()) {
@@ -138,7 +138,7 @@ int simulate(const Graph& g, int64_t n_streams, const int64_t* stream_len, const
       if (qpos[s] != queues[s].size()) return false;
     return true;
   };
-  auto next_candidate = [&](int64_t now, int64_t* best) -> bool {  // sim.py:370-387
+  auto next_candidate = [&](int64_t now, int64_t* best) -> bool {  // sim.py:178-195
     bool have = false;
     for (int64_t s = 0; s < n_streams; ++s) {
       if (qpos[s] == queues[s].size()) continue;
@@ -164,7 +164,7 @@ int simulate(const Graph& g, int64_t n_streams, const int64_t* stream_len, const
 
   pump();
   int64_t now = 0;
-  while (true) {  // sim.py:389-401
+  while (true) {  // sim.py:197-209
     while (true) {
       if (wave(now)) continue;
       if (pump()) continue;
@@ -181,7 +181,7 @@ int simulate(const Graph& g, int64_t n_streams, const int64_t* stream_len, const
                   running.end());
   }
 
-  // sim.py:403-426 — makespan and union measure of busy intervals
+  // sim.py:211-234 — makespan and union measure of busy intervals
   int64_t ms = 0;
   std::vector<std::pair<int64_t, int64_t>> spans;
   for (auto& kv : *intervals) {

@@ -1,6 +1,6 @@
 // Device runtime of the AoT engine (include/streamweave_b200.h, group 2).
 //
-// The pre_run schedule (schedule.py:352-414: per-stream FIFOs of LAUNCH /
+// The pre_run schedule (schedule.py:53-115: per-stream FIFOs of LAUNCH /
 // RECORD / WAIT in a global capture order) is realised op for op under CUDA
 // stream capture:
 //   origin stream:  [H2D input memcpy] → fork event
@@ -125,7 +125,7 @@ struct sw_engine {
   int device = 0;
   cudaStream_t launch = nullptr;
   std::vector<cudaStream_t> streams;  // logical stream pool (capture)
-  std::vector<cudaEvent_t> events;    // one per sync edge (schedule.py:370)
+  std::vector<cudaEvent_t> events;    // one per sync edge (schedule.py:71)
   std::vector<cudaEvent_t> joins;
   cudaEvent_t fork = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;

@@ -210,9 +210,9 @@ def _pack_weights(prog: Program):
             kpad = (kdim + TC_BK - 1) // TC_BK * TC_BK
             wp = np.zeros((k_out, kpad), dtype=np.float32)
             wp[:, :kdim] = w.numpy().reshape(k_out, kdim)
-            hi = (wp.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+            hi = tf32_round(wp)
             arrays[(t.tid, "w_tc_hi")] = hi.reshape(-1)
-            arrays[(t.tid, "w_tc_lo")] = (wp - hi).astype(np.float32).reshape(-1)
+            arrays[(t.tid, "w_tc_lo")] = tf32_round((wp - hi).astype(np.float32)).reshape(-1)
             if n.attrs["bias"] is not None:
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
         elif t.kind == "dwconv":
@@ -253,6 +253,13 @@ def _pack_weights(prog: Program):
             arrays[(t.tid, "scale")] = n.attrs["scale"].float().numpy().reshape(-1)
             arrays[(t.tid, "shift")] = n.attrs["shift"].float().numpy().reshape(-1)
     return arrays
+
+
+def tf32_round(a: np.ndarray) -> np.ndarray:
+    """fp32 → nearest TF32 (ties away from zero, = PTX cvt.rna.tf32.f32),
+    kept in fp32 storage with the low 13 mantissa bits zero."""
+    bits = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    return ((bits + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
 
 
 def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict,

@@ -1,4 +1,4 @@
-"""AoT schedule capture of the drop-in API (`streamweave/schedule.py:323-514`).
+"""AoT schedule capture of the drop-in API (`streamweave/schedule.py:24-215`).
 
 ``pre_run`` walks the canonical topological order once and records, per
 stream, the FIFO of LAUNCH / RECORD / WAIT operations plus a first-fit arena

@@ -1,4 +1,4 @@
-"""Integer-time simulator of the drop-in API (`streamweave/sim.py:193-486`).
+"""Integer-time simulator of the drop-in API (`streamweave/sim.py:38-294`).
 
 The B200 engine replaces this model with a real CUDA-graph replay; the native
 simulator (`csrc/planner/sim.cpp`) remains the semantic reference for replay
@@ -115,7 +115,7 @@ def sim_result_to_json(r: SimResult) -> str:
 
 
 def chrome_trace(r: SimResult, g: CompGraph, stream_of: dict[int, int]) -> str:
-    """Complete-event ("ph":"X") timeline, tid = stream (sim.py:469-486)."""
+    """Complete-event ("ph":"X") timeline, tid = stream (sim.py:277-294)."""
     rows = []
     for t in g.nodes:
         if t.id in r.intervals:

@@ -9,9 +9,9 @@ It imports the unmodified reference package read-only from
 /root/reference/pkg/tests for the seeded corpora) and records, for every
 case, the reference's own bytes:
 
-  graph      graph_to_json(g)                         (graph.py:404-420)
+  graph      graph_to_json(g)                         (graph.py:306-322)
   assign     assignment_to_json(g, f, plan, meg)      (assign.py:275-282)
-  sched      schedule_to_json(pre_run(g, f, plan))    (schedule.py:473-487)
+  sched      schedule_to_json(pre_run(g, f, plan))    (schedule.py:174-188)
   critical_path, fold[k] (fold_streams, assign.py:243-270),
   sim        sim_result_to_json of replay/framework runs (sim.py:64-80)
   compare    compare_to_json(compare_modes(g, cfg))   (compare.py:50-131)
@@ -122,7 +122,7 @@ def planner_cases():
     cases.append(reference_case(
         sw, sw.CompGraph.build([T(0), T(1)], []), "two_independent", sim_cfgs=sims))
 
-    # error cases, in validation order (graph.py:209-234)
+    # error cases, in validation order (graph.py:111-136)
     cases.append(reference_case(sw, sw.CompGraph.build([T(0), T(1)], [(0, 1), (1, 0)]), "cycle2"))
     cases.append(reference_case(
         sw, sw.CompGraph.build([T(i) for i in range(5)], [(0, 1), (1, 2), (2, 3), (3, 1), (3, 4)]),
