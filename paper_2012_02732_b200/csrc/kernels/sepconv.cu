@@ -773,6 +773,7 @@ static cudaError_t launch_sep_tma_ks(int v, const SepArgs& a, const sw_op_desc& 
 }
 
 int launch_sepconv(const sw_op_desc& op, void* stream) {
+  if (op.variant == SEP_TC_VARIANT) return launch_sepconv_tc(op, stream);  // sepconv_tc.cu
   SepArgs a = sep_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a.M == 0 || a.K == 0) return 0;

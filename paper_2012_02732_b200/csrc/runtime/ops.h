@@ -189,6 +189,12 @@ void init_simt_kernels();
 void init_pw_kernels();
 int launch_sepconv(const sw_op_desc& op, void* stream);
 void init_sep_kernels();
+// K_SEPCONV variant SEP_TC_VARIANT: depthwise + tcgen05 pointwise, persistent
+// warp-specialised (sepconv_tc.cu); PT_W_TC_LO = the packed 3xTF32 pointwise
+// weight images [block][hi | lo][Cpad/4][BN][4] (engine.py sep_tc_layout)
+constexpr int SEP_TC_VARIANT = 100;
+int launch_sepconv_tc(const sw_op_desc& op, void* stream);
+void init_sep_tc_kernels();
 int launch_train(const sw_op_desc& op, void* stream);  // K_BN_* .. K_SGD, K_EW_BWD
 int launch_sep2(const sw_op_desc& op, void* stream);   // K_SEP2 (sep2.cu)
 void init_sep2_kernels();

@@ -90,6 +90,7 @@ SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (
              6: (4, 32), 7: (8, 32), 8: (8, 64), 9: (16, 32), 10: (16, 64),
              # row-blocked depthwise (4 pixels per thread, large batches)
              11: (64, 32), 12: (128, 32), 13: (64, 64), 14: (64, 128), 15: (32, 128)}
+SEP_TC_VARIANT = 100  # csrc/kernels/sepconv_tc.cu: persistent depthwise + tcgen05 pointwise
 SEP_TMA_FIRST = 6
 SEP_ROW_FIRST = 11
 
@@ -227,6 +228,7 @@ def _pack_weights(prog: Program):
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
             dw = n.attrs["dw_weight"].float()[:, 0].permute(1, 2, 0).contiguous()  # [R][S][C]
             arrays[(t.tid, "dw")] = dw.numpy().reshape(-1)
+            arrays[(t.tid, "w_sep_tc")] = sep_tc_pack(pw.numpy(), dw.numpy())
             if n.attrs["dw_bias"] is not None:
                 arrays[(t.tid, "dwb")] = n.attrs["dw_bias"].float().numpy().reshape(-1)
         elif t.kind == "sep2":
@@ -253,6 +255,42 @@ def _pack_weights(prog: Program):
             arrays[(t.tid, "scale")] = n.attrs["scale"].float().numpy().reshape(-1)
             arrays[(t.tid, "shift")] = n.attrs["shift"].float().numpy().reshape(-1)
     return arrays
+
+
+def sep_tc_layout(C: int, K: int) -> tuple[int, int, int]:
+    """(Cpad, BN, nblk) of the tcgen05 sepconv (csrc/kernels/sepconv_tc.cu
+    sep_tc_blocking): K chunks of 16 channels; ceil(K16/128) output-channel
+    blocks of BN (a multiple of 16, <= 128) columns."""
+    cpad = (C + 15) // 16 * 16
+    k16 = (K + 15) // 16 * 16
+    nblk = (k16 + 127) // 128
+    bn = ((K + nblk - 1) // nblk + 15) // 16 * 16
+    return cpad, bn, nblk
+
+
+def sep_tc_pack(pw: np.ndarray, dw: np.ndarray) -> np.ndarray:
+    """Weights of the tcgen05 sepconv, one buffer (csrc/kernels/sepconv_tc.cu):
+    (1) pointwise [K][C] → per output-channel block the 3xTF32 hi and lo
+    images in the canonical K-major SWIZZLE_NONE UMMA layout the kernel
+    bulk-copies into shared memory as is: [blk][hi | lo][Cpad/4][BN][4];
+    (2) depthwise [R][S][C] → chunk-major [Cpad/16][R*S][16] (one bulk copy
+    per 16-channel K chunk).  Zero padded (C to Cpad, K to nblk*BN)."""
+    K, C = pw.shape
+    cpad, bn, nblk = sep_tc_layout(C, K)
+    wp = np.zeros((nblk * bn, cpad), dtype=np.float32)
+    wp[:K, :C] = pw
+    hi = tf32_round(wp)
+    lo = tf32_round((wp - hi).astype(np.float32))
+    img = np.empty((nblk, 2, cpad // 4, bn, 4), dtype=np.float32)
+    for b in range(nblk):
+        for i, part in enumerate((hi, lo)):
+            blk = part[b * bn:(b + 1) * bn]  # [BN][Cpad]
+            img[b, i] = blk.reshape(bn, cpad // 4, 4).transpose(1, 0, 2)
+    R, S, _ = dw.shape
+    dwp = np.zeros((R * S, cpad), dtype=np.float32)
+    dwp[:, :C] = dw.reshape(R * S, C)
+    dwc = dwp.reshape(R * S, cpad // 16, 16).transpose(1, 0, 2)
+    return np.concatenate([img.reshape(-1), dwc.reshape(-1)])
 
 
 def tf32_round(a: np.ndarray) -> np.ndarray:
@@ -326,6 +364,7 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 q[PT_BIAS] = wptr("b")
                 q[PT_WS] = wptr("dw")
                 q[PT_DW_BIAS] = wptr("dwb")
+                q[PT_W_TC_LO] = wptr("w_sep_tc")  # tcgen05 variant's weight images
                 vals[SP_DW_ACT] = n.attrs["dw_act"]
             else:
                 d.kind = K_CONV
@@ -678,6 +717,8 @@ class Engine:
                 cands = sorted({(K_SEP2, 0, sep2_cluster(P, r)) for r in (1, 2, 3, 4, 7) if r <= P})
             elif t.kind == "sepconv":
                 cands = [(K_SEPCONV, v, 1) for v in SEP_TILES]
+                if p[SP_C] % 4 == 0:
+                    cands.append((K_SEPCONV, SEP_TC_VARIANT, 1))  # depthwise + tcgen05 pointwise
                 # TMA kernel with the depthwise split over a cluster of the column blocks
                 cands += [(K_SEPCONV, v, 2) for v, (bm, bn) in SEP_TILES.items()
                           if SEP_TMA_FIRST <= v < SEP_ROW_FIRST and 2 <= math.ceil(K / bn) <= 8]
@@ -738,6 +779,9 @@ class Engine:
             return cd(M / bm) * cd(K / bn) * max(1, split)
         if kind == K_CONV_TC:
             return cd(M / 128) * cd(K / (variant % 1000)) * max(1, split)
+        if kind == K_SEPCONV and variant == SEP_TC_VARIANT:
+            _, bn, nblk = sep_tc_layout(p[SP_C], K)
+            return nblk * min(cd(M / 128), max(1, NUM_SMS // nblk))
         if kind == K_SEPCONV:
             bm, bn = SEP_TILES[variant]
             if SEP_TMA_FIRST <= variant < SEP_ROW_FIRST:

@@ -327,6 +327,54 @@ def test_sepconv_tma_variants(variant, split, c, k, s, h, res):
     eng.close()
 
 
+@pytest.mark.parametrize("c,k,s,h,res,batch", [(44, 5, 1, 14, True, 1), (176, 3, 1, 7, True, 3),
+                                               (88, 7, 2, 14, False, 2), (44, 3, 2, 28, False, 1),
+                                               (32, 7, 1, 9, True, 5), (176, 5, 2, 14, False, 2),
+                                               (16, 5, 1, 30, True, 4), (88, 5, 1, 14, True, 37)])
+def test_sepconv_tcgen05(c, k, s, h, res, batch):
+    """Persistent warp-specialised sepconv (depthwise on CUDA cores, pointwise
+    on tcgen05 3xTF32 with main + correction TMEM accumulators), forced:
+    1..3 output-channel blocks, stride 1 / 2, residual, ragged last pixel
+    tile, several tiles per CTA (batch 37: 7252 px = 57 tiles)."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_SEPCONV, SEP_TC_VARIANT, SLOT_MULTI
+    from paper_2012_02732_b200.networks import randomize_bn
+    torch.manual_seed(6)
+    m = SepBlock(c, k, s, res).eval()
+    randomize_bn(m, seed=3)
+    x = torch.randn(batch, c, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    idx = [i for i, d in enumerate(eng.ops) if d.kind == K_SEPCONV]
+    assert len(idx) == 1
+    eng.ops[idx[0]].variant = SEP_TC_VARIANT
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.ops), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
+def test_sepconv_tcgen05_refuses_oversized_weights():
+    """264 -> 264 channels: the resident 3xTF32 weight block plus the ring
+    exceed 227 KB of shared memory, so the launcher refuses (the autotuner
+    then keeps a CUDA-core variant) instead of launching something wrong."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_SEPCONV, SEP_TC_VARIANT, SLOT_MULTI
+    m = SepBlock(264, 3, 1, False).eval()
+    x = torch.randn(1, 264, 7, 7)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    idx = [i for i, d in enumerate(eng.ops) if d.kind == K_SEPCONV]
+    eng.ops[idx[0]].variant = SEP_TC_VARIANT
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.ops), eng.ops))
+    with pytest.raises(sw.CudaError):
+        eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.close()
+
+
 class PwBlock(nn.Module):
     """1x1 convs reading a zero-copy concat buffer (whole and one channel
     slice), with a residual and pre-ReLU, feeding NHWC consumers."""
