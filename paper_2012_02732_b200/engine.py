@@ -257,40 +257,33 @@ def _pack_weights(prog: Program):
     return arrays
 
 
-def sep_tc_layout(C: int, K: int) -> tuple[int, int, int]:
-    """(Cpad, BN, nblk) of the tcgen05 sepconv (csrc/kernels/sepconv_tc.cu
-    sep_tc_blocking): K chunks of 16 channels; ceil(K16/128) output-channel
-    blocks of BN (a multiple of 16, <= 128) columns."""
-    cpad = (C + 15) // 16 * 16
-    k16 = (K + 15) // 16 * 16
-    nblk = (k16 + 127) // 128
-    bn = ((K + nblk - 1) // nblk + 15) // 16 * 16
-    return cpad, bn, nblk
+def sep_tc_layout(C: int, K: int) -> tuple[int, int]:
+    """(Cpad, BN) of the tcgen05 sepconv (csrc/kernels/sepconv_tc.cu
+    sep_tc_blocking): K chunks of 16 input channels; all K <= 256 outputs in
+    one UMMA N of BN (a multiple of 16) columns."""
+    return (C + 15) // 16 * 16, (K + 15) // 16 * 16
 
 
 def sep_tc_pack(pw: np.ndarray, dw: np.ndarray) -> np.ndarray:
     """Weights of the tcgen05 sepconv, one buffer (csrc/kernels/sepconv_tc.cu):
-    (1) pointwise [K][C] → per output-channel block the 3xTF32 hi and lo
+    (1) pointwise [K][C] → per 16-channel K chunk the 3xTF32 hi and lo
     images in the canonical K-major SWIZZLE_NONE UMMA layout the kernel
-    bulk-copies into shared memory as is: [blk][hi | lo][Cpad/4][BN][4];
-    (2) depthwise [R][S][C] → chunk-major [Cpad/16][R*S][16] (one bulk copy
-    per 16-channel K chunk).  Zero padded (C to Cpad, K to nblk*BN)."""
+    bulk-copies into shared memory as is: [Cpad/16][hi | lo][4 quads][BN][4];
+    (2) depthwise [R][S][C] → chunk-major [Cpad/16][R*S][16].  Zero padded
+    (C to Cpad, K to BN)."""
     K, C = pw.shape
-    cpad, bn, nblk = sep_tc_layout(C, K)
-    wp = np.zeros((nblk * bn, cpad), dtype=np.float32)
+    cpad, bn = sep_tc_layout(C, K)
+    wp = np.zeros((bn, cpad), dtype=np.float32)
     wp[:K, :C] = pw
     hi = tf32_round(wp)
     lo = tf32_round((wp - hi).astype(np.float32))
-    img = np.empty((nblk, 2, cpad // 4, bn, 4), dtype=np.float32)
-    for b in range(nblk):
-        for i, part in enumerate((hi, lo)):
-            blk = part[b * bn:(b + 1) * bn]  # [BN][Cpad]
-            img[b, i] = blk.reshape(bn, cpad // 4, 4).transpose(1, 0, 2)
+    # [BN][Cpad] → [chunk][quad][BN][4]
+    img = np.stack([part.reshape(bn, cpad // 16, 4, 4).transpose(1, 2, 0, 3) for part in (hi, lo)], axis=1)
     R, S, _ = dw.shape
     dwp = np.zeros((R * S, cpad), dtype=np.float32)
     dwp[:, :C] = dw.reshape(R * S, C)
     dwc = dwp.reshape(R * S, cpad // 16, 16).transpose(1, 0, 2)
-    return np.concatenate([img.reshape(-1), dwc.reshape(-1)])
+    return np.concatenate([np.ascontiguousarray(img).reshape(-1), np.ascontiguousarray(dwc).reshape(-1)])
 
 
 def tf32_round(a: np.ndarray) -> np.ndarray:
@@ -780,8 +773,7 @@ class Engine:
         if kind == K_CONV_TC:
             return cd(M / 128) * cd(K / (variant % 1000)) * max(1, split)
         if kind == K_SEPCONV and variant == SEP_TC_VARIANT:
-            _, bn, nblk = sep_tc_layout(p[SP_C], K)
-            return nblk * min(cd(M / 128), max(1, NUM_SMS // nblk))
+            return min(cd(M / 128), NUM_SMS)
         if kind == K_SEPCONV:
             bm, bn = SEP_TILES[variant]
             if SEP_TMA_FIRST <= variant < SEP_ROW_FIRST:

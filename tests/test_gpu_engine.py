@@ -330,6 +330,7 @@ def test_sepconv_tma_variants(variant, split, c, k, s, h, res):
 @pytest.mark.parametrize("c,k,s,h,res,batch", [(44, 5, 1, 14, True, 1), (176, 3, 1, 7, True, 3),
                                                (88, 7, 2, 14, False, 2), (44, 3, 2, 28, False, 1),
                                                (32, 7, 1, 9, True, 5), (176, 5, 2, 14, False, 2),
+                                               (256, 3, 1, 7, True, 2), (200, 7, 2, 15, False, 3),
                                                (16, 5, 1, 30, True, 4), (88, 5, 1, 14, True, 37)])
 def test_sepconv_tcgen05(c, k, s, h, res, batch):
     """Persistent warp-specialised sepconv (depthwise on CUDA cores, pointwise
@@ -358,10 +359,10 @@ def test_sepconv_tcgen05(c, k, s, h, res, batch):
     eng.close()
 
 
-def test_sepconv_tcgen05_refuses_oversized_weights():
-    """264 -> 264 channels: the resident 3xTF32 weight block plus the ring
-    exceed 227 KB of shared memory, so the launcher refuses (the autotuner
-    then keeps a CUDA-core variant) instead of launching something wrong."""
+def test_sepconv_tcgen05_refuses_wide_outputs():
+    """264 -> 264 channels: more output channels than one UMMA N (256), so
+    the launcher refuses (the autotuner then keeps a CUDA-core variant)
+    instead of launching something wrong."""
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import K_SEPCONV, SEP_TC_VARIANT, SLOT_MULTI
     m = SepBlock(264, 3, 1, False).eval()
