@@ -35,6 +35,10 @@
  *   schedule.py:53 pre_run                  -> sw_plan_pre_run
  *   schedule.py:118 reserve_arena            -> sw_plan_reserve_arena
  *   sim.py:64/69 simulate / run_framework_mode -> sw_plan_simulate
+ *   oracle.py:30  oracle_plan_is_safe       -> sw_plan_oracle_plan_is_safe
+ *   oracle.py:149 min_syncs_brute           -> sw_plan_min_syncs_brute
+ *   oracle.py:219 enumerate_assignments     -> sw_plan_enumerate_assignments
+ *   oracle.py:271/296 verify_optimal / verify_given -> sw_plan_verify
  *   (the CUDA Stream Capture / Graph Launch step the
  *    package abstracted into TaskSchedule)   -> sw_engine_capture / sw_engine_replay
  */
@@ -137,6 +141,24 @@ int sw_plan_assign_streams(const sw_graph_view* g, int64_t* out_ids, int64_t* ou
 /* out_ids/out_streams: n_nodes (topo order). */
 int sw_plan_fold_streams(const sw_graph_view* g, const sw_assignment_view* f,
                          int64_t max_streams, int64_t* out_ids, int64_t* out_streams);
+
+/* ---- oracle.py (exhaustive verifiers; compare.py:85-91 with_oracle) ------ */
+/* f == NULL: verify_optimal (checks assign_streams' own plan; plan ignored);
+ * else verify_given.  out5 = {optimal, algo_syncs, oracle_min,
+ * assignments_checked, plan_safe}.  > 7 nodes or > 20 edges: SW_TOO_LARGE. */
+int sw_plan_verify(const sw_graph_view* g, const sw_assignment_view* f, int64_t n_plan,
+                   const int64_t* plan, int64_t* out5);
+/* Path-walking safety predicate (independent of sw_plan_plan_is_safe). */
+int sw_plan_oracle_plan_is_safe(const sw_graph_view* g, const sw_assignment_view* f,
+                                int64_t n_plan, const int64_t* plan, int32_t* out_bool);
+/* Exact smallest safe plan size for f; bound < 0: no bound. */
+int sw_plan_min_syncs_brute(const sw_graph_view* g, const sw_assignment_view* f, int64_t bound,
+                            int64_t* out);
+/* Max-concurrency set partitions in restricted-growth order: out_order =
+ * n_nodes topo-ordered ids; out_streams[a * n_nodes + i] = label of
+ * out_order[i] in candidate a, for a < cap; *out_count = all candidates. */
+int sw_plan_enumerate_assignments(const sw_graph_view* g, int64_t cap, int64_t* out_order,
+                                  int64_t* out_streams, int64_t* out_count);
 
 /* ---- schedule.py -------------------------------------------------------- */
 /* Caller capacities: ops_cap >= n_nodes + 2*n_plan, streams_cap >= n_nodes,

@@ -79,6 +79,11 @@ PROTOTYPES = {
     "sw_plan_assign_streams": (C.c_int, [C.POINTER(GraphView), P64, P64, P64, P64, P64, P64]),
     "sw_plan_fold_streams": (C.c_int, [C.POINTER(GraphView), C.POINTER(AssignView), i64, P64,
                                        P64]),
+    "sw_plan_verify": (C.c_int, [C.POINTER(GraphView), C.POINTER(AssignView), i64, P64, P64]),
+    "sw_plan_oracle_plan_is_safe": (C.c_int, [C.POINTER(GraphView), C.POINTER(AssignView), i64,
+                                              P64, P32]),
+    "sw_plan_min_syncs_brute": (C.c_int, [C.POINTER(GraphView), C.POINTER(AssignView), i64, P64]),
+    "sw_plan_enumerate_assignments": (C.c_int, [C.POINTER(GraphView), i64, P64, P64, P64]),
     "sw_plan_pre_run": (C.c_int, [C.POINTER(GraphView), C.POINTER(AssignView), i64, P64,
                                   C.POINTER(ScheduleOut)]),
     "sw_plan_reserve_arena": (C.c_int, [i64, P64, P32, P64, P64, P64, P64]),

@@ -124,6 +124,28 @@ int sw_plan_assign_streams(const sw_graph_view* v, int64_t* out_ids, int64_t* ou
          write_pairs(meg, out_meg, out_n_meg); return SW_OK;)
 }
 
+int sw_plan_verify(const sw_graph_view* v, const sw_assignment_view* f, int64_t n_plan, const int64_t* plan,
+                   int64_t* out5) {
+  SW_TRY(Graph g = Graph::from_view(v); if (!f) return sw::verify(g, nullptr, Pairs(), out5);
+         Assign a = Assign::from_view(f); return sw::verify(g, &a, pairs_of(n_plan, plan), out5);)
+}
+
+int sw_plan_oracle_plan_is_safe(const sw_graph_view* v, const sw_assignment_view* f, int64_t n_plan,
+                                const int64_t* plan, int32_t* out_bool) {
+  SW_TRY(Graph g = Graph::from_view(v); bool ok = false;
+         int rc = sw::oracle_plan_is_safe(g, Assign::from_view(f), pairs_of(n_plan, plan), &ok);
+         if (rc) return rc; *out_bool = ok ? 1 : 0; return SW_OK;)
+}
+
+int sw_plan_min_syncs_brute(const sw_graph_view* v, const sw_assignment_view* f, int64_t bound, int64_t* out) {
+  SW_TRY(Graph g = Graph::from_view(v); return sw::min_syncs_brute(g, Assign::from_view(f), bound, out);)
+}
+
+int sw_plan_enumerate_assignments(const sw_graph_view* v, int64_t cap, int64_t* out_order, int64_t* out_streams,
+                                  int64_t* out_count) {
+  SW_TRY(Graph g = Graph::from_view(v); return sw::enumerate_assignments(g, cap, out_order, out_streams, out_count);)
+}
+
 int sw_plan_fold_streams(const sw_graph_view* v, const sw_assignment_view* f, int64_t max_streams,
                          int64_t* out_ids, int64_t* out_streams) {
   SW_TRY(Graph g = Graph::from_view(v);

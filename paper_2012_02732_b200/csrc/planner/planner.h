@@ -91,5 +91,12 @@ int plan_is_safe(const Graph& g, const Assign& f, const std::vector<std::pair<in
 int fold_streams(const Graph& g, const Assign& f, int64_t max_streams, std::vector<std::pair<int64_t, int64_t>>* out);
 int pre_run(Graph& g, const Assign& f, const std::vector<std::pair<int64_t, int64_t>>& plan, sw_schedule_out* out);
 std::vector<std::pair<int64_t, int64_t>> canonical(const Graph& g, const std::vector<int64_t>& group_of);
+// verify.cpp (oracle.py exhaustive verifiers)
+int verify(Graph& g, const Assign* f_given, const std::vector<std::pair<int64_t, int64_t>>& plan_given,
+           int64_t out[5]);
+int oracle_plan_is_safe(Graph& g, const Assign& f, const std::vector<std::pair<int64_t, int64_t>>& plan,
+                        bool* out);
+int min_syncs_brute(Graph& g, const Assign& f, int64_t bound, int64_t* out);
+int enumerate_assignments(Graph& g, int64_t cap, int64_t* out_order, int64_t* out_streams, int64_t* out_count);
 
 }  // namespace sw
