@@ -16,6 +16,7 @@ namespace sw {
 #ifdef SW_PROBE
 struct ProbeBuf {
   unsigned long long pt[16];
+  unsigned long long trace[64];  // free-form clock64 stamps of CTA (0,0,0) (probe_trace)
   unsigned long long start[16];
   unsigned long long end[16];
   unsigned int started, finished;
@@ -32,6 +33,15 @@ __device__ __forceinline__ unsigned long long probe_time() {
 // phase points in SM clock cycles (globaltimer ticks in 256 ns steps here)
 __device__ __forceinline__ void probe_pt(int i) {
   if (threadIdx.x == 0 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) g_probe.pt[i] = clock64();
+}
+
+// any thread of CTA (0,0,0) (e.g. a specialised producer / MMA warp)
+__device__ __forceinline__ void probe_pt_any(int i) {
+  if ((blockIdx.x | blockIdx.y | blockIdx.z) == 0) g_probe.pt[i] = clock64();
+}
+
+__device__ __forceinline__ void probe_trace(int i) {
+  if ((blockIdx.x | blockIdx.y | blockIdx.z) == 0 && i >= 0 && i < 64) g_probe.trace[i] = clock64();
 }
 
 __device__ __forceinline__ void probe_begin() {
@@ -70,6 +80,8 @@ static void probe_tu_access(ProbeBuf* out, bool reset) {
 static int g_probe_registered = probe_register(&probe_tu_access);
 #else
 __device__ __forceinline__ void probe_pt(int) {}
+__device__ __forceinline__ void probe_pt_any(int) {}
+__device__ __forceinline__ void probe_trace(int) {}
 __device__ __forceinline__ void probe_begin() {}
 __device__ __forceinline__ void probe_end() {}
 #endif

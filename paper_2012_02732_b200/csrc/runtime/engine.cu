@@ -55,8 +55,9 @@ extern "C" int sw_probe_reset() {
   for (auto fn : sw::probe_registry()) fn(nullptr, true);
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
 }
+// out: 128 words — pt[16], start[16], end[16], started, finished, ..., trace[64] at 64
 extern "C" int sw_probe_read(uint64_t* out) {
-  for (int i = 0; i < 64; ++i) out[i] = 0;
+  for (int i = 0; i < 128; ++i) out[i] = 0;
   for (auto fn : sw::probe_registry()) {
     sw::ProbeBuf b;
     fn(&b, false);
@@ -68,6 +69,7 @@ extern "C" int sw_probe_read(uint64_t* out) {
     }
     out[48] = b.started;
     out[49] = b.finished;
+    for (int i = 0; i < 64; ++i) out[64 + i] = b.trace[i];
   }
   return 0;
 }
@@ -284,6 +286,7 @@ int sw_engine_create(int32_t device, sw_engine** out) {
   }
   CU(cudaStreamCreateWithFlags(&e->launch, cudaStreamNonBlocking));
   sw::init_tc_kernels();
+  sw::init_tcs_kernels();
   sw::init_simt_kernels();
   sw::init_pw_kernels();
   sw::init_sep_kernels();

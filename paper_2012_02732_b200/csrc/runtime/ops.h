@@ -185,6 +185,10 @@ int launch_eltwise(const sw_op_desc& op, void* stream);
 int launch_global_pool(const sw_op_desc& op, void* stream);
 int launch_concat(const sw_op_desc& op, void* stream);
 void init_tc_kernels();
+// K_CONV_TC variants 6000 + NT: weight-streaming swap-AB tcgen05 conv for
+// few output pixels (conv_tcs.cu)
+int launch_conv_tcs(const sw_op_desc& op, void* stream);
+void init_tcs_kernels();
 void init_simt_kernels();
 void init_pw_kernels();
 int launch_sepconv(const sw_op_desc& op, void* stream);

@@ -122,6 +122,11 @@ def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
     return bn, split
 
 
+# csrc/kernels/conv_tcs.cu: pixel tile widths (UMMA N) of variants 6000 + NT
+TCS_TILES = (32, 64, 128)
+TCS_MAX_M = 1024  # pixels per image batch up to which those variants are candidates
+
+
 def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tuple[int, int, int]]:
     """(kernel kind, variant, split) choices the prepare-time autotuner times."""
     out = []
@@ -174,6 +179,17 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
                 if bn <= 128 and split == 1 and M >= 4096:  # persistent tile loop (+ 128-B swizzle)
                     out.append((K_CONV_TC, 3000 + bn, 1))
                     out.append((K_CONV_TC, 4000 + bn, 1))
+    if M <= TCS_MAX_M:
+        # weight-streaming swap-AB tcgen05 kernel (conv_tcs.cu): out channels on
+        # the UMMA M side, NT pixels per tile, split-K cluster <= 16
+        for nt in TCS_TILES:
+            if nt > 2 * max(M, 16) or math.ceil(M / nt) > 8:
+                continue
+            ctas = math.ceil(K / TCS_BM) * math.ceil(M / nt)
+            for split in (1, 2, 4, 8, 16):
+                if split > ktiles or ctas * split > 2 * NUM_SMS:
+                    continue
+                out.append((K_CONV_TC, 6000 + nt, split))
     return out
 
 
@@ -213,7 +229,10 @@ def _pack_weights(prog: Program):
             wp[:, :kdim] = w.numpy().reshape(k_out, kdim)
             hi = tf32_round(wp)
             arrays[(t.tid, "w_tc_hi")] = hi.reshape(-1)
-            arrays[(t.tid, "w_tc_lo")] = tf32_round((wp - hi).astype(np.float32)).reshape(-1)
+            lo = tf32_round((wp - hi).astype(np.float32))
+            arrays[(t.tid, "w_tc_lo")] = lo.reshape(-1)
+            if t.out.st.n * t.out.st.h * t.out.st.w <= TCS_MAX_M:
+                arrays[(t.tid, "w_tcs")] = tcs_pack(hi, lo)
             if n.attrs["bias"] is not None:
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
         elif t.kind == "dwconv":
@@ -255,6 +274,24 @@ def _pack_weights(prog: Program):
             arrays[(t.tid, "scale")] = n.attrs["scale"].float().numpy().reshape(-1)
             arrays[(t.tid, "shift")] = n.attrs["shift"].float().numpy().reshape(-1)
     return arrays
+
+
+TCS_BM = 128  # out channels per tile of the weight-streaming kernel
+
+
+def tcs_pack(hi: np.ndarray, lo: np.ndarray) -> np.ndarray:
+    """Weights of the weight-streaming tcgen05 conv (csrc/kernels/conv_tcs.cu):
+    the 3xTF32 hi / lo [K][Kpad] matrices as shared-memory images of the
+    K-major no-swizzle UMMA layout, [K/128 tile][Kpad/32 block][hi | lo]
+    [8 chunks of 4][128 rows][4]; out channels zero-padded to the tile."""
+    k_out, kpad = hi.shape
+    tiles, nkb = (k_out + TCS_BM - 1) // TCS_BM, kpad // 32
+    parts = []
+    for w in (hi, lo):
+        wp = np.zeros((tiles * TCS_BM, kpad), dtype=np.float32)
+        wp[:k_out] = w
+        parts.append(wp.reshape(tiles, TCS_BM, nkb, 8, 4).transpose(0, 2, 3, 1, 4))
+    return np.ascontiguousarray(np.stack(parts, axis=2)).reshape(-1)
 
 
 def sep_tc_layout(C: int, K: int) -> tuple[int, int]:
@@ -365,6 +402,7 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 q[PT_BIAS] = wptr("b")
                 q[PT_W_TC_HI] = wptr("w_tc_hi")
                 q[PT_W_TC_LO] = wptr("w_tc_lo")
+                q[PT_WS] = wptr("w_tcs")  # weight-streaming variants' packed images (small M only)
                 M = nb * P * Q
                 Kdim = R * S * c
                 vals[SP_KPAD] = (Kdim + TC_BK - 1) // TC_BK * TC_BK
@@ -770,6 +808,8 @@ class Engine:
                 return cd(M / 128)
             bm, bn = PW_TILES[variant] if variant >= 16 else SIMT_TILES[variant]
             return cd(M / bm) * cd(K / bn) * max(1, split)
+        if kind == K_CONV_TC and variant >= 6000:
+            return cd(K / TCS_BM) * cd(M / (variant % 1000)) * max(1, split)
         if kind == K_CONV_TC:
             return cd(M / 128) * cd(K / (variant % 1000)) * max(1, split)
         if kind == K_SEPCONV and variant == SEP_TC_VARIANT:

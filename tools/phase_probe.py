@@ -61,7 +61,7 @@ def main():
         cand = [t for t in eng.program.tasks if t.kind in kinds]
         cand.sort(key=lambda t: -per[t.tid])
         tids = [t.tid for t in cand[: a.limit]]
-    buf = (C.c_uint64 * 64)()
+    buf = (C.c_uint64 * 128)()
     for tid in tids:
         t = eng.program.tasks[tid]
         d = eng.ops[tid]
@@ -83,6 +83,10 @@ def main():
               f"gap {np.mean(gaps) if gaps else 0:+6.2f}us  CTAs {ctas}  "
               f"{t.name}")
         print("        phases(us): " + "  ".join(f"{i}:{p:.2f}" for i, p in sorted(ph.items())))
+        tr = v[64:128]
+        if tr.any():
+            print("        trace(us):  " + "  ".join(f"{i}:{(tr[i] - pts[0]) / (a.sm_mhz * 1e-3) / 1e3:.2f}"
+                                                   for i in range(64) if tr[i]))
 
 
 
