@@ -7,6 +7,10 @@ Workload (BASELINE.json north_star target): NASNet-A mobile, batch-1 fp32
 inference, multi-stream AoT CUDA-graph replay.  One step = one forward pass
 of one batch per GPU.  Multi-GPU = independent replicas (batch-1 latency does
 not shard), one process per GPU under torchrun, weak scaling.
+At N > 1 the line also carries the configs that do shard: NASNet-A mobile
+bs256 batch-sharded 256/N per rank (replicas, max-over-ranks device time)
+and MobileNetV2 / EfficientNet-B0 data-parallel training with the captured
+NCCL gradient allreduce (bs32 per rank).
 
 Printed JSON (rank 0): value = whole-job images/s with the input already in
 HBM (device-resident replay, L2 flushed between steps); e2e = the same metric
@@ -41,6 +45,49 @@ def load_peaks():
             d = json.load(fh)
         return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def load_fp32_peaks():
+    """fp32 compute peaks measured on a B200 of this pool (tools/peaks_fp32.cu
+    → profiles/peaks_fp32.json): FFMA, and the fp32-accurate tensor-core rate
+    (tcgen05 kind::tf32 / 3, the 3xTF32 split every contraction here uses)."""
+    with open(os.path.join(ROOT, "profiles", "peaks_fp32.json")) as fh:
+        d = json.load(fh)
+    return float(d["ffma_fp32_tflops"]), float(d["tcgen05_3xtf32_effective_tflops"])
+
+
+def roofline_sum_fp32(eng, hbm):
+    """Σ per task max(flops / P, bytes / BW) at fp32: contractions (dense /
+    1x1 conv, the sepconv pointwise) at the 3xTF32 tensor-core peak, the
+    depthwise / pool / elementwise flops at the FFMA peak."""
+    from paper_2012_02732_b200.engine import task_cost
+    ffma, tc3 = load_fp32_peaks()
+    total = 0.0
+    for t in eng.program.tasks:
+        f, b = task_cost(t)
+        if t.kind == "sepconv":
+            R, S = t.node.attrs["k"]
+            pix = t.out.st.n * t.out.st.h * t.out.st.w
+            c = t.inputs[0].c
+            dwf = 2.0 * pix * c * R * S
+            tf = dwf / (ffma * 1e12) + (f - dwf) / (tc3 * 1e12)
+        elif t.kind == "conv":
+            tf = f / (tc3 * 1e12)
+        else:
+            tf = f / (ffma * 1e12)
+        total += max(tf, b / (hbm * 1e9)) * 1e6
+    return total
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -174,6 +221,7 @@ def run_reference(args, world, rank):
                    "batch_per_replica": args.batch},
         "latency_us": round(mean * 1e6, 1),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{args.steps} forward passes of {args.config} bs{args.batch} "
                                    f"(torch CPU fp32, same module) + one oracle planner pass "
                                    f"({plan_s * 1e3:.1f} ms)"},
@@ -316,17 +364,39 @@ def run_ours(args, world, rank, local):
     stream_ms_max = reduce_max(world, stream_ms, dev)
     assert torch.equal(outs_stream[-1], eng(xh)), "infer_stream result differs from engine(x)"
 
-    # host launch overhead per iteration (cudaGraphLaunch call) vs GPU time
+    # host launch overhead per iteration: (a) the cudaGraphLaunch call timed
+    # in C (sw_engine_time_replay), (b) the whole Python → C-ABI call
+    # `eng.replay(multi=True)`, back to back so the host never
+    # waits on the device
     gpu_us, host_us = eng.time_replay(multi=True, iters=200)
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    for _ in range(200):
+        eng.replay(multi=True)
+    py_us = (time.perf_counter() - t) / 200 * 1e6
+    torch.cuda.synchronize(dev)
 
-    # per-task device times (eager, serialised) → dominant kernel family roofline
+    # dominant kernel family, two per-launch durations:
+    #  * in_replay: every task bracketed by timing events inside one replay of
+    #    the multi-stream graph after the same 512 MB L2 flush as the timed
+    #    steps (Engine.trace; the event nodes add per-task overhead, so this
+    #    under-states the kernels' own speed);
+    #  * warm_isolated: each task as a graph-captured chain of back-to-back
+    #    launches of itself (warm L2), the autotuner's measurement.
     per_task = eng.profile_tasks(reps=10)
+
+    def flush_on_stream():
+        with torch.cuda.stream(stream):
+            flush.zero_()
+
+    iv, _ = eng.trace(multi=True, before_last=flush_on_stream)
     fam = {}
     for t in eng.program.tasks:
         f_, b_ = task_cost(t)
         k = t.kind
-        d = fam.setdefault(k, {"us": 0.0, "flops": 0.0, "bytes": 0.0, "n": 0})
+        d = fam.setdefault(k, {"us": 0.0, "trace_us": 0.0, "flops": 0.0, "bytes": 0.0, "n": 0})
         d["us"] += per_task[t.tid]
+        d["trace_us"] += iv[t.tid][1] - iv[t.tid][0] if t.tid in iv else 0.0
         d["flops"] += f_
         d["bytes"] += b_
         d["n"] += 1
@@ -341,9 +411,12 @@ def run_ours(args, world, rank, local):
     sim_multi = swpkg.simulate(swpkg.pre_run(gd, fd, pd), gd, swpkg.SimConfig()).makespan / 1000
     sim_single = sum(per_task)
     crit = swpkg.critical_path_time(gd) / 1000
-    dom = max(fam, key=lambda k: fam[k]["us"])
+    dom = max(fam, key=lambda k: fam[k]["trace_us"])
     dd = fam[dom]
-    achieved = dd["bytes"] / (dd["us"] * 1e-6) / 1e9
+    bytes_per_launch = dd["bytes"] / dd["n"]
+    launch_in_replay = dd["trace_us"] / dd["n"]
+    launch_warm = dd["us"] / dd["n"]
+    achieved = bytes_per_launch / (launch_in_replay * 1e-6) / 1e9
     # DRAM bytes per launch of this family from the committed ncu --set full
     # capture (profiles/traffic.json, written by tools/ncu_summary.py --traffic)
     traffic = None
@@ -351,14 +424,22 @@ def run_ours(args, world, rank, local):
     if os.path.exists(tp):
         with open(tp) as fh:
             traffic = json.load(fh).get(dom)
-    roof_sum = eng.roofline_sum_us(hbm, bf16)
+    roof_sum = roofline_sum_fp32(eng, hbm)
+    ffma_peak, tc3_peak = load_fp32_peaks()
 
     extra = None
-    if rank == 0 and world == 1 and not args.skip_extra:
-        extra = other_configs(args, dev, hbm, bf16, flush, stream)
+    if not args.skip_extra:
+        if world == 1:
+            if rank == 0:
+                extra = other_configs(args, dev, hbm, flush, stream)
+        else:
+            extra = sharded_big_batch(args, dev, hbm, flush, world, rank)
     training = None
-    if not args.skip_train and (world == 1 or args.train_dp):
-        training = train_configs(args, dev, world, rank)
+    if not args.skip_train:
+        try:
+            training = train_configs(args, dev, world, rank)
+        except Exception as e:  # noqa: BLE001 — report, do not lose the inference line
+            training = {"error": f"{type(e).__name__}: {e}"}
 
     line = None
     if rank == 0:
@@ -371,6 +452,7 @@ def run_ours(args, world, rank, local):
             ct, plan_s = cpu_path_run(args.config, args.batch, nsteps, 2, thr)
             cpu_val = args.batch / (sum(ct) / len(ct))
             cpu = {"value": round(cpu_val, 3), "unit": UNIT, "cores": thr, "kind": "port",
+                   "cpu_model": cpu_model(),
                    "sample": f"{nsteps} fp32 CPU forwards of {args.config} bs{args.batch} "
                              f"(same module; oracle/numerics.py) + oracle planner "
                              f"{plan_s * 1e3:.1f} ms; {time.perf_counter() - t0:.1f} s total"}
@@ -397,19 +479,30 @@ def run_ours(args, world, rank, local):
                 "aot_over_eager": round(eager_ms / ms, 4),
             },
             "host_overhead": {"launch_us_per_iter": round(host_us, 3),
+                              "python_call_us_per_iter": round(py_us, 3),
                               "gpu_us_per_iter": round(gpu_us, 3),
                               "fraction_of_gpu_time": round(host_us / gpu_us, 5),
+                              "python_call_fraction_of_gpu_time": round(py_us / gpu_us, 5),
                               "fraction_of_roofline_sum": round(host_us / roof_sum, 5)},
             "simulated_from_measured": {"multi_stream_us": round(sim_multi, 2),
                                         "single_stream_us": round(sim_single, 2),
                                         "critical_path_us": round(crit, 2)},
             "roofline_sum_us": round(roof_sum, 3),
+            "roofline_sum_peaks": {"hbm_gbs": hbm, "contraction_tflops": tc3_peak,
+                                   "contraction_peak": "tcgen05 kind::tf32 / 3 (3xTF32), profiles/peaks_fp32.json",
+                                   "other_tflops": ffma_peak, "other_peak": "FFMA, profiles/peaks_fp32.json"},
             "latency_over_roofline_sum": round(ms * 1e3 / roof_sum, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 5), "traffic": traffic,
-                         "algorithmic_bytes_per_launch": round(dd["bytes"] / dd["n"], 1),
-                         "kernel": f"{dom} family ({dd['n']} launches, "
-                                   f"{dd['us'] / n_tasks:.2f} µs avg/task)",
+                         "algorithmic_bytes_per_launch": round(bytes_per_launch, 1),
+                         "launch_us_in_replay": round(launch_in_replay, 3),
+                         "launch_us_warm_isolated": round(launch_warm, 3),
+                         "family_share_of_replay_task_time": round(
+                             dd["trace_us"] / sum(v["trace_us"] for v in fam.values()), 4),
+                         "kernel": f"{dom} family: {dd['n']} launches, {launch_in_replay:.2f} µs per launch "
+                                   f"inside a flushed-L2 replay (event-bracketed), {launch_warm:.2f} µs per "
+                                   f"launch as a warm isolated chain",
+                         "method": "achieved = algorithmic bytes per launch / per-launch time inside the replay",
                          "peak_source": peak_src},
             "e2e": {"value": round(world * args.batch / (e2e_ms_max / 1e3), 3), "unit": UNIT,
                     "ms_per_step": round(e2e_ms_max, 5),
@@ -429,6 +522,7 @@ def run_ours(args, world, rank, local):
             "parity": parity,
             "prepare_s": {k: round(v, 3) for k, v in eng.plan_seconds.items()},
             "kernel_families_us": {k: round(v["us"], 2) for k, v in fam.items()},
+            "kernel_families_in_replay_us": {k: round(v["trace_us"], 2) for k, v in fam.items()},
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
@@ -441,11 +535,64 @@ def run_ours(args, world, rank, local):
     return line
 
 
-def other_configs(args, dev, hbm, bf16, flush, stream):
+def _timed_replays(eng, dev, flush, steps, multi):
+    """Mean device time (µs) of `steps` replays on the engine's launch stream,
+    the 512 MB L2 flush before each (same discipline as the headline)."""
+    import ctypes as C
+    import torch
+    from paper_2012_02732_b200 import _native as N
+    sh = C.c_uint64()
+    N.check(N.lib().sw_engine_stream(eng._h, C.byref(sh)))
+    stream = torch.cuda.ExternalStream(sh.value, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for a, b in ev:
+            flush.zero_()
+            a.record(stream)
+            eng.replay(multi=multi)
+            b.record(stream)
+    torch.cuda.synchronize(dev)
+    return sum(a.elapsed_time(b) for a, b in ev) / steps * 1e3
+
+
+def _parity(model, x, y, n=8):
+    """fp32 gate on the first n images (images are independent, so a slice of
+    a large batch checks the kernels the autotuner picked for that batch)."""
+    import torch
+    from oracle.numerics import cpu_forward
+    k = min(n, x.shape[0])
+    ref = cpu_forward(model, x[:k])
+    yy = y[:k].cpu()
+    return {"images_checked": k, "max_abs_err": float((yy - ref).abs().max()),
+            "ok": bool(torch.allclose(yy, ref, rtol=1e-3, atol=1e-4))}
+
+
+def _family_roofline(eng, hbm, reps=3):
+    from paper_2012_02732_b200.engine import task_cost
+    per = eng.profile_tasks(reps=reps)
+    fams = {}
+    for t in eng.program.tasks:
+        f_, b_ = task_cost(t)
+        d = fams.setdefault(t.kind, [0.0, 0.0, 0.0, 0])
+        d[0] += per[t.tid]
+        d[1] += b_
+        d[2] += f_
+        d[3] += 1
+    dom = max(fams, key=lambda k: fams[k][0])
+    us_, b_, f_, n_ = fams[dom]
+    return {"kernel": f"{dom} family ({n_} launches, {us_ / n_:.1f} µs per launch, warm isolated)",
+            "bound": "hbm", "achieved": round(b_ / (us_ * 1e-6) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(b_ / (us_ * 1e-6) / 1e9 / hbm, 4),
+            "achieved_tflops_fp32": round(f_ / (us_ * 1e-6) / 1e12, 2),
+            "family_share_of_task_time": round(us_ / sum(v[0] for v in fams.values()), 3)}
+
+
+def other_configs(args, dev, hbm, flush, stream):
     """The remaining BASELINE configs, same engine and timing discipline:
     latency (µs) of multi-stream AoT replay, single-stream AoT replay and the
     eager launch loop for the 8-op cell / ResNet-50 / Inception-v3 at batch 1,
-    and NASNet-A mobile images/s at batch 256 (one replica)."""
+    and NASNet-A mobile images/s at batch 256 (one replica); every config
+    carries its fp32 parity against the CPU forward."""
     import torch
     from paper_2012_02732_b200.engine import Engine
     from paper_2012_02732_b200.networks import build_model, example_input
@@ -458,66 +605,22 @@ def other_configs(args, dev, hbm, bf16, flush, stream):
         model, shape = build_model(name)
         x = example_input(shape, batch=batch)
         eng = Engine(model, device=dev.index or 0).prepare(x)
+        y = eng(x)
+        parity = _parity(model, x, y)
         eng.load_input_device(x)
-
-        def timed(multi):
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in range(steps)]
-            with torch.cuda.stream(stream):
-                for a, b in ev:
-                    flush.zero_()
-                    a.record(stream)
-                    eng.replay(multi=multi)
-                    b.record(stream)
-            torch.cuda.synchronize(dev)
-            return sum(a.elapsed_time(b) for a, b in ev) / steps * 1e3
-
-        # the engine has its own launch stream; time on it
-        import ctypes as C
-        from paper_2012_02732_b200 import _native as N
-        sh = C.c_uint64()
-        N.check(N.lib().sw_engine_stream(eng._h, C.byref(sh)))
-        stream = torch.cuda.ExternalStream(sh.value, device=dev)
         for _ in range(3):
             eng.replay(multi=True)
             eng.replay(multi=False)
         torch.cuda.synchronize(dev)
-        multi_us = timed(True)
-        single_us = timed(False)
+        multi_us = _timed_replays(eng, dev, flush, steps, True)
+        single_us = _timed_replays(eng, dev, flush, steps, False)
         t = time.perf_counter()
         for _ in range(3):
             eng.run_eager()
         eng.synchronize()
         eager_us = (time.perf_counter() - t) / 3 * 1e6
-        eng.run_framework(True)
-        eng.synchronize()
-        t = time.perf_counter()
-        for _ in range(5):
-            eng.run_framework(True)
-        eng.synchronize()
-        fw_us = (time.perf_counter() - t) / 5 * 1e6
-        roof = eng.roofline_sum_us(hbm, bf16)
-        fam_roof = None
-        if batch > 1:
-            # large batch: kernels are throughput-bound, so the dominant
-            # family's achieved bandwidth vs the HBM peak is meaningful here
-            from paper_2012_02732_b200.engine import task_cost
-            per = eng.profile_tasks(reps=3)
-            fams = {}
-            for t in eng.program.tasks:
-                f_, b_ = task_cost(t)
-                d = fams.setdefault(t.kind, [0.0, 0.0, 0.0, 0])
-                d[0] += per[t.tid]
-                d[1] += b_
-                d[2] += f_
-                d[3] += 1
-            dom = max(fams, key=lambda k: fams[k][0])
-            us_, b_, f_, n_ = fams[dom]
-            fam_roof = {"kernel": f"{dom} family ({n_} launches)", "bound": "hbm",
-                        "achieved": round(b_ / (us_ * 1e-6) / 1e9, 1), "peak": hbm, "unit": "GB/s",
-                        "frac": round(b_ / (us_ * 1e-6) / 1e9 / hbm, 4),
-                        "achieved_tflops_fp32": round(f_ / (us_ * 1e-6) / 1e12, 2),
-                        "family_share_of_task_time": round(us_ / sum(v[0] for v in fams.values()), 3)}
+        roof = roofline_sum_fp32(eng, hbm)
+        fam_roof = _family_roofline(eng, hbm) if batch > 1 else None
         out[f"{name}_bs{batch}"] = {
             "multi_stream_aot_us": round(multi_us, 2), "single_stream_aot_us": round(single_us, 2),
             "eager_non_aot_us": round(eager_us, 2),
@@ -525,11 +628,49 @@ def other_configs(args, dev, hbm, bf16, flush, stream):
             "multi_over_single": round(single_us / multi_us, 4),
             "tasks": len(eng.program.tasks), "streams": eng.assignment.num_streams,
             "syncs": len(eng.plan), "roofline_sum_us": round(roof, 3),
+            "latency_over_roofline_sum": round(multi_us / roof, 3),
             "arena_mb": round(eng.arena.numel() / 1e6, 2),
-            "roofline_dominant_family": fam_roof,
+            "roofline_dominant_family": fam_roof, "parity": parity,
+            "tcgen05_tasks": sum(1 for d in eng.ops[:len(eng.program.tasks)]
+                                 if d.kind == 6 or (d.kind == 8 and d.variant == 100)),
             "prepare_s": round(time.perf_counter() - t0, 2)}
         eng.close()
     return out
+
+
+def sharded_big_batch(args, dev, hbm, flush, world, rank):
+    """BASELINE config 4 at N > 1 GPUs: NASNet-A mobile bs256 batch-sharded,
+    256/N images per rank, each rank an independent captured replica (no
+    data-path collective).  images/s = 256 / the slowest
+    rank's mean device time per step (barrier before the timed steps)."""
+    import torch
+    from paper_2012_02732_b200.engine import Engine
+    from paper_2012_02732_b200.networks import build_model, example_input
+
+    per_rank = max(1, args.big_batch // world)
+    model, shape = build_model("nasnet_mobile")
+    x = example_input(shape, batch=per_rank, seed=1 + rank)
+    t0 = time.perf_counter()
+    eng = Engine(model, device=dev.index or 0).prepare(x)
+    y = eng(x)
+    parity = _parity(model, x, y)
+    eng.load_input_device(x)
+    for _ in range(3):
+        eng.replay(multi=True)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    steps = max(10, min(args.steps, 50))
+    us = _timed_replays(eng, dev, flush, steps, True)
+    us_max = reduce_max(world, us, dev)
+    ok = reduce_max(world, 0.0 if parity["ok"] else 1.0, dev) == 0.0
+    rec = {f"nasnet_mobile_bs{per_rank * world}_sharded": {
+        "images_per_rank": per_rank, "ranks": world, "ms_per_step_max_over_ranks": round(us_max / 1e3, 4),
+        "images_per_s": round(per_rank * world / (us_max * 1e-6), 2),
+        "parity_all_ranks_ok": ok, "parity_rank0": parity,
+        "roofline_sum_us": round(roofline_sum_fp32(eng, hbm), 3),
+        "prepare_s": round(time.perf_counter() - t0, 2)}}
+    eng.close()
+    return rec
 
 
 def train_configs(args, dev, world=1, rank=0):
@@ -638,7 +779,8 @@ def main():
     ap.add_argument("--big-batch", type=int, default=256, help="NASNet images/s batch (one replica)")
     ap.add_argument("--skip-train", action="store_true", help="skip the training configs")
     ap.add_argument("--train-dp", action="store_true",
-                    help="under torchrun: data-parallel training with the captured NCCL allreduce")
+                    help="(default now) under torchrun the training configs run data-parallel with the "
+                         "captured NCCL allreduce")
     ap.add_argument("--tuning-cache", default=None,
                     help="reuse kernel picks (e.g. for an ncu launch list of this command)")
     args = ap.parse_args()

@@ -330,31 +330,43 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                              ((uint32_t)(ST_BM >> 4) << 24);
       const uint32_t LBO_B = (uint32_t)BN * 16;
       const uint32_t bhalf = a.b_bytes / 2;
-      int seq = 0;
+      // Descriptors are computed once per chunk (no division on the way to
+      // an MMA: a per-MMA address chain with `seq % G` held the issue rate
+      // to ~135 clocks per MMA, tools/mma_rate.cu r02j); the group index and
+      // its phase advance incrementally.
+      int g = 0, use = 0;
       for (int ti = 0; ti < ntiles; ++ti) {
         const int b = ti % a.tbufs, tuse = ti / a.tbufs;
         if (tuse >= 1) mbar_wait_parity(t_empty(b), (tuse & 1) ^ 1);
         st_fence_after();
         const uint32_t d_main = tmem + (uint32_t)(b * 2 * BN), d_corr = d_main + (uint32_t)BN;
-        for (int kc = 0; kc < nchunks; ++kc, ++seq) {
-          const int g = seq % G, use = seq / G;
-          mbar_wait_parity(b_full(g), use & 1);
-          mbar_wait_parity(a_full(g), use & 1);
-          st_fence_after();
+        for (int kc = 0; kc < nchunks; ++kc) {
           const uint32_t stg = sbase + a.off_g + (uint32_t)g * a.gstage;
           const uint32_t ah = stg + a.off_a, al = ah + ST_AHALF;
           const uint32_t bh = stg + a.off_b, bl = bh + bhalf;
+          uint64_t dah[ST_CK / 8], dal[ST_CK / 8], dbh[ST_CK / 8], dbl[ST_CK / 8];
 #pragma unroll
           for (int ks = 0; ks < ST_CK / 8; ++ks) {
-            const uint64_t dah = st_desc(ah + ks * 2 * ST_LBO_A, ST_LBO_A);
-            const uint64_t dal = st_desc(al + ks * 2 * ST_LBO_A, ST_LBO_A);
-            const uint64_t dbh = st_desc(bh + ks * 2 * LBO_B, LBO_B), dbl = st_desc(bl + ks * 2 * LBO_B, LBO_B);
+            dah[ks] = st_desc(ah + ks * 2 * ST_LBO_A, ST_LBO_A);
+            dal[ks] = st_desc(al + ks * 2 * ST_LBO_A, ST_LBO_A);
+            dbh[ks] = st_desc(bh + ks * 2 * LBO_B, LBO_B);
+            dbl[ks] = st_desc(bl + ks * 2 * LBO_B, LBO_B);
+          }
+          mbar_wait_parity(b_full(g), use & 1);
+          mbar_wait_parity(a_full(g), use & 1);
+          st_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < ST_CK / 8; ++ks) {
             const uint32_t first = (kc | ks) ? 1u : 0u;
-            st_mma(d_main, dah, dbh, idesc, first);
-            st_mma(d_corr, dah, dbl, idesc, first);
-            st_mma(d_corr, dal, dbh, idesc, 1u);
+            st_mma(d_main, dah[ks], dbh[ks], idesc, first);
+            st_mma(d_corr, dah[ks], dbl[ks], idesc, first);
+            st_mma(d_corr, dal[ks], dbh[ks], idesc, 1u);
           }
           st_commit(a_empty(g));
+          if (++g == G) {
+            g = 0;
+            ++use;
+          }
         }
         st_commit(t_full(b));
       }

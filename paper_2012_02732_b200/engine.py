@@ -1074,14 +1074,15 @@ class Engine:
         e = int(ne[0])
         return kinds[:n], task[:n], edges[:2 * e].reshape(-1, 2)
 
-    def trace(self, multi: bool = True, warm: int = 3):
+    def trace(self, multi: bool = True, warm: int = 3, before_last=None):
         """Measured timeline of one device-resident replay:
         the schedule is re-captured with timing events around every task
         (SW_ENGINE_TRACE; the events sit between kernels, so same-stream PDL
         overlap is lost in this diagnostic capture), replayed, read back, and
         the normal capture restored.  Returns (intervals {task: (start_us,
         end_us)}, Chrome-trace JSON in the reference's format, sim.py:277-294,
-        tid = logical stream)."""
+        tid = logical stream).  ``before_last()`` runs before the measured
+        replay (e.g. an L2 flush enqueued on the engine's launch stream)."""
         from .sim import SimResult, chrome_trace
         lib = N.lib()
         slot = SLOT_MULTI if multi else SLOT_SINGLE
@@ -1089,8 +1090,11 @@ class Engine:
         try:
             N.check(lib.sw_engine_set_flags(self._h, self._flags() | 16))
             self._capture(slot, ts, False)
-            for _ in range(warm + 1):
+            for _ in range(warm):
                 N.check(lib.sw_engine_replay(self._h, slot))
+            if before_last is not None:
+                before_last()
+            N.check(lib.sw_engine_replay(self._h, slot))
             n = len(self.program.tasks)
             a = np.zeros(n, dtype=np.float64)
             b = np.zeros(n, dtype=np.float64)

@@ -170,6 +170,65 @@ __global__ void __launch_bounds__(128, 1) rate_kernel_warp(int n, int reps, int 
   if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// descriptors precomputed for NS stages (registers), stage walked by an
+// unrolled loop: the pattern of a pipelined kernel's issuer after hoisting
+template <int NS>
+__global__ void __launch_bounds__(128, 1) rate_kernel_table(int n, int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (64 * 1024) / 16; i += 128) reinterpret_cast<int4*>(smem)[i] = make_int4(0, 0, 0, 0);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su(&slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  if (tid < 32) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | (8u << 24);
+    const uint32_t a = su(smem), b = su(smem + 32 * 1024);
+    const uint64_t a0 = desc_ns(a, 2048, 128), b0 = desc_ns(b, n * 16, 128);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; r += 4 * NS) {
+#pragma unroll
+      for (int st = 0; st < NS; ++st) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t da = a0 + (uint64_t)(((st & 3) * 512 + ks * 4096) >> 4);
+          const uint64_t db = b0 + (uint64_t)(((st & 3) * 512 + ks * 2 * n * 16) >> 4);
+          if (elect_one()) mma<0>(tmem + (st & 1) * n, da, db, idesc, (r | st | ks) ? 1u : 0u);
+          __syncwarp();
+        }
+      }
+    }
+    if (elect_one())
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su(&bar))
+                   : "memory");
+    __syncwarp();
+    uint32_t done = 0;
+    do {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(su(&bar))
+          : "memory");
+    } while (!done);
+    long long t1 = clock64();
+    if (tid == 0) out[blockIdx.x] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 int main() {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
@@ -210,5 +269,22 @@ int main() {
     printf("tf32 warp-uniform elect issue N=%3d: %7.1f clk/MMA  %7.0f MAC/clk/SM  (%s)\n", n, avg / reps,
            128.0 * n * 8 * reps / avg, cudaGetErrorString(e));
   }
+  cudaFuncSetAttribute(rate_kernel_table<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  cudaFuncSetAttribute(rate_kernel_table<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  for (int ns : {4, 16})
+    for (int n : {64, 128, 256}) {
+      for (int w = 0; w < 2; ++w) {
+        if (ns == 4) rate_kernel_table<4><<<148, 128, 96 * 1024>>>(n, reps, d);
+        else rate_kernel_table<16><<<148, 128, 96 * 1024>>>(n, reps, d);
+      }
+      cudaError_t e = cudaDeviceSynchronize();
+      long long h[148];
+      cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (int i = 0; i < 148; ++i) avg += h[i];
+      avg /= 148;
+      printf("tf32 hoisted-table stages=%2d N=%3d: %7.1f clk/MMA  %7.0f MAC/clk/SM  (%s)\n", ns, n, avg / reps,
+             128.0 * n * 8 * reps / avg, cudaGetErrorString(e));
+    }
   return 0;
 }
