@@ -533,12 +533,14 @@ class Engine:
     def __init__(self, model: torch.nn.Module, multi_stream: bool = True, fuse: bool = True,
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
                  tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb",
-                 fuse_sep_pairs: bool = False, l2_prefetch: bool = False):
+                 fuse_sep_pairs: bool = False, l2_prefetch: bool = False,
+                 max_streams: int | None = None):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
         self.model = model.eval()
         self.multi_stream = multi_stream
+        self.max_streams = max_streams
         self.fuse = fuse
         self.device = device
         self.conv_impl = conv_impl
@@ -566,6 +568,11 @@ class Engine:
         t1 = time.perf_counter()
         g = prog.graph
         f, plan, meg = assign_streams_full(g)
+        if self.max_streams is not None and f.num_streams > self.max_streams:
+            # the reference's physical-stream cap (assign.py:243-270): keep the
+            # busiest logical streams, fold the rest round-robin, same plan
+            from .assign import fold_streams
+            f, plan = fold_streams(g, f, plan, self.max_streams)
         ts = pre_run(g, f, plan)
         single_f = StreamAssignment({t.id: 0 for t in g.nodes})
         ts_single = pre_run(g, single_f, SyncPlan(()))

@@ -409,7 +409,10 @@ def test_sepconv_tma_variants(variant, split, c, k, s, h, res):
                                                (88, 7, 2, 14, False, 2), (44, 3, 2, 28, False, 1),
                                                (32, 7, 1, 9, True, 5), (176, 5, 2, 14, False, 2),
                                                (256, 3, 1, 7, True, 2), (200, 7, 2, 15, False, 3),
-                                               (16, 5, 1, 30, True, 4), (88, 5, 1, 14, True, 37)])
+                                               (16, 5, 1, 30, True, 4), (88, 5, 1, 14, True, 37),
+                                               (44, 5, 1, 28, False, 3), (24, 7, 1, 56, True, 2),
+                                               (44, 3, 1, 28, True, 2), (88, 7, 1, 14, False, 2),
+                                               (12, 3, 1, 23, True, 3)])
 def test_sepconv_tcgen05(c, k, s, h, res, batch):
     """Persistent warp-specialised sepconv (depthwise on CUDA cores, pointwise
     on tcgen05 3xTF32 with main + correction TMEM accumulators), forced:
