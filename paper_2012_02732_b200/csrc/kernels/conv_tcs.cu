@@ -33,10 +33,15 @@
 //    and applies bias (folded BN), residual and activation with coalesced
 //    NHWC channel-row stores.
 //
-// Variants 6000 + NT (NT = 32, 64, 128 pixels per tile).
+// Variants 6000 + NT (NT = 32, 64, 128 pixels per tile).  Variants 7000 + NT
+// are the bf16 path (Engine(precision="bf16"), a separately stated
+// tolerance): bf16 weight image, activations rounded to bf16 in shared
+// memory, one kind::f16 MMA per 16-wide K step into one fp32 accumulator.
 #include <cooperative_groups.h>
 
 #include <algorithm>
+
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -68,23 +73,26 @@ constexpr int TCS_UM = 128;  // UMMA M
 constexpr int TCS_BK = 32;   // fp32 per K block = one 128-B swizzle row
 constexpr int TCS_THREADS = 192;  // warps 0-3 activations + epilogue, 4 weight TMA, 5 MMA issue
 
-template <int NT>
+template <int NT, bool BF16 = false>
 struct TcsSmem {
-  static constexpr int A_BYTES = TCS_BM * TCS_BK * 4;  // 16 KB per hi / lo weight image
-  static constexpr int W_STAGE = 2 * A_BYTES;
+  // weights per K block: 3xTF32 hi | lo (2 x 16 KB) or bf16 (8 KB)
+  static constexpr int A_BYTES = TCS_BM * TCS_BK * (BF16 ? 2 : 4);
+  static constexpr int W_STAGE = BF16 ? A_BYTES : 2 * A_BYTES;
   static constexpr int B_BYTES = NT * TCS_BK * 4;      // one raw fp32 activation K block
-  static constexpr int B_STAGE = 2 * B_BYTES;          // split activations hi | lo
+  static constexpr int B_OP = NT * TCS_BK * (BF16 ? 2 : 4);  // one activation operand (hi or lo / bf16)
+  static constexpr int B_STAGE = BF16 ? B_OP : 2 * B_OP;
   // raw activation ring RB deep (refilled as soon as the split consumed a
   // slot — never gated by the tensor pipe), split ring SB, weight ring W
   static constexpr int RB = NT == 32 ? 16 : 4;
   static constexpr int SB = NT == 128 ? 2 : 4;
-  static constexpr int W = NT == 128 ? 2 : 4;
+  static constexpr int W = BF16 ? 8 : (NT == 128 ? 2 : 4);
   static constexpr int RAW_OFF = W * W_STAGE;
   static constexpr int B_OFF = RAW_OFF + RB * B_BYTES;
   static constexpr int RING = B_OFF + SB * B_STAGE;
-  static constexpr int ROW = TCS_BM * 4;               // epilogue tile row: 64 channels
+  static constexpr int ROW = TCS_BM * 4;               // epilogue tile row: 128 channels
   static constexpr int TOTAL = RING + 256;             // + mbarriers + TMEM slot
-  static constexpr int COLS = 2 * NT < 32 ? 32 : 2 * NT;  // main + correction accumulators
+  // main (+ correction) accumulators
+  static constexpr int COLS = (BF16 ? NT : 2 * NT) < 32 ? 32 : (BF16 ? NT : 2 * NT);
   static_assert(NT == 32 || NT == 64 || NT == 128, "pixel tile");
   static_assert(TOTAL <= 227 * 1024, "smem");
   static_assert(NT * ROW * 2 <= RING, "epilogue tiles (part + receive) fit the dead ring");
@@ -111,6 +119,20 @@ __device__ __forceinline__ void umma_tf32(uint32_t d, uint64_t a, uint64_t b, ui
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x (low half) = lo
+  return *reinterpret_cast<const uint32_t*>(&v);
 }
 
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
@@ -156,10 +178,10 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 }  // namespace
 
-template <int NT>
+template <int NT, bool BF16>
 __global__ void __launch_bounds__(TCS_THREADS, 1)
     conv_tcs_kernel(TcsArgs a) {
-  using L = TcsSmem<NT>;
+  using L = TcsSmem<NT, BF16>;
   constexpr int W = L::W, SB = L::SB;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + L::RING);
@@ -211,7 +233,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
     // constants, so it runs ahead of the PDL wait
     if (lane == 0) {
       // this CTA's K slice of its out-channel tile is one contiguous run of
-      // 32-KB [hi | lo] images: one bulk copy per K block
+      // [hi | lo] (or bf16) images: one bulk copy per K block
       const float* src = a.wimg + ((size_t)blockIdx.x * ktiles + kt0) * (L::W_STAGE / 4);
 #pragma unroll 1
       for (int t = 0; t < iters; ++t) {
@@ -228,9 +250,13 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
     // descriptor is a loop-invariant base + an immediate: recomputing them per
     // MMA in registers (R2UR on every issue) held the issue rate to ~135
     // clocks per MMA against 48 for an N = 64 MMA (tools/mma_rate.cu, r02j).
-    constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) |
+    // D f32; A / B tf32 (2) or bf16 (1), K-major; N = NT pixels, M = 128 channels
+    constexpr uint32_t fmt = BF16 ? 1u : 2u;
+    constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(NT >> 3) << 17) |
                                ((uint32_t)(TCS_UM >> 4) << 24);
+    // 16-B core-matrix columns: 4 tf32 or 8 bf16; one MMA K step = 32 B = 2 columns
     constexpr uint32_t LBO_B = NT * 16, LBO_A = TCS_BM * 16;
+    constexpr int KSTEPS = TCS_BK * (BF16 ? 2 : 4) / 32;
     static_assert(W % SB == 0, "split ring period divides the weight ring");
     const uint64_t a0 = desc_noswz(sbase, LBO_A, 128);
     const uint64_t b0 = desc_noswz(sbase + L::B_OFF, LBO_B, 128);
@@ -248,15 +274,19 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
         tc_fence_after_sync();
         if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < TCS_BK / 8; ++ks) {
+          for (int ks = 0; ks < KSTEPS; ++ks) {
             const uint64_t ah = a0 + (uint64_t)((s * L::W_STAGE + ks * 2 * LBO_A) >> 4);
-            const uint64_t al = ah + (uint64_t)(L::A_BYTES >> 4);
             const uint64_t bh = b0 + (uint64_t)((sb * L::B_STAGE + ks * 2 * LBO_B) >> 4);
-            const uint64_t bl = bh + (uint64_t)(L::B_BYTES >> 4);
             const uint32_t acc = (t | ks) ? 1u : 0u;
-            umma_tf32(tmem, ah, bh, idesc, acc);
-            umma_tf32(tmem + NT, ah, bl, idesc, acc);
-            umma_tf32(tmem + NT, al, bh, idesc, 1u);
+            if constexpr (BF16) {
+              umma_bf16(tmem, ah, bh, idesc, acc);
+            } else {
+              const uint64_t al = ah + (uint64_t)(L::A_BYTES >> 4);
+              const uint64_t bl = bh + (uint64_t)(L::B_OP >> 4);
+              umma_tf32(tmem, ah, bh, idesc, acc);
+              umma_tf32(tmem + NT, ah, bl, idesc, acc);
+              umma_tf32(tmem + NT, al, bh, idesc, 1u);
+            }
           }
           umma_commit(su32(&wfree[s]));
           umma_commit(su32(&bfree[sb]));
@@ -315,18 +345,37 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
       if (tid == 0 && t < 16) probe_trace(48 + t);  // raw K block t landed
       // the split slot is free once the MMAs of K block t - SB completed
       if (t >= SB) mbar_wait_parity(su32(&bfree[sb]), (uint32_t)(((t / SB) - 1) & 1));
-      const float4* raw = reinterpret_cast<const float4*>(smem + L::RAW_OFF + rb * L::B_BYTES);
-      float4* hi = reinterpret_cast<float4*>(smem + L::B_OFF + sb * L::B_STAGE);
-      float4* lo = reinterpret_cast<float4*>(smem + L::B_OFF + sb * L::B_STAGE + L::B_BYTES);
+      const uint8_t* rawb = smem + L::RAW_OFF + rb * L::B_BYTES;
+      if constexpr (BF16) {
+        // raw 4-float columns 2j, 2j+1 of a row → one 8-bf16 column j
+        uint4* ob = reinterpret_cast<uint4*>(smem + L::B_OFF + sb * L::B_STAGE);
 #pragma unroll
-      for (int i = tid; i < L::B_BYTES / 16; i += 128) {
-        float4 x = raw[i];
-        if (a.pre_relu) {
-          x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+        for (int i = tid; i < NT * 4; i += 128) {
+          const int j = i / NT, row = i - j * NT;
+          const int roff = (row >> 3) * 128 + (row & 7) * 16;
+          float4 x0 = *reinterpret_cast<const float4*>(rawb + (2 * j) * (NT * 16) + roff);
+          float4 x1 = *reinterpret_cast<const float4*>(rawb + (2 * j + 1) * (NT * 16) + roff);
+          if (a.pre_relu) {
+            x0 = make_float4(fmaxf(x0.x, 0.f), fmaxf(x0.y, 0.f), fmaxf(x0.z, 0.f), fmaxf(x0.w, 0.f));
+            x1 = make_float4(fmaxf(x1.x, 0.f), fmaxf(x1.y, 0.f), fmaxf(x1.z, 0.f), fmaxf(x1.w, 0.f));
+          }
+          ob[(j * (NT * 16) + roff) / 16] = make_uint4(pack_bf16x2(x0.x, x0.y), pack_bf16x2(x0.z, x0.w),
+                                                     pack_bf16x2(x1.x, x1.y), pack_bf16x2(x1.z, x1.w));
         }
-        const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-        hi[i] = h;
-        lo[i] = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z), tf32_rna(x.w - h.w));
+      } else {
+        const float4* raw = reinterpret_cast<const float4*>(rawb);
+        float4* hi = reinterpret_cast<float4*>(smem + L::B_OFF + sb * L::B_STAGE);
+        float4* lo = reinterpret_cast<float4*>(smem + L::B_OFF + sb * L::B_STAGE + L::B_OP);
+#pragma unroll
+        for (int i = tid; i < L::B_BYTES / 16; i += 128) {
+          float4 x = raw[i];
+          if (a.pre_relu) {
+            x.x = fmaxf(x.x, 0.f); x.y = fmaxf(x.y, 0.f); x.z = fmaxf(x.z, 0.f); x.w = fmaxf(x.w, 0.f);
+          }
+          const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+          hi[i] = h;
+          lo[i] = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z), tf32_rna(x.w - h.w));
+        }
       }
       fence_proxy_async_cta();
       named_bar(1, 128);  // every thread read raw slot rb and wrote split slot sb
@@ -353,7 +402,12 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
       float v[16], u[16];
       if (iters > 0) {
         tmem_ld_x16(t_row + (uint32_t)c0, v);
-        tmem_ld_x16(t_row + (uint32_t)(NT + c0), u);
+        if constexpr (BF16) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) u[j] = 0.f;
+        } else {
+          tmem_ld_x16(t_row + (uint32_t)(NT + c0), u);
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = u[j] = 0.f;
@@ -428,7 +482,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
   probe_end();
 }
 
-template <int NT>
+template <int NT, bool BF16>
 static int launch_tcs(const sw_op_desc& op, cudaStream_t st) {
   const int64_t* p = op.params;
   TcsArgs a;
@@ -456,31 +510,40 @@ static int launch_tcs(const sw_op_desc& op, cudaStream_t st) {
   // 16-B im2col chunks: 4 consecutive channels of one tap, 16-B aligned rows
   const bool vec = a.C % 4 == 0 && p[SP_IN_SC] == 1 && a.in_sn % 4 == 0 && a.in_sh % 4 == 0 &&
                    a.in_sw % 4 == 0 && (op.ptrs[PT_IN] & 15) == 0;
+  // the packed image at PT_WS must be the one this variant reads
+  if (p[SP_WS_KIND] != (BF16 ? 1 : 0)) return (int)cudaErrorInvalidValue;
   if (!vec || !a.wimg || (op.ptrs[PT_WS] & 15) || a.Kpad < a.Kdim || a.Kpad % TCS_BK ||
       a.split > 16 || NT % a.split || a.split > a.Kpad / TCS_BK)
     return (int)cudaErrorInvalidValue;
   dim3 grid((unsigned)cdiv(a.K, TCS_BM), (unsigned)cdiv(a.M, NT), (unsigned)a.split);
-  return (int)launch_k(conv_tcs_kernel<NT>, grid, dim3(TCS_THREADS), (size_t)TcsSmem<NT>::TOTAL, st,
+  return (int)launch_k(conv_tcs_kernel<NT, BF16>, grid, dim3(TCS_THREADS), (size_t)TcsSmem<NT, BF16>::TOTAL, st,
                        (unsigned)a.split, a);
 }
 
 int launch_conv_tcs(const sw_op_desc& op, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (op.variant) {
-    case 6032: return launch_tcs<32>(op, st);
-    case 6064: return launch_tcs<64>(op, st);
-    case 6128: return launch_tcs<128>(op, st);
+    case 6032: return launch_tcs<32, false>(op, st);
+    case 6064: return launch_tcs<64, false>(op, st);
+    case 6128: return launch_tcs<128, false>(op, st);
+    case 7032: return launch_tcs<32, true>(op, st);
+    case 7064: return launch_tcs<64, true>(op, st);
+    case 7128: return launch_tcs<128, true>(op, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }
 
 void init_tcs_kernels() {
-#define SW_TCS_ATTR(NT_)                                                                                     \
-  cudaFuncSetAttribute(conv_tcs_kernel<NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcsSmem<NT_>::TOTAL); \
-  cudaFuncSetAttribute(conv_tcs_kernel<NT_>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  SW_TCS_ATTR(32)
-  SW_TCS_ATTR(64)
-  SW_TCS_ATTR(128)
+#define SW_TCS_ATTR(NT_, B_)                                                                    \
+  cudaFuncSetAttribute(conv_tcs_kernel<NT_, B_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       TcsSmem<NT_, B_>::TOTAL);                                              \
+  cudaFuncSetAttribute(conv_tcs_kernel<NT_, B_>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  SW_TCS_ATTR(32, false)
+  SW_TCS_ATTR(64, false)
+  SW_TCS_ATTR(128, false)
+  SW_TCS_ATTR(32, true)
+  SW_TCS_ATTR(64, true)
+  SW_TCS_ATTR(128, true)
 #undef SW_TCS_ATTR
 }
 

@@ -150,6 +150,10 @@ enum SpatialParam : int {
   SP_DW_ACT,                           // K_SEPCONV: activation between depthwise and pointwise
   SP_POOL_MUL                          // K_POOL: integer output multiplier (0 → 1): twin pools merged
 };
+// K_CONV / K_CONV_TC: which packed weight image PT_WS holds for the
+// weight-streaming variants (conv_tcs.cu): 0 = 3xTF32 hi|lo (variants 6000 +
+// NT), 1 = bf16 (variants 7000 + NT, the engine's precision="bf16" path)
+constexpr int SP_WS_KIND = 49;
 // K_SEPCONV: PT_W / PT_BIAS = pointwise [K][C] / [K]; PT_WS = depthwise
 // weights [R][S][C]; PT_DW_BIAS = depthwise bias [C]; spatial params describe
 // the depthwise geometry, SP_K the pointwise output channels.

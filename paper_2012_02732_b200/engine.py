@@ -47,6 +47,7 @@ EW_ADD, EW_MUL, EW_AFFINE, EW_COPY = 0, 1, 2, 3
  SP_OUT_SW, SP_RES_SN, SP_RES_SH, SP_RES_SW, SP_HAS_RES, SP_POOL_MODE, SP_COUNT_PAD,
  SP_PAD_BOTTOM, SP_PAD_RIGHT, SP_SPLIT_K, SP_OUT_SC, SP_RES_SC, SP_KPAD, SP_DW_ACT, SP_POOL_MUL) = range(36)
 PT_IN, PT_OUT, PT_W, PT_BIAS, PT_RES, PT_WS, PT_W_TC_HI, PT_W_TC_LO = range(8)
+SP_WS_KIND = 49  # runtime/ops.h: image at PT_WS for the weight-streaming convs (0 3xTF32, 1 bf16)
 PT_DW_BIAS = 6  # K_SEPCONV
 K_SEPCONV = 8
 K_SEP2 = 24  # fused NASNet separable block (csrc/kernels/sep2.cu)
@@ -125,9 +126,11 @@ def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
 # csrc/kernels/conv_tcs.cu: pixel tile widths (UMMA N) of variants 6000 + NT
 TCS_TILES = (32, 64, 128)
 TCS_MAX_M = 1024  # pixels per image batch up to which those variants are candidates
+BF16_TUNE_RTOL = 3e-2  # autotuner check of a bf16 candidate: |d| <= 3e-2 * max(1, max|ref|)
 
 
-def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tuple[int, int, int]]:
+def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
+                    bf16: bool = False) -> list[tuple[int, int, int]]:
     """(kernel kind, variant, split) choices the prepare-time autotuner times."""
     out = []
     if M <= 8 and R == 1 and S == 1 and tuple(pad) == (0, 0):
@@ -189,7 +192,8 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad) -> list[tupl
             for split in (1, 2, 4, 8, 16):
                 if split > ktiles or ctas * split > 2 * NUM_SMS:
                     continue
-                out.append((K_CONV_TC, 6000 + nt, split))
+                # precision="bf16": the bf16 image replaces the 3xTF32 one
+                out.append((K_CONV_TC, (7000 if bf16 else 6000) + nt, split))
     return out
 
 
@@ -213,8 +217,9 @@ def _strides(v: View):
     return v.strides()
 
 
-def _pack_weights(prog: Program):
-    """Kernel-layout parameter arrays per task (host numpy, fp32)."""
+def _pack_weights(prog: Program, precision: str = "fp32"):
+    """Kernel-layout parameter arrays per task (host numpy, fp32; the bf16
+    weight-streaming image is packed as pairs inside fp32 words)."""
     arrays = {}
     for t in prog.tasks:
         n = t.node
@@ -232,7 +237,7 @@ def _pack_weights(prog: Program):
             lo = tf32_round((wp - hi).astype(np.float32))
             arrays[(t.tid, "w_tc_lo")] = lo.reshape(-1)
             if t.out.st.n * t.out.st.h * t.out.st.w <= TCS_MAX_M:
-                arrays[(t.tid, "w_tcs")] = tcs_pack(hi, lo)
+                arrays[(t.tid, "w_tcs")] = tcs_pack_bf16(wp) if precision == "bf16" else tcs_pack(hi, lo)
             if n.attrs["bias"] is not None:
                 arrays[(t.tid, "b")] = n.attrs["bias"].float().numpy().reshape(-1)
         elif t.kind == "dwconv":
@@ -294,6 +299,27 @@ def tcs_pack(hi: np.ndarray, lo: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(np.stack(parts, axis=2)).reshape(-1)
 
 
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """fp32 → bf16 bit patterns (uint16), round to nearest even (= PTX
+    cvt.rn.bf16.f32 / __float2bfloat16_rn for finite values)."""
+    bits = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    rounded = (bits + 0x7FFF + ((bits >> 16) & 1)) >> 16
+    return rounded.astype(np.uint16)
+
+
+def tcs_pack_bf16(w: np.ndarray) -> np.ndarray:
+    """bf16 weights of the weight-streaming conv's bf16 variants (conv_tcs.cu,
+    7000 + NT): [K][Kpad] → [K/128 tile][Kpad/32 block][4 columns of 8]
+    [128 rows][8] bf16 (the K-major no-swizzle UMMA image), returned as the
+    fp32 words holding the bf16 pairs."""
+    k_out, kpad = w.shape
+    tiles, nkb = (k_out + TCS_BM - 1) // TCS_BM, kpad // 32
+    wp = np.zeros((tiles * TCS_BM, kpad), dtype=np.float32)
+    wp[:k_out] = w
+    img = bf16_round(wp).reshape(tiles, TCS_BM, nkb, 4, 8).transpose(0, 2, 3, 1, 4)
+    return np.ascontiguousarray(img).reshape(-1).view(np.float32)
+
+
 def sep_tc_layout(C: int, K: int) -> tuple[int, int]:
     """(Cpad, BN) of the tcgen05 sepconv (csrc/kernels/sepconv_tc.cu
     sep_tc_blocking): K chunks of 16 input channels; all K <= 256 outputs in
@@ -331,7 +357,7 @@ def tf32_round(a: np.ndarray) -> np.ndarray:
 
 
 def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict,
-                  conv_impl: str = "simt"):
+                  conv_impl: str = "simt", precision: str = "fp32"):
     """Encode every task as an sw_op_desc; pointers via base_of(storage)."""
     ops = (N.OpDesc * len(prog.tasks))()
     for t in prog.tasks:
@@ -403,6 +429,7 @@ def lower_program(prog: Program, base_of, weight_base: int, weight_offsets: dict
                 q[PT_W_TC_HI] = wptr("w_tc_hi")
                 q[PT_W_TC_LO] = wptr("w_tc_lo")
                 q[PT_WS] = wptr("w_tcs")  # weight-streaming variants' packed images (small M only)
+                vals[SP_WS_KIND] = 1 if precision == "bf16" else 0
                 M = nb * P * Q
                 Kdim = R * S * c
                 vals[SP_KPAD] = (Kdim + TC_BK - 1) // TC_BK * TC_BK
@@ -534,13 +561,19 @@ class Engine:
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
                  tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb",
                  fuse_sep_pairs: bool = False, l2_prefetch: bool = False,
-                 max_streams: int | None = None):
+                 max_streams: int | None = None, precision: str = "fp32"):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
         self.model = model.eval()
         self.multi_stream = multi_stream
         self.max_streams = max_streams
+        if precision not in ("fp32", "bf16"):
+            raise ValueError(f"precision must be 'fp32' or 'bf16', not {precision!r}")
+        # "bf16": the batch-1 weight-streaming contractions may run in bf16
+        # (kind::f16, fp32 accumulate) — a separately stated tolerance
+        # (DESIGN §7); every other kernel stays fp32
+        self.precision = precision
         self.fuse = fuse
         self.device = device
         self.conv_impl = conv_impl
@@ -617,7 +650,7 @@ class Engine:
         self.base_map = base_map
 
         # packed parameters (one device allocation, 256-B aligned slices)
-        arrays = _pack_weights(prog)
+        arrays = _pack_weights(prog, self.precision)
         woff = {}
         total = 0
         for key, a in arrays.items():
@@ -629,7 +662,8 @@ class Engine:
         self.weights = torch.from_numpy(host).to(dev)
         self.weight_bytes = total
         self.ops = lower_program(prog, lambda st: base_map[st.sid], self.weights.data_ptr(), woff,
-                                 conv_impl="tc" if self.conv_impl == "tc" else "simt")
+                                 conv_impl="tc" if self.conv_impl == "tc" else "simt",
+                                 precision=self.precision)
 
         out = prog.output_view
         self.out_shape = tuple(prog.out_shape) or tuple(self.model_output_shape(prog))
@@ -761,7 +795,8 @@ class Engine:
                 cands += [(K_SEPCONV, v, 2) for v, (bm, bn) in SEP_TILES.items()
                           if SEP_TMA_FIRST <= v < SEP_ROW_FIRST and 2 <= math.ceil(K / bn) <= 8]
             else:
-                cands = conv_candidates(M, K, Kdim, p[SP_R], p[SP_S], (p[SP_PAD_H], p[SP_PAD_W]))
+                cands = conv_candidates(M, K, Kdim, p[SP_R], p[SP_S], (p[SP_PAD_H], p[SP_PAD_W]),
+                                        bf16=self.precision == "bf16")
             timed = []
             for kind, variant, split in cands:
                 trial.kind = kind
@@ -792,7 +827,9 @@ class Engine:
                     self._out_tensor(t).fill_(float("nan"))
                     N.check(lib.sw_engine_run_op(self._h, C.byref(trial)))
                     err = (self._out_tensor(t) - ref_out).abs().max().item()
-                    if not err <= tol:  # NaN-safe
+                    # bf16 candidates are checked at the bf16 tolerance
+                    lim = tol * BF16_TUNE_RTOL / rtol if 7000 <= cand[2] < 8000 else tol
+                    if not err <= lim:  # NaN-safe
                         self.tuning_rejected.setdefault(t.tid, []).append((cand[1:], err))
                         continue
                 best = cand

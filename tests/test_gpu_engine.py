@@ -218,6 +218,77 @@ def test_tcgen05_weight_streaming(nt, split, cin, cout, k, s, p, hw, batch, pre)
     eng.close()
 
 
+# bf16 path (Engine(precision="bf16")): a separately stated tolerance.  The
+# weight-streaming variants 7000 + NT round weights and activations to bf16
+# and accumulate in fp32; against the same product computed by torch from
+# bf16-rounded operands the only differences are accumulation order and the
+# rare bf16 rounding flip of an activation that differs in its last fp32 bits
+# → |d| <= 2e-3 * max|ref|; against the fp32 CPU output the bf16 rounding
+# itself (2^-9 relative per operand) → relative L2 <= 1e-2.
+BF16_EMU_TOL = 2e-3
+BF16_REL_L2 = 1e-2
+
+
+@pytest.mark.parametrize("nt", [32, 64, 128])
+@pytest.mark.parametrize("split", [1, 4, 16])
+@pytest.mark.parametrize("cin,cout,k,s,p,hw,batch,pre", [
+    (256, 200, 3, 1, 1, 14, 1, True),
+    (64, 128, 3, 2, 1, 15, 2, False),
+    (1024, 300, 1, 1, 0, 7, 1, False),
+    (44, 64, 5, 1, 2, 9, 1, True),
+])
+def test_tcgen05_weight_streaming_bf16(nt, split, cin, cout, k, s, p, hw, batch, pre):
+    import torch.nn.functional as F
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
+    torch.manual_seed(7)
+    lead = nn.Conv2d(cin, cin, 1, bias=False)
+    last = nn.Conv2d(cin, cout, k, s, p, bias=True)
+    m = nn.Sequential(lead, *([nn.ReLU()] if pre else []), last).eval()
+    x = torch.randn(batch, cin, hw, hw)
+    with torch.no_grad():
+        ref = m(x)
+        h = lead(x)
+        if pre:
+            h = torch.relu(h)
+        emu = F.conv2d(h.bfloat16().float(), last.weight.bfloat16().float(), last.bias, s, p)
+    eng = Engine(m, conv_impl="tc", precision="bf16").prepare(x)
+    d = eng.ops[len(eng.program.tasks) - 1]
+    assert d.kind == K_CONV_TC
+    d.variant = 7000 + nt
+    d.params[SP_SPLIT_K] = split
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    y = eng.device_output().cpu()
+    assert (y - emu).abs().max().item() <= BF16_EMU_TOL * max(1.0, emu.abs().max().item())
+    assert ((y - ref).norm() / ref.norm()).item() <= BF16_REL_L2
+    eng.close()
+
+
+# network-level bf16 tolerance: logits of O(1) within 5e-2 max
+# abs and 5e-2 relative L2 of the fp32 CPU forward (measured r02zc: ResNet-50
+# 4.1e-2 / 1.9e-2, Inception-v3 1.6e-2 / 2.4e-2)
+BF16_NET_ABS = 5e-2
+BF16_NET_REL_L2 = 5e-2
+
+
+@pytest.mark.parametrize("name", ["resnet50", "inception_v3"])
+def test_network_parity_bf16(name):
+    from oracle.numerics import cpu_forward
+    model, shape = build_model(name)
+    x = example_input(shape)
+    eng = Engine(model, precision="bf16").prepare(x)
+    assert any(7000 <= d.variant < 8000 for d in eng.ops[:len(eng.program.tasks)]), "no bf16 kernel picked"
+    y = eng(x)
+    ref = cpu_forward(model, x)
+    assert (y - ref).abs().max().item() <= BF16_NET_ABS
+    assert ((y - ref).norm() / ref.norm()).item() <= BF16_NET_REL_L2
+    eng.close()
+
+
 @pytest.mark.parametrize("split", [1, 4])
 def test_tcgen05_weight_streaming_residual(split):
     """Residual add + ReLU fused into the weight-streaming conv's epilogue."""
