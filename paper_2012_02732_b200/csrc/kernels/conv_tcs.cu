@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
     // every rank's ring is dead (its last MMA completed) before anyone writes into it
     cluster_arrive_relaxed();
     cluster_wait();
+    if (tid == 0) probe_trace(60);  // every rank's ring is dead
     if (tid == 0) {
       mbar_expect_tx(su32(recv), (uint32_t)((a.split - 1) * R * L::ROW));
 #pragma unroll 1
@@ -439,17 +440,32 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
       bulk_commit();
     }
     if (warp < 4) mbar_wait_parity(su32(recv), 0);
+    if (tid == 0) probe_trace(61);  // peers' rows in
   }
   if (warp < 4) {
-    // thread → (channel tid % 64, every other pixel row from tid / 64)
+    // thread = output channel; its rows are independent, so the loop is
+    // unrolled for ILP and the (image, row, column) of consecutive pixels is
+    // advanced incrementally (a single warp per sub-partition runs this
+    // tail: the per-row divisions and dependent smem / store chain of a
+    // rolled loop cost ~0.35 us per pixel row, probe r02ze)
     const int cl = tid & (TCS_BM - 1);
     const int n = n0 + cl;
     const float bias = (a.bias && n < a.K) ? a.bias[n] : 0.f;
-#pragma unroll 1
-    for (int j = tid / TCS_BM; j < R; j += 128 / TCS_BM) {
+    constexpr int STEP = 128 / TCS_BM;
+    const int j0 = tid / TCS_BM;
+    const int rows = min(R, a.M - (m0 + me * R));
+    int qq = 0, pp = 0, nb = 0;
+    {
+      const int m = m0 + me * R + j0;
+      qq = m % a.Q;
+      const int tt = m / a.Q;
+      pp = tt % a.P;
+      nb = tt / a.P;
+    }
+    if (tid == 0) probe_trace(62);
+#pragma unroll 4
+    for (int j = j0; j < rows; j += STEP) {
       const int p = me * R + j;
-      const int m = m0 + p;
-      if (m >= a.M) break;
       float v = part[p * TCS_BM + cl];
       if (a.split > 1) {
         float t[15];
@@ -461,13 +477,17 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
           if (r < a.split - 1) v += t[r];
       }
       if (n < a.K) {
-        const int qq = m % a.Q;
-        const int tt = m / a.Q;
-        const int pp = tt % a.P;
-        const int nb = tt / a.P;
         v += bias;
         if (a.has_res) v += a.res[nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + n * a.res_sc];
         a.out[nb * a.out_sn + pp * a.out_sh + qq * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
+      }
+      qq += STEP;
+      while (qq >= a.Q) {
+        qq -= a.Q;
+        if (++pp == a.P) {
+          pp = 0;
+          ++nb;
+        }
       }
     }
     probe_pt(6);
