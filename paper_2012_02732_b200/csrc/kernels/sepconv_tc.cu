@@ -148,9 +148,12 @@ __device__ __forceinline__ void st_tile(const SepTcArgs& a, int tile, int& n0, i
   r0 = (tile % a.bands) * a.TH;
 }
 
+// ST_PY <= 3: register-blocked items (ST_PY output rows); ST_PY >= 4
+// (stride 1, wide maps): sliding-row producers with PXN = ST_PY columns
 template <int KS, int SW, int ST_PY>
 __global__ void __launch_bounds__(ST_THREADS, 1)
     sepconv_tc_kernel(const __grid_constant__ CUtensorMap tin, SepTcArgs a) {
+  constexpr bool SLIDE = SW == 1 && ST_PY >= 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = su32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -231,7 +234,91 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                  reinterpret_cast<const char*>(a.w_pw) + (size_t)kc * a.b_bytes, a.b_bytes, b_full(g));
       }
     }
-  } else if (warp < G * ST_GROUP_WARPS) {
+  } else if (SLIDE && warp < G * ST_GROUP_WARPS) {
+    // ---------------- depthwise producers (stride 1, wide maps: sliding rows) ----------------
+    // thread = (one channel of the 16-channel chunk, a block of PXN output
+    // columns of one image); it sweeps the tile's input rows once, each row
+    // read as a PXN + k - 1 scalar register window, and keeps the k output
+    // rows the row contributes to as rotating register accumulators.  A
+    // finished output row is split into TF32 hi / lo and stored into the
+    // group's A stage as soon as it completes.  (28x28 NASNet maps at bs256:
+    // 84 → 66 us per 44-channel 5x5 layer; narrower maps keep the items,
+    // profiles/r02_ab_sepconv_producers.txt)
+    constexpr int PXN = SLIDE ? ST_PY : 1;
+    constexpr int WN = PXN + KS - 1;
+    const int g = warp / ST_GROUP_WARPS;
+    const int gt = threadIdx.x - g * ST_GROUP_WARPS * 32;
+    const int ch = gt & (ST_CK - 1);
+    const int xblocks = (a.Q + PXN - 1) / PXN;
+    const int nblk = a.TN * xblocks;
+    const int nrows = a.TH + KS - 1;
+    for (int seq = g; seq < total; seq += G) {
+      const int use = seq / G, kc = seq % nchunks, pi = seq % SP;
+      const uint8_t* st = smem + (size_t)pi * a.pstage;
+      mbar_wait_parity(p_full(pi), (seq / SP) & 1);
+      if (use >= 1) mbar_wait_parity(a_empty(g), (use & 1) ^ 1);  // the group's previous MMAs are done
+      const float* patch = reinterpret_cast<const float*>(st);
+      const float* filt = reinterpret_cast<const float*>(st + a.patch_bytes) + ch;  // [k*k][16]
+      const int c = kc * ST_CK + ch;
+      const bool cin = c < a.C;
+      const float bias = bdw[c];
+      uint8_t* ahi = smem + a.off_g + (size_t)g * a.gstage + a.off_a + (ch >> 2) * ST_LBO_A + (ch & 3) * 4;
+      for (int blk = gt >> 4; blk < nblk; blk += (ST_GROUP_WARPS * 32) >> 4) {
+        const int img = blk / xblocks;
+        const int q0 = (blk - img * xblocks) * PXN;
+        const float* prow = patch + ((size_t)img * a.IH * a.IW + q0) * ST_CK + ch;
+        float acc[KS][PXN];
+#pragma unroll
+        for (int j = 0; j < KS; ++j)
+#pragma unroll
+          for (int x = 0; x < PXN; ++x) acc[j][x] = bias;
+#pragma unroll 1
+        for (int ir = 0; ir < nrows; ++ir) {
+          float win[WN];
+#pragma unroll
+          for (int j = 0; j < WN; ++j) {
+            win[j] = prow[((size_t)ir * a.IW + j) * ST_CK];
+            if (a.pre_relu) win[j] = fmaxf(win[j], 0.f);
+          }
+          // acc[j] = output row ir - (KS-1) + j, tap row KS-1-j
+#pragma unroll
+          for (int j = 0; j < KS; ++j) {
+#pragma unroll
+            for (int t = 0; t < KS; ++t) {
+              const float w = filt[((KS - 1 - j) * KS + t) * ST_CK];
+#pragma unroll
+              for (int x = 0; x < PXN; ++x) acc[j][x] = fmaf(win[x + t], w, acc[j][x]);
+            }
+          }
+          const int y = ir - (KS - 1);  // acc[0] is complete
+          if (y >= 0) {
+            const int rbase = (img * a.TH + y) * a.Q + q0;
+#pragma unroll
+            for (int x = 0; x < PXN; ++x) {
+              if (q0 + x >= a.Q) break;
+              const float v = cin ? apply_act(acc[0][x], a.dw_act) : 0.f;
+              const float h = st_rn(v);
+              const int row = rbase + x;
+              const int off = (row >> 3) * 128 + (row & 7) * 16;
+              *reinterpret_cast<float*>(ahi + off) = h;
+              *reinterpret_cast<float*>(ahi + ST_AHALF + off) = st_rn(v - h);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < KS - 1; ++j)
+#pragma unroll
+            for (int x = 0; x < PXN; ++x) acc[j][x] = acc[j + 1][x];
+#pragma unroll
+          for (int x = 0; x < PXN; ++x) acc[KS - 1][x] = bias;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) st_arrive(p_empty(pi));  // every patch read of this warp is done
+      fence_proxy_async_cta();
+      __syncwarp();
+      if (lane == 0) st_arrive(a_full(g));
+    }
+  } else if (!SLIDE && warp < G * ST_GROUP_WARPS) {
     // ---------------- depthwise producers ----------------
     // item = (image, PY x PX block of output pixels, channel quad), quad
     // fastest.  Per output quad ~k*k/PX filter and ((PY-1)*s+k)((PX-1)*s+k)/
@@ -474,12 +561,17 @@ int launch_sepconv_tc(const sw_op_desc& op, void* stream) {
   const int s = a.sh;
   a.TH = std::min(a.P, ST_BM / a.Q);
   a.TN = a.TH == a.P ? std::min(a.N, std::max(1, ST_BM / (a.P * a.Q))) : 1;
-  a.IW = (((a.Q + ST_PX - 1) / ST_PX) * ST_PX - 1) * s + ks;  // every window column an item reads
+  // stride 1 on wide maps (Q >= 21): sliding-row producers, 7 columns per thread
+  const bool slide = s == 1 && ks <= 5 && a.Q >= 21;
+  constexpr int SLIDE_PXN = 7;
+  a.IW = slide ? (a.Q + SLIDE_PXN - 1) / SLIDE_PXN * SLIDE_PXN + ks - 1
+               : (((a.Q + ST_PX - 1) / ST_PX) * ST_PX - 1) * s + ks;  // every window column an item reads
   a.filt_bytes = (uint32_t)(ks * ks * ST_CK * 4);
   a.b_bytes = 2u * (uint32_t)a.BN * ST_CK * 4u;
   int PY = 3;
   auto layout = [&](int g, int sp) {
-    a.IH = (((a.TH + PY - 1) / PY) * PY - 1) * s + ks;  // rows of the last (ragged) block too
+    a.IH = slide ? a.TH + ks - 1
+                 : (((a.TH + PY - 1) / PY) * PY - 1) * s + ks;  // rows of the last (ragged) block too
     a.patch_bytes = (uint32_t)(a.TN * a.IH * a.IW * ST_CK * 4);
     a.pstage = (a.patch_bytes + a.filt_bytes + 1023u) / 1024u * 1024u;  // TMA destinations aligned
     a.off_b = 0;
@@ -530,9 +622,11 @@ int launch_sepconv_tc(const sw_op_desc& op, void* stream) {
   const int grid = std::min(a.ntile, 148);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t rc = cudaErrorInvalidValue;
+  if (slide) PY = SLIDE_PXN;
 #define SW_SEPTC(K_, S_, PY_)                                                                             \
   if (ks == K_ && s == S_ && PY == PY_)                                                                 \
     rc = launch_k(sepconv_tc_kernel<K_, S_, PY_>, dim3(grid), dim3(ST_THREADS), smem, st, 1u, tin, a);
+  SW_SEPTC(3, 1, 7) SW_SEPTC(5, 1, 7)
   SW_SEPTC(3, 1, 3) SW_SEPTC(5, 1, 3)
   SW_SEPTC(3, 1, 2) SW_SEPTC(5, 1, 2) SW_SEPTC(7, 1, 2) SW_SEPTC(3, 2, 2) SW_SEPTC(5, 2, 2) SW_SEPTC(7, 2, 2)
 #undef SW_SEPTC
@@ -542,6 +636,7 @@ int launch_sepconv_tc(const sw_op_desc& op, void* stream) {
 void init_sep_tc_kernels() {
 #define SW_SEPTC_ATTR(K_, S_, PY_) \
   cudaFuncSetAttribute(sepconv_tc_kernel<K_, S_, PY_>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM_MAX);
+  SW_SEPTC_ATTR(3, 1, 7) SW_SEPTC_ATTR(5, 1, 7)
   SW_SEPTC_ATTR(3, 1, 3) SW_SEPTC_ATTR(5, 1, 3)
   SW_SEPTC_ATTR(3, 1, 2) SW_SEPTC_ATTR(5, 1, 2) SW_SEPTC_ATTR(7, 1, 2)
   SW_SEPTC_ATTR(3, 2, 2) SW_SEPTC_ATTR(5, 2, 2) SW_SEPTC_ATTR(7, 2, 2)
