@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
   const int tstride = (int)gridDim.x;
   const int ntiles = t0 < a.ntile ? (a.ntile - 1 - t0) / tstride + 1 : 0;
   const int total = ntiles * nchunks;  // chunk sequence of this CTA
+  probe_begin();
 
   // barriers: p_full[SP], p_empty[SP], b_full[G], a_full[G], a_empty[G], t_full[2], t_empty[2], tmem slot
   const int SP = a.SP;
@@ -177,6 +178,9 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
   auto t_empty = [&](int b) { return bar + 8u * (uint32_t)(2 * ST_MAX_SP + 3 * ST_MAX_G + 2 + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + a.off_bar + 8 * (2 * ST_MAX_SP + 3 * ST_MAX_G + 4));
   float* bdw = reinterpret_cast<float*>(smem + a.off_bdw);  // [Cpad] depthwise bias
+  float* bpw = bdw + a.Cpad;  // [BN] pointwise bias: the epilogue reads it from smem (a global
+                              // __ldg per 4 channels missed the tiny L1 and cost an L2 round
+                              // trip per 16 outputs, ~0.8 us per group, probe r02zj)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SP; ++i) {
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   for (int c = threadIdx.x; c < a.Cpad; c += ST_THREADS) bdw[c] = (a.b_dw && c < a.C) ? a.b_dw[c] : 0.f;
+  for (int c = threadIdx.x; c < BN; c += ST_THREADS) bpw[c] = (a.b_pw && c < a.K) ? a.b_pw[c] : 0.f;
   st_fence_before();
   __syncthreads();
   st_fence_after();
@@ -469,6 +474,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
       int n0, r0;
       st_tile(a, t0 + ti * tstride, n0, r0);
       mbar_wait_parity(t_full(b), tuse & 1);
+      if (row == 0 && ti < 4) probe_trace(32 + 8 * ti);  // accumulators of tile ti ready
       st_fence_after();
       const int img = row / per_img, rr = row % per_img;
       const int n = n0 + img, p = r0 + rr / a.Q, q = rr % a.Q;
@@ -476,34 +482,69 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
       float* o = a.out + (ok ? n * a.out_sn + p * a.out_sh + q * a.out_sw : 0);
       const float* rp = (a.has_res && ok) ? a.res + n * a.res_sn + p * a.res_sh + q * a.res_sw : nullptr;
       const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * 2 * BN);
+      // TMEM → registers is software-pipelined: group k0 + 16's loads are in
+      // flight while group k0 is stored (a tcgen05.ld round trip is ~0.5 us
+      // while the next tile's MMAs run, probe r02zi; stores are not the cost)
+      // residual (global, an L2 round trip) and TMEM groups are prefetched one
+      // 16-channel group ahead of the one being stored
+      const bool rvec = rp && a.ovec;
+      float v[16], w[16];
+      float4 r4[4];
+      st_ld16(tl, v);
+      st_ld16(tl + (uint32_t)BN, w);
+      if (rvec && ok && 16 <= a.K) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r4[j] = *reinterpret_cast<const float4*>(rp + 4 * j);
+      }
+      st_tc_wait_ld();
       for (int k0 = 0; k0 < BN; k0 += 16) {
-        float v[16], w[16];
-        st_ld16(tl + (uint32_t)k0, v);
-        st_ld16(tl + (uint32_t)(BN + k0), w);
-        st_tc_wait_ld();
-        if (!ok || k0 >= a.K) continue;
+        float vn[16], wn[16];
+        float4 rn[4];
+        const bool more = k0 + 16 < BN;
+        if (more) {
+          st_ld16(tl + (uint32_t)(k0 + 16), vn);
+          st_ld16(tl + (uint32_t)(BN + k0 + 16), wn);
+          if (rvec && ok && k0 + 32 <= a.K) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] += w[j];
-        if (a.ovec && k0 + 16 <= a.K) {
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            if (a.b_pw) x = f4add(x, __ldg(reinterpret_cast<const float4*>(a.b_pw + k0 + j)));
-            if (rp) x = f4add(x, *reinterpret_cast<const float4*>(rp + k0 + j));
-            *reinterpret_cast<float4*>(o + k0 + j) = act4(x, a.act);
+            for (int j = 0; j < 4; ++j) rn[j] = *reinterpret_cast<const float4*>(rp + k0 + 16 + 4 * j);
           }
-        } else {
+        }
+        if (row == 0 && ti < 4 && k0 < 48) probe_trace(33 + 8 * ti + k0 / 16 * 2);  // TMEM group k0 in
+        if (ok && k0 < a.K) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += w[j];
+          if (a.ovec && k0 + 16 <= a.K) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              x = f4add(x, *reinterpret_cast<const float4*>(bpw + k0 + j));
+              if (rp) x = f4add(x, r4[j / 4]);
+              *reinterpret_cast<float4*>(o + k0 + j) = act4(x, a.act);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (k0 + j >= a.K) break;
+              float x = v[j] + bpw[k0 + j];
+              if (rp) x += rp[k0 + j];
+              o[k0 + j] = apply_act(x, a.act);
+            }
+          }
+        }
+        if (more) {
+          st_tc_wait_ld();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            if (k0 + j >= a.K) break;
-            float x = v[j] + (a.b_pw ? a.b_pw[k0 + j] : 0.f);
-            if (rp) x += rp[k0 + j];
-            o[k0 + j] = apply_act(x, a.act);
+            v[j] = vn[j];
+            w[j] = wn[j];
           }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r4[j] = rn[j];
         }
       }
       st_fence_before();
       __syncwarp();
+      if (row == 0 && ti < 4) probe_trace(39 + 8 * ti);  // tile ti stored
       if (lane == 0) st_arrive(t_empty(b));
     }
   }
@@ -513,6 +554,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     st_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
   }
+  probe_end();
 }
 
 // Channel padding shared with the host packer (engine.py sep_tc_layout):
@@ -579,7 +621,7 @@ int launch_sepconv_tc(const sw_op_desc& op, void* stream) {
     a.gstage = (a.off_a + 2u * ST_AHALF + 127u) / 128u * 128u;
     a.off_g = (uint32_t)sp * a.pstage;
     a.off_bdw = a.off_g + (uint32_t)g * a.gstage;
-    a.off_bar = (a.off_bdw + (uint32_t)a.Cpad * 4u + 15u) / 16u * 16u;
+    a.off_bar = (a.off_bdw + (uint32_t)(a.Cpad + a.BN) * 4u + 15u) / 16u * 16u;
     return (size_t)a.off_bar + 8 * (2 * ST_MAX_SP + 3 * ST_MAX_G + 4) + 16;
   };
   // output rows per depthwise thread: the block height that wastes least

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--tuning-cache", default=None)
     ap.add_argument("--no-pdl", action="store_true", help="time the chains without programmatic dependent launch")
     ap.add_argument("--sm-mhz", type=float, default=1965.0, help="SM clock for the clock64 phase stamps")
+    ap.add_argument("--force", default=None, help="kind,variant,split to time instead of the tuned pick")
     a = ap.parse_args()
 
     import numpy as np
@@ -65,6 +66,10 @@ def main():
     for tid in tids:
         t = eng.program.tasks[tid]
         d = eng.ops[tid]
+        if a.force:
+            fk, fv, fs = (int(v) for v in a.force.split(","))
+            d.kind, d.variant = fk, fv
+            d.params[30] = fs  # SP_SPLIT_K
         lib.sw_probe_reset()
         us = C.c_double()
         N.check(lib.sw_engine_time_op(eng._h, C.byref(d), a.reps, C.byref(us)))
