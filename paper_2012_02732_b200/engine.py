@@ -125,7 +125,7 @@ def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
 
 # csrc/kernels/conv_tcs.cu: pixel tile widths (UMMA N) of variants 6000 + NT
 TCS_TILES = (32, 64, 128)
-TCS_MAX_M = 1024  # pixels per image batch up to which those variants are candidates
+TCS_MAX_M = 4096  # pixels per image batch up to which those variants are candidates
 BF16_TUNE_RTOL = 3e-2  # autotuner check of a bf16 candidate: |d| <= 3e-2 * max(1, max|ref|)
 
 
@@ -186,7 +186,7 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
         # weight-streaming swap-AB tcgen05 kernel (conv_tcs.cu): out channels on
         # the UMMA M side, NT pixels per tile, split-K cluster <= 16
         for nt in TCS_TILES:
-            if nt > 2 * max(M, 16) or math.ceil(M / nt) > 8:
+            if nt > 2 * max(M, 16) or math.ceil(M / nt) > 32:
                 continue
             ctas = math.ceil(K / TCS_BM) * math.ceil(M / nt)
             for split in (1, 2, 4, 8, 16):
