@@ -515,6 +515,7 @@ def run_ours(args, world, rank, local):
                               "note": "requests back to back, next H2D overlapped with the current replay; "
                                       "L2 not flushed between requests"},
             "gpu_launches": n_tasks * args.steps,
+            "tcgen05_tasks": sum(1 for d in eng.ops[:n_tasks] if d.kind == 6 or (d.kind == 8 and d.variant == 100)),
             "tasks": n_tasks, "streams": eng.assignment.num_streams, "syncs": len(eng.plan),
             "arena": {"mode": eng.arena_mode, "bytes": int(eng.arena.numel()),
                       "never_free_bytes": int(eng.arena_layout.reference_total) if eng.arena_layout else None},
