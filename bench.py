@@ -617,8 +617,8 @@ def other_configs(args, dev, hbm, flush, stream):
             from oracle.numerics import cpu_forward
             ref = cpu_forward(model, x)
             err, rel = (y - ref).abs().max().item(), ((y - ref).norm() / ref.norm()).item()
-            parity = {"max_abs_err": err, "rel_l2": rel, "tolerance": "bf16: max abs 5e-2, rel L2 5e-2",
-                      "ok": bool(err <= 5e-2 and rel <= 5e-2)}
+            parity = {"max_abs_err": err, "rel_l2": rel, "tolerance": "bf16: max abs 1e-1, rel L2 5e-2",
+                      "ok": bool(err <= 1e-1 and rel <= 5e-2)}
         else:
             parity = _parity(model, x, y)
         eng.load_input_device(x)
