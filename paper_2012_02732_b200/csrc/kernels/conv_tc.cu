@@ -947,6 +947,7 @@ static int launch_tc_tma(const TcArgs& a, const sw_op_desc& op, cudaStream_t st)
 
 int launch_conv_tc(const sw_op_desc& op, void* stream) {
   if (op.variant >= 6000 && op.variant < 8000) return launch_conv_tcs(op, stream);
+  if (op.variant >= 8000 && op.variant < 9000) return launch_conv_pw_tc(op, stream);
   TcArgs a = tc_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a.M == 0 || a.K == 0) return 0;

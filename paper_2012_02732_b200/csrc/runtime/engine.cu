@@ -287,6 +287,7 @@ int sw_engine_create(int32_t device, sw_engine** out) {
   CU(cudaStreamCreateWithFlags(&e->launch, cudaStreamNonBlocking));
   sw::init_tc_kernels();
   sw::init_tcs_kernels();
+  sw::init_pw_tc_kernels();
   sw::init_simt_kernels();
   sw::init_pw_kernels();
   sw::init_sep_kernels();

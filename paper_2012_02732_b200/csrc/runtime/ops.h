@@ -193,6 +193,10 @@ void init_tc_kernels();
 // few output pixels (conv_tcs.cu)
 int launch_conv_tcs(const sw_op_desc& op, void* stream);
 void init_tcs_kernels();
+// K_CONV_TC variants 8000 + BN: large-batch pointwise conv, persistent
+// warp-specialised tcgen05 GEMM with double-buffered TMEM (conv_pw_tc.cu)
+int launch_conv_pw_tc(const sw_op_desc& op, void* stream);
+void init_pw_tc_kernels();
 void init_simt_kernels();
 void init_pw_kernels();
 int launch_sepconv(const sw_op_desc& op, void* stream);

@@ -125,6 +125,8 @@ def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
 
 # csrc/kernels/conv_tcs.cu: pixel tile widths (UMMA N) of variants 6000 + NT
 TCS_TILES = (32, 64, 128)
+# csrc/kernels/conv_pw_tc.cu: output-channel tiles of variants 8000 + BN
+PWTC_TILES = (48, 64, 96, 128)
 TCS_MAX_M = 4096  # pixels per image batch up to which those variants are candidates
 # the bf16 variants stay in the weight-streaming regime their tolerance was
 # stated for: more bf16 layers compound the bf16 rounding
@@ -185,6 +187,13 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
                 if bn <= 128 and split == 1 and M >= 4096:  # persistent tile loop (+ 128-B swizzle)
                     out.append((K_CONV_TC, 3000 + bn, 1))
                     out.append((K_CONV_TC, 4000 + bn, 1))
+    if pointwise and M >= 4096:
+        # large-batch pointwise: persistent warp-specialised tcgen05 GEMM
+        # (conv_pw_tc.cu), BN output channels per N tile
+        for bn in PWTC_TILES:
+            if bn > 2 * max(K, 16) or (bn < K and math.ceil(K / bn) * bn - K >= bn // 2 and bn != 128):
+                continue
+            out.append((K_CONV_TC, 8000 + bn, 1))
     if M <= TCS_MAX_M:
         # weight-streaming swap-AB tcgen05 kernel (conv_tcs.cu): out channels on
         # the UMMA M side, NT pixels per tile, split-K cluster <= 16
@@ -860,6 +869,9 @@ class Engine:
                 return cd(M / 128)
             bm, bn = PW_TILES[variant] if variant >= 16 else SIMT_TILES[variant]
             return cd(M / bm) * cd(K / bn) * max(1, split)
+        if kind == K_CONV_TC and variant >= 8000:
+            ntn = cd(K / (variant % 1000))
+            return min(cd(M / 128), max(1, NUM_SMS // ntn)) * ntn
         if kind == K_CONV_TC and variant >= 6000:
             return cd(K / TCS_BM) * cd(M / (variant % 1000)) * max(1, split)
         if kind == K_CONV_TC:

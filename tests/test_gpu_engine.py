@@ -130,6 +130,53 @@ def test_tcgen05_tma_persistent(bn, cin, cout, hw, batch, pre):
     eng.close()
 
 
+@pytest.mark.parametrize("bn", [48, 64, 96, 128])
+@pytest.mark.parametrize("cin,cout,hw,batch,pre,res", [(264, 44, 28, 8, True, False), (528, 176, 14, 20, False, True),
+                                                       (64, 200, 17, 20, True, True), (1056, 88, 7, 90, False, False),
+                                                       (44, 48, 9, 60, False, False)])
+def test_tcgen05_pointwise_persistent_ws(bn, cin, cout, hw, batch, pre, res):
+    """Large-batch pointwise conv on the persistent warp-specialised tcgen05
+    kernel (variants 8000 + BN, conv_pw_tc.cu): every N tile width, ragged
+    M / N / K, several N tiles, pre-ReLU, fused BN bias and a residual."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
+    torch.manual_seed(8)
+
+    class M(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.lead = nn.Conv2d(cin, cin, 1, bias=False)
+            self.c = Conv(cin, cout, 1, 1, 0, bias=False, act=None, bn=True)
+            self.r = nn.Conv2d(cin, cout, 1, bias=False)
+            self.tail = nn.Conv2d(cout, 8, 1, bias=False)  # the tested conv writes an NHWC activation
+
+        def forward(self, x):
+            h = self.lead(x)
+            if pre:
+                h = torch.relu(h)
+            y = self.c(h)
+            return self.tail(y + self.r(x) if res else y)
+
+    m = M().eval()
+    x = torch.randn(batch, cin, hw, hw)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="tc").prepare(x)
+    tids = [t.tid for t in eng.program.tasks if t.kind == "conv" and t.name.startswith("c.")]
+    assert len(tids) == 1
+    d = eng.ops[tids[0]]
+    assert d.kind == K_CONV_TC
+    d.variant = 8000 + bn
+    d.params[SP_SPLIT_K] = 1
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 @pytest.mark.parametrize("bn", [32, 64, 128, 256, 1032, 1064, 4032, 4064, 4128, 4256])
 @pytest.mark.parametrize("split", [1, 2, 8, 16])
 @pytest.mark.parametrize("cin,cout,hw,batch,pre", [(264, 88, 28, 2, True), (1056, 200, 7, 1, False),
