@@ -757,6 +757,7 @@ def train_configs(args, dev, world=1, rank=0):
                "aot_over_eager": round(eager_us / multi_us, 4),
                "tasks": len(eng.prog.tasks), "streams": eng.assignment.num_streams,
                "syncs": len(eng.plan), "allreduce": eng.allreduce,
+               "tcgen05_tasks": sum(1 for t in eng.prog.tasks if eng.ops[t.tid].kind == 6),
                "params": eng.builder.param_count, "prepare_s": round(time.perf_counter() - t0, 2)}
         eng.close()
         if rank == 0 and world == 1 and not args.skip_cpu:

@@ -23,7 +23,10 @@
 //    drain them (TMEM lane = pixel) with bias (shared memory) + residual +
 //    activation into NHWC, while the next tile's MMAs fill the other pair.
 //
-// Variants 8000 + BN (BN = 48, 64, 96, 128 output channels per N tile).
+// Variants 8000 + BN (BN = 48, 64, 96, 128 output channels per N tile) read
+// the prepare-time 3xTF32 weight copies; 8100 + BN (8148, 8164, 8196, 8228)
+// read the fp32 weight and split it in the kernel (training steps, whose
+// weights change every step).
 #include <algorithm>
 
 #include "common.cuh"
@@ -105,7 +108,11 @@ struct PwArgs {
 
 }  // namespace
 
-template <int BN>
+// WSPLIT: the weights arrive as plain fp32 (the conv's [K][C] weight, e.g. a
+// training step's current parameters) and the split warps split them into
+// tf32 hi / lo beside the activations; otherwise the prepare-time 3xTF32
+// copies are loaded as they are.
+template <int BN, bool WSPLIT>
 __global__ void __launch_bounds__(PW_THREADS, 1)
     conv_pw_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                       const __grid_constant__ CUtensorMap tbl, PwArgs a) {
@@ -166,10 +173,10 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
         const int m0 = ((int)blockIdx.x + (q / kb) * (int)gridDim.x) * PW_BM;
         const int k0 = (q % kb) * PW_BK;
         const uint32_t st = sbase + s * L::STAGE;
-        mbar_expect_tx(su32(&full[s]), L::A_BYTES + 2 * L::B_BYTES);
+        mbar_expect_tx(su32(&full[s]), L::A_BYTES + (WSPLIT ? 1 : 2) * L::B_BYTES);
         tma_load_2d(st, &ta, k0, m0, su32(&full[s]));
         tma_load_2d(st + 2 * L::A_BYTES, &tbh, k0, n0, su32(&full[s]));
-        tma_load_2d(st + 2 * L::A_BYTES + L::B_BYTES, &tbl, k0, n0, su32(&full[s]));
+        if constexpr (!WSPLIT) tma_load_2d(st + 2 * L::A_BYTES + L::B_BYTES, &tbl, k0, n0, su32(&full[s]));
       }
     }
   } else if (warp < 4) {
@@ -187,6 +194,17 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
         const float4 h = make_float4(pw_tf32(x.x), pw_tf32(x.y), pw_tf32(x.z), pw_tf32(x.w));
         hi[i] = h;
         lo[i] = make_float4(pw_tf32(x.x - h.x), pw_tf32(x.y - h.y), pw_tf32(x.z - h.z), pw_tf32(x.w - h.w));
+      }
+      if constexpr (WSPLIT) {
+        float4* bhi = reinterpret_cast<float4*>(smem + s * L::STAGE + 2 * L::A_BYTES);
+        float4* blo = reinterpret_cast<float4*>(smem + s * L::STAGE + 2 * L::A_BYTES + L::B_BYTES);
+#pragma unroll 2
+        for (int i = tid; i < L::B_BYTES / 16; i += 128) {
+          const float4 x = bhi[i];
+          const float4 h = make_float4(pw_tf32(x.x), pw_tf32(x.y), pw_tf32(x.z), pw_tf32(x.w));
+          bhi[i] = h;
+          blo[i] = make_float4(pw_tf32(x.x - h.x), pw_tf32(x.y - h.y), pw_tf32(x.z - h.z), pw_tf32(x.w - h.w));
+        }
       }
       fence_proxy_async_cta();
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -291,7 +309,7 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
   }
 }
 
-template <int BN>
+template <int BN, bool WSPLIT>
 static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   const int64_t* p = op.params;
   const int N = (int)p[SP_N], H = (int)p[SP_H], W = (int)p[SP_W], C = (int)p[SP_C];
@@ -316,15 +334,16 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   // 1x1 / stride 1 / unpadded on dense NHWC pixel rows (a channel slice of a
   // concat is fine), 16-B aligned rows and outputs; NHWC outputs
   const void* in = reinterpret_cast<const void*>(op.ptrs[PT_IN]);
-  const void* whi = reinterpret_cast<const void*>(op.ptrs[PT_W_TC_HI]);
-  const void* wlo = reinterpret_cast<const void*>(op.ptrs[PT_W_TC_LO]);
+  const void* whi = reinterpret_cast<const void*>(WSPLIT ? op.ptrs[PT_W] : op.ptrs[PT_W_TC_HI]);
+  const void* wlo = reinterpret_cast<const void*>(WSPLIT ? op.ptrs[PT_W] : op.ptrs[PT_W_TC_LO]);
   if (p[SP_R] != 1 || p[SP_S] != 1 || p[SP_STRIDE_H] != 1 || p[SP_STRIDE_W] != 1 || p[SP_PAD_H] || p[SP_PAD_W] ||
       in_sc != 1 || C % 4 || (in_sw & 3) || (op.ptrs[PT_IN] & 15) || in_sn != (int64_t)H * W * in_sw ||
-      in_sh != (int64_t)W * in_sw || osc != 1 || (a.has_res && rsc != 1) || !whi || !wlo || Kpad % PW_BK ||
+      in_sh != (int64_t)W * in_sw || osc != 1 || (a.has_res && rsc != 1) || !whi || !wlo ||
+      (!WSPLIT && Kpad % PW_BK) ||
       (op.ptrs[PT_OUT] & 15) || (a.out_sw & 3) || (a.out_sh & 3) || (a.out_sn & 3))
     return (int)cudaErrorInvalidValue;
   if (a.has_res && ((op.ptrs[PT_RES] & 15) || (a.res_sw & 3))) return (int)cudaErrorInvalidValue;
-  a.kblocks = Kpad / PW_BK;
+  a.kblocks = WSPLIT ? (C + PW_BK - 1) / PW_BK : Kpad / PW_BK;
   CUtensorMap ta, tbh, tbl;
   {
     const uint64_t dims[2] = {(uint64_t)C, (uint64_t)a.M};
@@ -332,9 +351,10 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
     const uint32_t box[2] = {PW_BK, PW_BM};
     if (!encode_tmap_f32(&ta, in, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return (int)cudaErrorInvalidValue;
   }
-  {
-    const uint64_t dims[2] = {(uint64_t)Kpad, (uint64_t)K};
-    const uint64_t strides[1] = {(uint64_t)Kpad * 4};
+  {  // pre-split copies [K][Kpad], or the fp32 weight [K][C] (1x1)
+    const uint64_t wcols = WSPLIT ? (uint64_t)C : (uint64_t)Kpad;
+    const uint64_t dims[2] = {wcols, (uint64_t)K};
+    const uint64_t strides[1] = {wcols * 4};
     const uint32_t box[2] = {PW_BK, (uint32_t)BN};
     if (!encode_tmap_f32(&tbh, whi, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !encode_tmap_f32(&tbl, wlo, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -343,26 +363,32 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   const int ntn = (K + BN - 1) / BN;
   const int mtiles = (a.M + PW_BM - 1) / PW_BM;
   const int gx = std::max(1, std::min(mtiles, std::max(1, 148 / ntn)));
-  return (int)launch_k(conv_pw_tc_kernel<BN>, dim3((unsigned)gx, (unsigned)ntn), dim3(PW_THREADS),
+  return (int)launch_k(conv_pw_tc_kernel<BN, WSPLIT>, dim3((unsigned)gx, (unsigned)ntn), dim3(PW_THREADS),
                        (size_t)PwSmem<BN>::TOTAL, st, 1u, ta, tbh, tbl, a);
 }
 
 int launch_conv_pw_tc(const sw_op_desc& op, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (op.variant) {
-    case 8048: return launch_pw<48>(op, st);
-    case 8064: return launch_pw<64>(op, st);
-    case 8096: return launch_pw<96>(op, st);
-    case 8128: return launch_pw<128>(op, st);
+    case 8048: return launch_pw<48, false>(op, st);
+    case 8064: return launch_pw<64, false>(op, st);
+    case 8096: return launch_pw<96, false>(op, st);
+    case 8128: return launch_pw<128, false>(op, st);
+    // 8100 + BN: fp32 weights split in-kernel (no prepare-time copies: training)
+    case 8148: return launch_pw<48, true>(op, st);
+    case 8164: return launch_pw<64, true>(op, st);
+    case 8196: return launch_pw<96, true>(op, st);
+    case 8228: return launch_pw<128, true>(op, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }
 
 void init_pw_tc_kernels() {
-  cudaFuncSetAttribute(conv_pw_tc_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, PwSmem<48>::TOTAL);
-  cudaFuncSetAttribute(conv_pw_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, PwSmem<64>::TOTAL);
-  cudaFuncSetAttribute(conv_pw_tc_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, PwSmem<96>::TOTAL);
-  cudaFuncSetAttribute(conv_pw_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, PwSmem<128>::TOTAL);
+#define SW_PW_ATTR(BN_, WS_) \
+  cudaFuncSetAttribute(conv_pw_tc_kernel<BN_, WS_>, cudaFuncAttributeMaxDynamicSharedMemorySize, PwSmem<BN_>::TOTAL);
+  SW_PW_ATTR(48, false) SW_PW_ATTR(64, false) SW_PW_ATTR(96, false) SW_PW_ATTR(128, false)
+  SW_PW_ATTR(48, true) SW_PW_ATTR(64, true) SW_PW_ATTR(96, true) SW_PW_ATTR(128, true)
+#undef SW_PW_ATTR
 }
 
 }  // namespace sw

@@ -126,7 +126,12 @@ def pick_conv_tc(M: int, K: int, Kdim: int) -> tuple[int, int]:
 # csrc/kernels/conv_tcs.cu: pixel tile widths (UMMA N) of variants 6000 + NT
 TCS_TILES = (32, 64, 128)
 # csrc/kernels/conv_pw_tc.cu: output-channel tiles of variants 8000 + BN
+# (pre-split weights) and 8100 + BN (fp32 weights split in the kernel)
 PWTC_TILES = (48, 64, 96, 128)
+
+
+def pw_tc_bn(variant: int) -> int:
+    return variant - (8100 if variant >= 8100 else 8000)
 TCS_MAX_M = 4096  # pixels per image batch up to which those variants are candidates
 # the bf16 variants stay in the weight-streaming regime their tolerance was
 # stated for: more bf16 layers compound the bf16 rounding
@@ -193,7 +198,8 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
         for bn in PWTC_TILES:
             if bn > 2 * max(K, 16) or (bn < K and math.ceil(K / bn) * bn - K >= bn // 2 and bn != 128):
                 continue
-            out.append((K_CONV_TC, 8000 + bn, 1))
+            out.append((K_CONV_TC, 8000 + bn, 1))  # prepare-time 3xTF32 weight copies
+            out.append((K_CONV_TC, 8100 + bn, 1))  # fp32 weights split in the kernel
     if M <= TCS_MAX_M:
         # weight-streaming swap-AB tcgen05 kernel (conv_tcs.cu): out channels on
         # the UMMA M side, NT pixels per tile, split-K cluster <= 16
@@ -870,7 +876,7 @@ class Engine:
             bm, bn = PW_TILES[variant] if variant >= 16 else SIMT_TILES[variant]
             return cd(M / bm) * cd(K / bn) * max(1, split)
         if kind == K_CONV_TC and variant >= 8000:
-            ntn = cd(K / (variant % 1000))
+            ntn = cd(K / pw_tc_bn(variant))
             return min(cd(M / 128), max(1, NUM_SMS // ntn)) * ntn
         if kind == K_CONV_TC and variant >= 6000:
             return cd(K / TCS_BM) * cd(M / (variant % 1000)) * max(1, split)

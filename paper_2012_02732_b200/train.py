@@ -1036,9 +1036,10 @@ class TrainEngine:
     def _autotune(self, reps: int = 5):
         """Kernel selection for the K_CONV tasks (forward convs and 1x1 dgrads),
         as in Engine._autotune: every SIMT / TMA-pointwise tile x split-K
-        candidate timed as a graph-captured chain; tcgen05 candidates are
-        excluded (they need weights pre-split at prepare, and these change every
-        step).  Only activation / gradient buffers are written while timing."""
+        candidate timed as a graph-captured chain; tcgen05 candidates that need
+        weights pre-split at prepare are excluded (these change every step) —
+        the pointwise tcgen05 kernel's in-kernel-split variants stay.  Only
+        activation / gradient buffers are written while timing."""
         lib = N.lib()
         us = C.c_double()
         for t in self.prog.tasks:
@@ -1047,8 +1048,12 @@ class TrainEngine:
                 continue
             p = d.params
             M = p[SP_N] * p[SP_P] * p[SP_Q]
+            # tcgen05 candidates need prepare-time weight copies, except the
+            # pointwise kernel's in-kernel-split variants (8100 + BN), which
+            # read the step's current fp32 weights
             cands = [c for c in conv_candidates(M, p[SP_K], p[SP_R] * p[SP_S] * p[SP_C], p[SP_R], p[SP_S],
-                                                (p[SP_PAD_H], p[SP_PAD_W])) if c[0] != K_CONV_TC]
+                                                (p[SP_PAD_H], p[SP_PAD_W]))
+                     if c[0] != K_CONV_TC or 8100 <= c[1] < 8300]
             trial = N.OpDesc()
             C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
             best = None

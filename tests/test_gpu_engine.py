@@ -130,14 +130,16 @@ def test_tcgen05_tma_persistent(bn, cin, cout, hw, batch, pre):
     eng.close()
 
 
-@pytest.mark.parametrize("bn", [48, 64, 96, 128])
+@pytest.mark.parametrize("bn", [48, 64, 96, 128, 148, 164, 196, 228])
 @pytest.mark.parametrize("cin,cout,hw,batch,pre,res", [(264, 44, 28, 8, True, False), (528, 176, 14, 20, False, True),
                                                        (64, 200, 17, 20, True, True), (1056, 88, 7, 90, False, False),
                                                        (44, 48, 9, 60, False, False)])
 def test_tcgen05_pointwise_persistent_ws(bn, cin, cout, hw, batch, pre, res):
     """Large-batch pointwise conv on the persistent warp-specialised tcgen05
-    kernel (variants 8000 + BN, conv_pw_tc.cu): every N tile width, ragged
-    M / N / K, several N tiles, pre-ReLU, fused BN bias and a residual."""
+    kernel (variants 8000 + BN with prepare-time 3xTF32 weights, 8100 + BN
+    splitting the fp32 weights in the kernel; conv_pw_tc.cu): every N tile
+    width, ragged M / N / K, several N tiles, pre-ReLU, fused BN bias and a
+    residual."""
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
     torch.manual_seed(8)
