@@ -23,11 +23,15 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--k", type=int, default=1)
     ap.add_argument("--kind", type=int, default=6, help="6 = tcgen05, 1 = SIMT")
+    ap.add_argument("--tail", action="store_true",
+                    help="append a 1x1 conv so the tested conv writes an NHWC activation (not the NCHW output)")
     a = ap.parse_args()
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import Engine, K_CONV_TC, SP_SPLIT_K, SLOT_MULTI
-    m = nn.Sequential(nn.Conv2d(a.cin, a.cin, 1), nn.ReLU(),
-                      nn.Conv2d(a.cin, a.cout, a.k, padding=a.k // 2)).eval()
+    layers = [nn.Conv2d(a.cin, a.cin, 1), nn.ReLU(), nn.Conv2d(a.cin, a.cout, a.k, padding=a.k // 2)]
+    if a.tail:
+        layers.append(nn.Conv2d(a.cout, 8, 1))
+    m = nn.Sequential(*layers).eval()
     x = torch.randn(a.batch, a.cin, a.hw, a.hw)
     eng = Engine(m, conv_impl="tc").prepare(x)
     d = eng.ops[1]
