@@ -584,13 +584,17 @@ class Engine:
                  device: int = 0, conv_impl: str = "auto", pdl: bool = True,
                  tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb",
                  fuse_sep_pairs: bool = False, l2_prefetch: bool = False,
-                 max_streams: int | None = None, precision: str = "fp32"):
+                 max_streams: int | None = None, precision: str = "fp32",
+                 fuse_separable: bool = True):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
         self.model = model.eval()
         self.multi_stream = multi_stream
         self.max_streams = max_streams
+        # False: depthwise and pointwise stay separate tasks (the pointwise
+        # then runs on the large-batch tcgen05 GEMM; an A/B option at bs256)
+        self.fuse_separable = fuse_separable
         if precision not in ("fp32", "bf16"):
             raise ValueError(f"precision must be 'fp32' or 'bf16', not {precision!r}")
         # "bf16": the batch-1 weight-streaming contractions may run in bf16
@@ -620,7 +624,8 @@ class Engine:
             raise CudaError("Engine.prepare needs a CUDA device (there is no CPU fallback)")
         t0 = time.perf_counter()
         ex = example.detach().float().cpu().contiguous()
-        prog = build_program(self.model, ex, fuse=self.fuse, fuse_sep_pairs=self.fuse_sep_pairs)
+        prog = build_program(self.model, ex, fuse=self.fuse, fuse_separable=self.fuse_separable,
+                             fuse_sep_pairs=self.fuse_sep_pairs)
         t1 = time.perf_counter()
         g = prog.graph
         f, plan, meg = assign_streams_full(g)
