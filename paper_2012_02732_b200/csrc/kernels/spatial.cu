@@ -211,7 +211,149 @@ static int launch_spatial(const sw_op_desc& op, void* stream) {
   return (int)(v4 ? launch_ks<KIND, 4>(ks, blocks, st, a, total) : launch_ks<KIND, 1>(ks, blocks, st, a, total));
 }
 
-int launch_dwconv(const sw_op_desc& op, void* stream) { return launch_spatial<0>(op, stream); }
-int launch_pool(const sw_op_desc& op, void* stream) { return launch_spatial<1>(op, stream); }
+// a filter tap load the compiler may not CSE across the unrolled rows (keeping
+// all k*k taps live in registers spilled the blocks; each use re-reads L1)
+__device__ __forceinline__ float4 ld_tap(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Variant 1: register-blocked rows (large batches).  A thread owns one
+// channel quad x a TH x PX block of output pixels and walks the block's
+// (TH-1)*SW + KS input rows once; each row is loaded as one (PX-1)*SW + KS
+// float4 window and every tap it feeds is applied from registers (all row /
+// tap indices are compile-time).  Input loads per output drop from k*k to
+// ((TH-1)s+k)((PX-1)s+k)/(TH PX) (5x5, s 1, 2x4 block: 25 → 6); consecutive threads
+// take consecutive channel quads, so every window load is a coalesced
+// NHWC row segment.
+// ---------------------------------------------------------------------------
+template <int KIND, int KS, int SW, int TH, int PX>
+__global__ void __launch_bounds__(256, 2) spatial_rows_kernel(SpatialArgs a, int64_t total, int bands, int cols) {
+  constexpr int NR = (TH - 1) * SW + KS;  // input rows of the block
+  constexpr int WN = (PX - 1) * SW + KS;  // window width
+  pdl_trigger();
+  pdl_wait();
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int64_t)idx >= total) return;
+  const uint32_t CG = (uint32_t)(a.C / 4);
+  const int cg = (int)(idx % CG);
+  uint32_t t = idx / CG;
+  const int bx = (int)(t % (uint32_t)cols);
+  t /= (uint32_t)cols;
+  const int by = (int)(t % (uint32_t)bands);
+  const int n = (int)(t / (uint32_t)bands);
+  const int c = cg * 4;
+  const int p0 = by * TH, q0 = bx * PX;
+  const int ih0 = p0 * SW - a.ph, iw0 = q0 * SW - a.pw;
+  const float* base = a.in + n * a.in_sn + c;
+  const bool avg = KIND == 1 && a.mode == 1, mx = KIND == 1 && a.mode == 0;
+  float4 acc[TH][PX];
+#pragma unroll
+  for (int y = 0; y < TH; ++y)
+#pragma unroll
+    for (int x = 0; x < PX; ++x) acc[y][x] = splat(mx ? -INFINITY : 0.f, float4{});
+#pragma unroll
+  for (int ir = 0; ir < NR; ++ir) {
+    const int ih = ih0 + ir;
+    const bool rok = (unsigned)ih < (unsigned)a.H;
+    const float* rowp = base + (rok ? ih : 0) * a.in_sh;
+    float4 win[WN];
+    bool wok[WN];
+#pragma unroll
+    for (int j = 0; j < WN; ++j) {
+      const int iw = iw0 + j;
+      wok[j] = rok && (unsigned)iw < (unsigned)a.W;
+      float4 v = __ldg(reinterpret_cast<const float4*>(rowp + (wok[j] ? iw : 0) * a.in_sw));
+      if (a.pre_relu) v = relu1(v);
+      win[j] = (wok[j] || mx) ? v : splat(0.f, float4{});
+    }
+#pragma unroll
+    for (int y = 0; y < TH; ++y) {
+      const int r = ir - y * SW;  // tap row of this input row for output row y
+      if (r < 0 || r >= KS) continue;
+#pragma unroll
+      for (int tp = 0; tp < KS; ++tp) {
+        if (KIND == 0) {
+          const float4 w = ld_tap(a.w + (r * KS + tp) * a.C + c);
+#pragma unroll
+          for (int x = 0; x < PX; ++x) fma_acc(acc[y][x], win[x * SW + tp], w);
+        } else if (mx) {
+#pragma unroll
+          for (int x = 0; x < PX; ++x)
+            if (wok[x * SW + tp]) max_to(acc[y][x], win[x * SW + tp]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < PX; ++x) add_to(acc[y][x], win[x * SW + tp]);
+        }
+      }
+    }
+  }
+  const float4 bias = (KIND == 0 && a.bias) ? __ldg(reinterpret_cast<const float4*>(a.bias + c)) : splat(0.f, float4{});
+#pragma unroll
+  for (int y = 0; y < TH; ++y) {
+    const int p = p0 + y;
+    if (p >= a.P) break;
+#pragma unroll
+    for (int x = 0; x < PX; ++x) {
+      const int q = q0 + x;
+      if (q >= a.Q) break;
+      float4 v = acc[y][x];
+      if (KIND == 0) {
+        add_to(v, bias);
+      } else if (avg) {
+        const int ihs = p * a.sh - a.ph, iws = q * a.sw - a.pw;
+        int div;
+        if (a.count_pad) {  // torch: window clipped to [-pad, H + pad_bottom)
+          const int he = min(ihs + KS, a.H + a.pad_b), we = min(iws + KS, a.W + a.pad_r);
+          div = (he - ihs) * (we - iws);
+        } else {
+          const int hl = max(ihs, 0), hh = min(ihs + KS, a.H), wl = max(iws, 0), wh = min(iws + KS, a.W);
+          div = max(hh - hl, 0) * max(wh - wl, 0);
+        }
+        scale(v, div > 0 ? 1.f / (float)div : 0.f);
+        if (a.mul != 1.f) scale(v, a.mul);
+      } else if (a.mul != 1.f) {
+        scale(v, a.mul);
+      }
+      if (a.has_res) add_to(v, __ldg(reinterpret_cast<const float4*>(a.res + n * a.res_sn + p * a.res_sh + q * a.res_sw + c)));
+      *reinterpret_cast<float4*>(a.out + n * a.out_sn + p * a.out_sh + q * a.out_sw + c) = actv(v, a.act);
+    }
+  }
+}
+
+template <int KIND>
+static int launch_rows(const sw_op_desc& op, void* stream) {
+  SpatialArgs a = spatial_args(op);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!can_vec4(a, op, KIND == 0) || a.R != a.S || a.sh != a.sw) return (int)cudaErrorInvalidValue;
+  const int ks = a.R, s = a.sh;
+  // blocks sized to stay within 128 registers (2 CTAs x 256 threads per SM)
+  const int TH = (s == 2 && ks == 7) ? 1 : 2;
+  const int PX = (s == 1 && ks <= 5) ? 4 : 2;
+  const int bands = (a.P + TH - 1) / TH, cols = (a.Q + PX - 1) / PX;
+  const int64_t total = (int64_t)a.N * bands * cols * (a.C / 4);
+  if (total == 0) return 0;
+  if (total >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;
+  const int blocks = (int)cdiv(total, 256);
+#define SW_ROWS(K_, S_, TH_, PX_)                                                                                \
+  if (ks == K_ && s == S_)                                                                                      \
+    return (int)launch_k(spatial_rows_kernel<KIND, K_, S_, TH_, PX_>, dim3(blocks), dim3(256), 0, st, 1, a, total, \
+                         bands, cols);
+  SW_ROWS(3, 1, 2, 4) SW_ROWS(5, 1, 2, 4) SW_ROWS(7, 1, 2, 2)
+  SW_ROWS(3, 2, 2, 2) SW_ROWS(5, 2, 2, 2) SW_ROWS(7, 2, 1, 2)
+#undef SW_ROWS
+  return (int)cudaErrorInvalidValue;
+}
+
+int launch_dwconv(const sw_op_desc& op, void* stream) {
+  return op.variant == 1 ? launch_rows<0>(op, stream) : launch_spatial<0>(op, stream);
+}
+int launch_pool(const sw_op_desc& op, void* stream) {
+  return op.variant == 1 ? launch_rows<1>(op, stream) : launch_spatial<1>(op, stream);
+}
 
 }  // namespace sw

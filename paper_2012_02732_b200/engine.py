@@ -788,6 +788,8 @@ class Engine:
             return (K_CONV, v, split)
         if t.kind == "sepconv":
             return (K_SEPCONV, 0, 1)
+        if t.kind in ("dwconv", "pool"):
+            return (d.kind, 0, 1)
         return None
 
     def _autotune(self, reps: int = 5, rtol: float = 1e-4):
@@ -803,7 +805,7 @@ class Engine:
         self.arena[: 4 * words].view(torch.float32).normal_(generator=gen)
         self.tuning_rejected = {}
         for t in self.program.tasks:
-            if t.kind not in ("conv", "sepconv", "sep2"):
+            if t.kind not in ("conv", "sepconv", "sep2", "dwconv", "pool"):
                 continue
             d = self.ops[t.tid]
             p = d.params
@@ -812,7 +814,11 @@ class Engine:
             Kdim = p[SP_R] * p[SP_S] * p[SP_C]
             trial = N.OpDesc()
             C.memmove(C.byref(trial), C.byref(d), C.sizeof(N.OpDesc))
-            if t.kind == "sep2":
+            if t.kind in ("dwconv", "pool"):
+                # per-output taps (variant 0) vs register-blocked rows (1); the
+                # rows kernel refuses layouts it cannot vectorise
+                cands = [(d.kind, 0, 1), (d.kind, 1, 1)]
+            elif t.kind == "sep2":
                 P = p[SP_P]
                 cands = sorted({(K_SEP2, 0, sep2_cluster(P, r)) for r in (1, 2, 3, 4, 7) if r <= P})
             elif t.kind == "sepconv":

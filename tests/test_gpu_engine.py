@@ -653,6 +653,62 @@ def test_pools_and_concat(c, h):
     close(y, ref)
 
 
+class RowsCase(nn.Module):
+    """Depthwise 3/5/7 (stride 1 and 2) and max / avg pools (count_include_pad
+    both ways, stride 1 and 2) on NHWC activations, results concatenated
+    (channel-slice stores) plus a residual add into one pool."""
+
+    def __init__(self, c):
+        super().__init__()
+        self.lead = nn.Conv2d(c, c, 1, bias=False)
+        self.d3 = nn.Conv2d(c, c, 3, 1, 1, groups=c, bias=True)
+        self.d5 = nn.Conv2d(c, c, 5, 1, 2, groups=c, bias=False)
+        self.d7 = nn.Conv2d(c, c, 7, 1, 3, groups=c, bias=False)
+        self.d5s = nn.Conv2d(c, c, 5, 2, 2, groups=c, bias=False)
+        self.d7s = nn.Conv2d(c, c, 7, 2, 3, groups=c, bias=False)
+        self.d3s = nn.Conv2d(c, c, 3, 2, 1, groups=c, bias=False)
+        self.mp = nn.MaxPool2d(3, 1, 1)
+        self.ap = nn.AvgPool2d(3, 1, 1, count_include_pad=False)
+        self.ap2 = nn.AvgPool2d(3, 1, 1, count_include_pad=True)
+        self.mps = nn.MaxPool2d(3, 2, 1)
+        self.aps = nn.AvgPool2d(3, 2, 1, count_include_pad=False)
+        self.tail_f = nn.Conv2d(6 * c, 8, 1, stride=2, bias=False)  # the maps stay NHWC activations
+        self.tail_h = nn.Conv2d(5 * c, 8, 1, bias=False)
+
+    def forward(self, x):
+        h = torch.relu(self.lead(x))
+        full = torch.cat([self.d3(h), self.d5(h), self.d7(h), self.mp(h), self.ap(h) + h, self.ap2(h)], 1)
+        half = torch.cat([self.d5s(h), self.d7s(h), self.d3s(h), self.mps(h), self.aps(h)], 1)
+        return torch.cat([self.tail_f(full), self.tail_h(half)], 1)
+
+
+@pytest.mark.parametrize("h,batch", [(28, 3), (23, 2), (14, 5)])
+def test_spatial_rows_variant(h, batch):
+    """Register-blocked rows variant (variant 1) of the depthwise / pool
+    kernels (spatial.cu spatial_rows_kernel), forced on every such task."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_DWCONV, K_POOL, SLOT_MULTI
+    torch.manual_seed(9)
+    m = RowsCase(24).eval()
+    x = torch.randn(batch, 24, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    n = 0
+    for d in eng.ops[:len(eng.program.tasks)]:
+        if d.kind in (K_DWCONV, K_POOL):
+            d.variant = 1
+            n += 1
+    assert n >= 11
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 class Shifted(nn.Module):
     def __init__(self, c):
         super().__init__()
