@@ -102,7 +102,7 @@ struct PwArgs {
   float* __restrict__ out;
   const float* __restrict__ bias;
   const float* __restrict__ res;
-  int M, K, P, Q, act, pre_relu, has_res, kblocks;
+  int M, K, P, Q, act, pre_relu, has_res, kblocks, ovec;  // ovec: float4 output / residual rows
   int64_t out_sn, out_sh, out_sw, res_sn, res_sh, res_sw;
 };
 
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
         }
         pw_wait_ld();
         if (!ok || nv <= 0) continue;
-        if (nv == 16) {
+        if (a.ovec && nv == 16) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {
             float4 x = make_float4(v[j] + w[j], v[j + 1] + w[j + 1], v[j + 2] + w[j + 2], v[j + 3] + w[j + 3]);
@@ -339,10 +339,12 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   if (p[SP_R] != 1 || p[SP_S] != 1 || p[SP_STRIDE_H] != 1 || p[SP_STRIDE_W] != 1 || p[SP_PAD_H] || p[SP_PAD_W] ||
       in_sc != 1 || C % 4 || (in_sw & 3) || (op.ptrs[PT_IN] & 15) || in_sn != (int64_t)H * W * in_sw ||
       in_sh != (int64_t)W * in_sw || osc != 1 || (a.has_res && rsc != 1) || !whi || !wlo ||
-      (!WSPLIT && Kpad % PW_BK) ||
-      (op.ptrs[PT_OUT] & 15) || (a.out_sw & 3) || (a.out_sh & 3) || (a.out_sn & 3))
+      (!WSPLIT && Kpad % PW_BK))
     return (int)cudaErrorInvalidValue;
-  if (a.has_res && ((op.ptrs[PT_RES] & 15) || (a.res_sw & 3))) return (int)cudaErrorInvalidValue;
+  // float4 epilogue rows when output (and residual) rows are 16-B aligned
+  // (e.g. not for an 11-channel NHWC map: scalar stores)
+  a.ovec = !((op.ptrs[PT_OUT] & 15) || (a.out_sw & 3) || (a.out_sh & 3) || (a.out_sn & 3) ||
+             (a.has_res && ((op.ptrs[PT_RES] & 15) || (a.res_sw & 3) || (a.res_sh & 3) || (a.res_sn & 3))));
   a.kblocks = WSPLIT ? (C + PW_BK - 1) / PW_BK : Kpad / PW_BK;
   CUtensorMap ta, tbh, tbl;
   {

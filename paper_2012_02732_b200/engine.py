@@ -196,7 +196,8 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
         # large-batch pointwise: persistent warp-specialised tcgen05 GEMM
         # (conv_pw_tc.cu), BN output channels per N tile
         for bn in PWTC_TILES:
-            if bn > 2 * max(K, 16) or (bn < K and math.ceil(K / bn) * bn - K >= bn // 2 and bn != 128):
+            if (bn > 2 * max(K, 16) and bn != 48) or \
+                    (bn < K and math.ceil(K / bn) * bn - K >= bn // 2 and bn != 128):
                 continue
             out.append((K_CONV_TC, 8000 + bn, 1))  # prepare-time 3xTF32 weight copies
             out.append((K_CONV_TC, 8100 + bn, 1))  # fp32 weights split in the kernel

@@ -133,7 +133,8 @@ def test_tcgen05_tma_persistent(bn, cin, cout, hw, batch, pre):
 @pytest.mark.parametrize("bn", [48, 64, 96, 128, 148, 164, 196, 228])
 @pytest.mark.parametrize("cin,cout,hw,batch,pre,res", [(264, 44, 28, 8, True, False), (528, 176, 14, 20, False, True),
                                                        (64, 200, 17, 20, True, True), (1056, 88, 7, 90, False, False),
-                                                       (44, 48, 9, 60, False, False)])
+                                                       (44, 48, 9, 60, False, False), (32, 11, 37, 5, True, False),
+                                                       (44, 22, 28, 6, False, True)])
 def test_tcgen05_pointwise_persistent_ws(bn, cin, cout, hw, batch, pre, res):
     """Large-batch pointwise conv on the persistent warp-specialised tcgen05
     kernel (variants 8000 + BN with prepare-time 3xTF32 weights, 8100 + BN
