@@ -63,6 +63,7 @@ struct TcsArgs {
   int64_t out_sn, out_sh, out_sw, out_sc;
   int64_t res_sn, res_sh, res_sw, res_sc;
   int M, Kdim, Kpad, split;
+  int ovec;  // output (and residual) pixel rows 16-B aligned with unit channel stride
 };
 
 // Out channels per tile = UMMA M = 128.  (A 64-channel tile with the MMA's
@@ -227,6 +228,14 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
   tc_fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
+  // folded-BN bias of this thread's 4 epilogue channels: constants, fetched
+  // now so their (cold) loads are not on the epilogue's critical path
+  float bias[4] = {0.f, 0.f, 0.f, 0.f};
+  if (warp < 4 && a.bias) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (n0 + 4 * lane + i < a.K) bias[i] = __ldg(a.bias + n0 + 4 * lane + i);
+  }
 
   if (warp == 4) {
     // ---- weight producer: the whole K slice streams through a W-deep ring,
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
       cp_wait_g<L::RB - 1>();  // raw K block t landed (this thread's part)
       named_bar(1, 128);
       if (t == 0) probe_pt(3);
-      if (tid == 0 && t < 16) probe_trace(48 + t);  // raw K block t landed
+      if (tid == 0 && t < 8) probe_trace(48 + t);  // raw K block t landed
       // the split slot is free once the MMAs of K block t - SB completed
       if (t >= SB) mbar_wait_parity(su32(&bfree[sb]), (uint32_t)(((t / SB) - 1) & 1));
       const uint8_t* rawb = smem + L::RAW_OFF + rb * L::B_BYTES;
@@ -427,7 +436,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
     // every rank's ring is dead (its last MMA completed) before anyone writes into it
     cluster_arrive_relaxed();
     cluster_wait();
-    if (tid == 0) probe_trace(60);  // every rank's ring is dead
+    if (tid == 0) probe_trace(56);  // every rank's ring is dead
     if (tid == 0) {
       mbar_expect_tx(su32(recv), (uint32_t)((a.split - 1) * R * L::ROW));
 #pragma unroll 1
@@ -440,48 +449,61 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
       bulk_commit();
     }
     if (warp < 4) mbar_wait_parity(su32(recv), 0);
-    if (tid == 0) probe_trace(61);  // peers' rows in
+    if (tid == 0) probe_trace(57);  // peers' rows in
+    // once every rank has received its rows every push has read its source:
+    // the exit waits on this barrier instead of on the bulk-copy groups
+    __syncwarp();
+    cluster_arrive_relaxed();
   }
   if (warp < 4) {
-    // thread = output channel; its rows are independent, so the loop is
-    // unrolled for ILP and the (image, row, column) of consecutive pixels is
-    // advanced incrementally (a single warp per sub-partition runs this
-    // tail: the per-row divisions and dependent smem / store chain of a
-    // rolled loop cost ~0.35 us per pixel row, probe r02ze)
-    const int cl = tid & (TCS_BM - 1);
-    const int n = n0 + cl;
-    const float bias = (a.bias && n < a.K) ? a.bias[n] : 0.f;
-    constexpr int STEP = 128 / TCS_BM;
-    const int j0 = tid / TCS_BM;
+    // thread = 4 consecutive output channels (lane) x every 4th pixel row
+    // (warp): float4 smem reads, bias, residual and NHWC stores, so a row
+    // costs a quarter of the instructions of a channel-per-thread loop (that
+    // loop ran ~0.25 us per pixel row, serially, probe r03f)
+    const int c4 = 4 * lane;
+    const int n = n0 + c4;
     const int rows = min(R, a.M - (m0 + me * R));
     int qq = 0, pp = 0, nb = 0;
     {
-      const int m = m0 + me * R + j0;
+      const int m = m0 + me * R + warp;
       qq = m % a.Q;
       const int tt = m / a.Q;
       pp = tt % a.P;
       nb = tt / a.P;
     }
-    if (tid == 0) probe_trace(62);
-#pragma unroll 4
-    for (int j = j0; j < rows; j += STEP) {
+    if (tid == 0) probe_trace(58);
+#pragma unroll 2
+    for (int j = warp; j < rows; j += 4) {
       const int p = me * R + j;
-      float v = part[p * TCS_BM + cl];
+      float4 v = *reinterpret_cast<const float4*>(part + p * TCS_BM + c4);
       if (a.split > 1) {
-        float t[15];
+        float4 t[15];
 #pragma unroll
         for (int r = 0; r < 15; ++r)
-          if (r < a.split - 1) t[r] = rcv[(r * R + j) * TCS_BM + cl];
+          if (r < a.split - 1) t[r] = *reinterpret_cast<const float4*>(rcv + (r * R + j) * TCS_BM + c4);
 #pragma unroll
         for (int r = 0; r < 15; ++r)
-          if (r < a.split - 1) v += t[r];
+          if (r < a.split - 1) v = f4add(v, t[r]);
       }
-      if (n < a.K) {
-        v += bias;
-        if (a.has_res) v += a.res[nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + n * a.res_sc];
-        a.out[nb * a.out_sn + pp * a.out_sh + qq * a.out_sw + n * a.out_sc] = apply_act(v, a.act);
+      v = f4add(v, make_float4(bias[0], bias[1], bias[2], bias[3]));
+      if (a.ovec && n + 3 < a.K) {
+        if (a.has_res)
+          v = f4add(v, *reinterpret_cast<const float4*>(a.res + nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + n));
+        *reinterpret_cast<float4*>(a.out + nb * a.out_sn + pp * a.out_sh + qq * a.out_sw + n) = act4(v, a.act);
+      } else {
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (n + i >= a.K) break;
+          float x = vv[i];
+          if (a.has_res) x += a.res[nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + (n + i) * a.res_sc];
+          a.out[nb * a.out_sn + pp * a.out_sh + qq * a.out_sw + (n + i) * a.out_sc] = apply_act(x, a.act);
+        }
       }
-      qq += STEP;
+#ifdef SW_PROBE
+      if (tid == 32 && j < 56) probe_trace(9 + j / 4);  // row j stored (warp 1)
+#endif
+      qq += 4;
       while (qq >= a.Q) {
         qq -= a.Q;
         if (++pp == a.P) {
@@ -491,10 +513,13 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
       }
     }
     probe_pt(6);
+    if (lane == 0) probe_trace(60 + warp);  // warp's stores issued
   }
-  if (a.split > 1 && tid == 0) bulk_wait_read0();  // my outgoing copies have read `part`
+  if (a.split > 1) cluster_wait();  // every push completed: `part` may be released
+  probe_pt(7);
   tc_fence_before_sync();
   __syncthreads();
+  probe_pt(8);
   if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)L::COLS)
                  : "memory");
@@ -526,6 +551,8 @@ static int launch_tcs(const sw_op_desc& op, cudaStream_t st) {
   a.Kpad = (int)p[SP_KPAD];
   a.split = p[SP_SPLIT_K] > 1 ? (int)p[SP_SPLIT_K] : 1;
   if (a.M == 0 || a.K == 0) return 0;
+  a.ovec = a.out_sc == 1 && !(op.ptrs[PT_OUT] & 15) && !((a.out_sn | a.out_sh | a.out_sw) & 3) &&
+           (!a.has_res || (a.res_sc == 1 && !(op.ptrs[PT_RES] & 15) && !((a.res_sn | a.res_sh | a.res_sw) & 3)));
   a.wimg = reinterpret_cast<const float*>(op.ptrs[PT_WS]);
   // 16-B im2col chunks: 4 consecutive channels of one tap, 16-B aligned rows
   const bool vec = a.C % 4 == 0 && p[SP_IN_SC] == 1 && a.in_sn % 4 == 0 && a.in_sh % 4 == 0 &&
