@@ -774,6 +774,7 @@ static cudaError_t launch_sep_tma_ks(int v, const SepArgs& a, const sw_op_desc& 
 
 int launch_sepconv(const sw_op_desc& op, void* stream) {
   if (op.variant == SEP_TC_VARIANT) return launch_sepconv_tc(op, stream);  // sepconv_tc.cu
+  if (op.variant >= 20 && op.variant < 30) return launch_sep_rows(op, stream);  // sep_rows.cu
   SepArgs a = sep_args(op);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (a.M == 0 || a.K == 0) return 0;

@@ -292,6 +292,7 @@ int sw_engine_create(int32_t device, sw_engine** out) {
   sw::init_pw_kernels();
   sw::init_sep_kernels();
   sw::init_sep_tc_kernels();
+  sw::init_sep_rows_kernels();
   sw::init_sep2_kernels();
   CU(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   CU(cudaEventCreate(&e->t0));

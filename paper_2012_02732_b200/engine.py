@@ -94,6 +94,9 @@ SEP_TILES = {0: (16, 32), 1: (8, 64), 2: (16, 64), 3: (32, 32), 4: (8, 32), 5: (
 SEP_TC_VARIANT = 100  # csrc/kernels/sepconv_tc.cu: persistent depthwise + tcgen05 pointwise
 SEP_TMA_FIRST = 6
 SEP_ROW_FIRST = 11
+# csrc/kernels/sep_rows.cu: whole output rows per CTA, input rows staged once
+# in shared memory (C, K <= 64): variant → (rows per CTA, pixels per thread)
+SEP_ROWS_VARIANTS = {20: (2, 4), 21: (4, 4), 22: (8, 4), 23: (4, 2)}
 
 # csrc/kernels/conv1x1.cu: TMA-staged pointwise conv, conv variant → (BM, BN)
 PW_TILES = {16: (8, 32), 17: (16, 32), 18: (32, 32), 19: (16, 64), 20: (32, 64), 21: (64, 32)}
@@ -824,6 +827,8 @@ class Engine:
                 cands = sorted({(K_SEP2, 0, sep2_cluster(P, r)) for r in (1, 2, 3, 4, 7) if r <= P})
             elif t.kind == "sepconv":
                 cands = [(K_SEPCONV, v, 1) for v in SEP_TILES]
+                if p[SP_C] <= 64 and K <= 64:
+                    cands += [(K_SEPCONV, v, 1) for v in SEP_ROWS_VARIANTS]  # row-staged (thin maps)
                 if p[SP_C] % 4 == 0:
                     cands.append((K_SEPCONV, SEP_TC_VARIANT, 1))  # depthwise + tcgen05 pointwise
                 # TMA kernel with the depthwise split over a cluster of the column blocks
@@ -896,6 +901,8 @@ class Engine:
             return cd(M / 128) * cd(K / (variant % 1000)) * max(1, split)
         if kind == K_SEPCONV and variant == SEP_TC_VARIANT:
             return min(cd(M / 128), NUM_SMS)
+        if kind == K_SEPCONV and variant in SEP_ROWS_VARIANTS:
+            return p[SP_N] * cd(p[SP_P] / SEP_ROWS_VARIANTS[variant][0])
         if kind == K_SEPCONV:
             bm, bn = SEP_TILES[variant]
             if SEP_TMA_FIRST <= variant < SEP_ROW_FIRST:

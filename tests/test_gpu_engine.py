@@ -447,6 +447,56 @@ def test_sepconv_row_blocked_variants(variant, c, k, s, h, batch):
     eng.close()
 
 
+class SepBN(nn.Module):
+    """ReLU → depthwise k x k → pointwise cin→cout → BN (+ a second branch
+    added, which the DAG builder fuses as the sepconv's residual)."""
+
+    def __init__(self, cin, cout, k, s, res):
+        super().__init__()
+        self.dw = nn.Conv2d(cin, cin, k, s, k // 2, groups=cin, bias=False)
+        self.pw = nn.Conv2d(cin, cout, 1, bias=False)
+        self.bn = nn.BatchNorm2d(cout)
+        self.res = nn.Conv2d(cin, cout, 1, s, 0, bias=False) if res else None
+
+    def forward(self, x):
+        y = self.bn(self.pw(self.dw(torch.relu(x))))
+        return y + self.res(x) if self.res is not None else y
+
+
+@pytest.mark.parametrize("variant", [20, 21, 22, 23])
+@pytest.mark.parametrize("cin,cout,k,s,h,batch,lead,res", [
+    (32, 11, 7, 2, 111, 2, True, False),   # NASNet stem sep1: 32 → 11 channels, 7x7 s2 on 111x111
+    (11, 11, 5, 1, 56, 2, True, False),    # 44-byte pixels (scalar staging), 5x5 s1
+    (22, 22, 7, 2, 56, 3, True, True),     # stem-1 shape + fused residual
+    (11, 13, 3, 2, 23, 2, False, False),   # NCHW network input read through strides, ragged tiles
+    (64, 48, 3, 1, 9, 3, True, True),      # widest channels the variant takes (chunked staging)
+])
+def test_sepconv_row_staged_variants(variant, cin, cout, k, s, h, batch, lead, res):
+    """sep_rows.cu (variants 20..23) forced: staged rows, swizzled windows,
+    channel chunks, padding, residual, odd channel counts."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_SEPCONV, SLOT_MULTI
+    from paper_2012_02732_b200.networks import randomize_bn
+    torch.manual_seed(6)
+    body = SepBN(cin, cout, k, s, res)
+    m = (nn.Sequential(nn.Conv2d(cin, cin, 1, bias=False), body) if lead else body).eval()
+    randomize_bn(m)
+    x = torch.randn(batch, cin, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    idx = [i for i in range(len(eng.program.tasks)) if eng.ops[i].kind == K_SEPCONV]
+    assert len(idx) == 1
+    eng.ops[idx[0]].variant = variant
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 @pytest.mark.parametrize("variant", range(6))
 @pytest.mark.parametrize("c,k,s,h", [(44, 5, 1, 14), (11, 7, 2, 23), (176, 3, 1, 7)])
 def test_sepconv_tile_variants(variant, c, k, s, h):
