@@ -25,6 +25,8 @@
 //      registers, the weight rows broadcast from shared memory): bias,
 //      residual, act, NHWC stores.
 // Variants 20..23 (TH, PX) = (2, 8), (4, 8), (8, 8), (4, 4).
+#include <algorithm>
+
 #include "common.cuh"
 #include "tma.cuh"
 
@@ -354,6 +356,201 @@ int launch_sep_rows(const sw_op_desc& op, void* stream) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row-staged k x k pooling (K_POOL variant 2) for thin wide maps: the same
+// staging as above (input rows once per CTA, a channel-per-thread window
+// sliding along the staged row), out-of-range taps staged as -inf (max) or 0
+// (avg, divisor from the valid-tap count or torch's count_include_pad clamp).
+// The 11 / 22-channel NASNet stem pools ran at 0.9-1.5 TB/s per-pixel (r03l).
+namespace {
+struct PoolRowsArgs {
+  const float* __restrict__ in;
+  float* __restrict__ out;
+  const float* __restrict__ res;
+  int N, H, W, C, P, Q, sh, sw, ph, pw, act, pre_relu, has_res, mode, count_pad, pad_b, pad_r;
+  float mul;
+  int64_t in_sn, in_sh, in_sw, in_sc;
+  int64_t out_sn, out_sh, out_sw, out_sc;
+  int64_t res_sn, res_sh, res_sw, res_sc;
+  int TH, CC, nch, IR, WP, RL, padG, QG;
+};
+}  // namespace
+
+template <int KS, int SW, int PX>
+__global__ void __launch_bounds__(SR_THREADS) pool_rows_kernel(PoolRowsArgs a) {
+  constexpr int NW = (PX - 1) * SW + KS;
+  constexpr int PS = PX * SW;
+  extern __shared__ __align__(16) float smem[];
+  float* X = smem;  // [buf][IR][RL]
+  const int tid = threadIdx.x;
+  const int tiles = (a.P + a.TH - 1) / a.TH;
+  const int nb = blockIdx.x / tiles;
+  const int p0 = (blockIdx.x - nb * tiles) * a.TH;
+  pdl_trigger();
+  pdl_wait();
+  const float* inb = a.in + nb * a.in_sn;
+  const int CC = a.CC, RL = a.RL, padG = a.padG;
+  const int bufsz = a.IR * RL;
+  const float fill = a.mode == 0 ? __int_as_float(0xff800000) : 0.f;  // max: -inf, avg: 0 (not counted)
+  auto stage = [&](int ch, int buf) {
+    const int c0 = ch * CC;
+    float* Xb = X + buf * bufsz;
+    const int diw = SR_THREADS / CC, dcc = SR_THREADS % CC;
+#pragma unroll 1
+    for (int ir = 0; ir < a.IR; ++ir) {
+      const int ih = p0 * a.sh - a.ph + ir;
+      const bool rok = (unsigned)ih < (unsigned)a.H;
+      const float* srow = inb + (rok ? ih * a.in_sh : 0);
+      float* drow = Xb + ir * RL;
+      int iw = tid / CC, cc = tid - (tid / CC) * CC;
+#pragma unroll 4
+      for (int f = tid; f < a.WP * CC; f += SR_THREADS) {
+        const int iwg = iw - a.pw;
+        const bool ok = rok && (unsigned)iwg < (unsigned)a.W;
+        float* dst = drow + iw * CC + cc + (iw / PS) * padG;
+        if (ok)
+          cp_async4(dst, srow + iwg * a.in_sw + (int64_t)(c0 + cc) * a.in_sc, true);
+        else
+          *dst = fill;
+        cc += dcc;
+        iw += diw;
+        if (cc >= CC) {
+          cc -= CC;
+          ++iw;
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  const int cl = tid % CC;
+  const int slot = tid / CC;
+  const int nslots = SR_THREADS / CC;
+  const float lo = a.pre_relu ? 0.f : __int_as_float(0xff800000);
+  stage(0, 0);
+#pragma unroll 1
+  for (int ch = 0; ch < a.nch; ++ch) {
+    const int c = ch * CC + cl;
+    if (ch + 1 < a.nch) {
+      stage(ch + 1, (ch + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (slot < nslots) {
+      const float* Xc = X + (ch & 1) * bufsz + cl;
+#pragma unroll 1
+      for (int it = slot; it < a.TH * a.QG; it += nslots) {
+        const int qg = it % a.QG;
+        const int tr = it / a.QG;
+        const int p = p0 + tr;
+        if (p >= a.P) continue;
+        float acc[PX];
+#pragma unroll
+        for (int j = 0; j < PX; ++j) acc[j] = a.mode == 0 ? __int_as_float(0xff800000) : 0.f;
+        const float* xb = Xc + tr * a.sh * RL + qg * (PS * CC + padG);
+#pragma unroll
+        for (int r = 0; r < KS; ++r) {
+          float x[NW];
+#pragma unroll
+          for (int j = 0; j < NW; ++j) x[j] = xb[r * RL + j * CC + (j / PS) * padG];
+          // ReLU before pooling (staged -inf / 0 fills are unchanged by it
+          // where they matter: max ignores -inf, avg adds 0)
+          if (a.pre_relu) {
+#pragma unroll
+            for (int j = 0; j < NW; ++j) x[j] = fmaxf(x[j], a.mode == 0 ? lo : 0.f);
+          }
+#pragma unroll
+          for (int s2 = 0; s2 < KS; ++s2)
+#pragma unroll
+            for (int j = 0; j < PX; ++j)
+              acc[j] = a.mode == 0 ? fmaxf(acc[j], x[j * SW + s2]) : acc[j] + x[j * SW + s2];
+        }
+        const int ih0 = p * a.sh - a.ph;
+        const int vr = min(ih0 + KS, a.H) - max(ih0, 0);
+        const int hr = min(ih0 + KS, a.H + a.pad_b) - ih0;
+        float* op = a.out + nb * a.out_sn + p * a.out_sh + c * a.out_sc;
+        const float* rp = a.has_res ? a.res + nb * a.res_sn + p * a.res_sh + c * a.res_sc : nullptr;
+#pragma unroll
+        for (int j = 0; j < PX; ++j) {
+          const int q = qg * PX + j;
+          if (q >= a.Q) break;
+          float v = acc[j];
+          if (a.mode == 1) {
+            const int iw0 = q * a.sw - a.pw;
+            const int div = a.count_pad ? hr * (min(iw0 + KS, a.W + a.pad_r) - iw0)
+                                        : vr * (min(iw0 + KS, a.W) - max(iw0, 0));
+            v *= div > 0 ? 1.f / (float)div : 0.f;
+          }
+          v *= a.mul;
+          if (rp) v += rp[q * a.res_sw];
+          op[q * a.out_sw] = apply_act(v, a.act);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int KS, int SW>
+static int launch_pr_ksw(const PoolRowsArgs& a, int px, size_t smem, cudaStream_t st) {
+  const dim3 grid((unsigned)(a.N * ((a.P + a.TH - 1) / a.TH)));
+  if (px == 4) return (int)launch_k(pool_rows_kernel<KS, SW, 4>, grid, dim3(SR_THREADS), smem, st, 1, a);
+  return (int)launch_k(pool_rows_kernel<KS, SW, 8>, grid, dim3(SR_THREADS), smem, st, 1, a);
+}
+
+int launch_pool_rows(const sw_op_desc& op, void* stream) {
+  const int64_t* p = op.params;
+  PoolRowsArgs a;
+  a.in = reinterpret_cast<const float*>(op.ptrs[PT_IN]);
+  a.out = reinterpret_cast<float*>(op.ptrs[PT_OUT]);
+  a.res = reinterpret_cast<const float*>(op.ptrs[PT_RES]);
+  a.N = (int)p[SP_N]; a.H = (int)p[SP_H]; a.W = (int)p[SP_W]; a.C = (int)p[SP_C];
+  a.P = (int)p[SP_P]; a.Q = (int)p[SP_Q];
+  a.sh = (int)p[SP_STRIDE_H]; a.sw = (int)p[SP_STRIDE_W];
+  a.ph = (int)p[SP_PAD_H]; a.pw = (int)p[SP_PAD_W];
+  a.act = (int)p[SP_ACT]; a.pre_relu = (int)p[SP_PRE_RELU]; a.has_res = (int)p[SP_HAS_RES];
+  a.mode = (int)p[SP_POOL_MODE]; a.count_pad = (int)p[SP_COUNT_PAD];
+  a.pad_b = (int)p[SP_PAD_BOTTOM]; a.pad_r = (int)p[SP_PAD_RIGHT];
+  a.mul = p[SP_POOL_MUL] > 0 ? (float)p[SP_POOL_MUL] : 1.f;
+  a.in_sn = p[SP_IN_SN]; a.in_sh = p[SP_IN_SH]; a.in_sw = p[SP_IN_SW]; a.in_sc = p[SP_IN_SC] ? p[SP_IN_SC] : 1;
+  a.out_sn = p[SP_OUT_SN]; a.out_sh = p[SP_OUT_SH]; a.out_sw = p[SP_OUT_SW];
+  a.out_sc = p[SP_OUT_SC] ? p[SP_OUT_SC] : 1;
+  a.res_sn = p[SP_RES_SN]; a.res_sh = p[SP_RES_SH]; a.res_sw = p[SP_RES_SW];
+  a.res_sc = p[SP_RES_SC] ? p[SP_RES_SC] : 1;
+  if ((int64_t)a.N * a.P * a.Q * a.C == 0) return 0;
+  const int ks = (int)p[SP_R];
+  if (p[SP_R] != p[SP_S] || (ks != 3 && ks != 5 && ks != 7) || a.sh != a.sw || (a.sw != 1 && a.sw != 2) ||
+      a.C > 256 || (a.mode != 0 && a.mode != 1) || a.ph < 0 || a.pw < 0)
+    return (int)cudaErrorInvalidValue;
+  const int th = 4, px = a.sw == 1 ? 8 : 4;
+  a.TH = th;
+  a.QG = (a.Q + px - 1) / px;
+  a.IR = (th - 1) * a.sh + ks;
+  a.WP = (a.QG * px - 1) * a.sw + ks;
+  const int ps = px * a.sw;
+  size_t smem = 0;
+  bool fit = false;
+  for (int cc = std::min(a.C, 64); cc >= 1; --cc) {
+    if (a.C % cc) continue;
+    const int pad = ((cc - ps * cc) % 32 + 32) % 32;
+    const int rl = (a.WP * cc + ((a.WP - 1) / ps) * pad + 4) / 4 * 4;
+    const int bufs = cc == a.C ? 1 : 2;
+    const size_t bytes = 4 * (size_t)bufs * a.IR * rl;
+    if (bytes <= (size_t)kSrSmemMax) {
+      a.CC = cc; a.nch = a.C / cc; a.padG = pad; a.RL = rl; smem = bytes; fit = true;
+      break;
+    }
+  }
+  if (!fit) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (ks) {
+    case 3: return a.sw == 1 ? launch_pr_ksw<3, 1>(a, 8, smem, st) : launch_pr_ksw<3, 2>(a, 4, smem, st);
+    case 5: return a.sw == 1 ? launch_pr_ksw<5, 1>(a, 8, smem, st) : launch_pr_ksw<5, 2>(a, 4, smem, st);
+    default: return a.sw == 1 ? launch_pr_ksw<7, 1>(a, 8, smem, st) : launch_pr_ksw<7, 2>(a, 4, smem, st);
+  }
+}
+
 template <int KS, int SW>
 static void init_sr_ksw() {
   cudaFuncSetAttribute(sep_rows_kernel<KS, SW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSrSmemMax);
@@ -361,6 +558,12 @@ static void init_sr_ksw() {
 }
 
 void init_sep_rows_kernels() {
+  cudaFuncSetAttribute(pool_rows_kernel<3, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSrSmemMax);
+  cudaFuncSetAttribute(pool_rows_kernel<3, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSrSmemMax);
+  cudaFuncSetAttribute(pool_rows_kernel<5, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSrSmemMax);
+  cudaFuncSetAttribute(pool_rows_kernel<5, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSrSmemMax);
+  cudaFuncSetAttribute(pool_rows_kernel<7, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSrSmemMax);
+  cudaFuncSetAttribute(pool_rows_kernel<7, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSrSmemMax);
   init_sr_ksw<3, 1>(); init_sr_ksw<3, 2>();
   init_sr_ksw<5, 1>(); init_sr_ksw<5, 2>();
   init_sr_ksw<7, 1>(); init_sr_ksw<7, 2>();

@@ -353,6 +353,7 @@ int launch_dwconv(const sw_op_desc& op, void* stream) {
   return op.variant == 1 ? launch_rows<0>(op, stream) : launch_spatial<0>(op, stream);
 }
 int launch_pool(const sw_op_desc& op, void* stream) {
+  if (op.variant == 2) return launch_pool_rows(op, stream);  // sep_rows.cu: row-staged, thin wide maps
   return op.variant == 1 ? launch_rows<1>(op, stream) : launch_spatial<1>(op, stream);
 }
 

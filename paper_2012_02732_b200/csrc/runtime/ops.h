@@ -208,6 +208,7 @@ constexpr int SEP_TC_VARIANT = 100;
 int launch_sepconv_tc(const sw_op_desc& op, void* stream);
 // sep_rows.cu: row-staged fused sepconv for thin wide maps (variants 20..23)
 int launch_sep_rows(const sw_op_desc& op, void* stream);
+int launch_pool_rows(const sw_op_desc& op, void* stream);  // K_POOL variant 2
 void init_sep_rows_kernels();
 void init_sep_tc_kernels();
 int launch_train(const sw_op_desc& op, void* stream);  // K_BN_* .. K_SGD, K_EW_BWD

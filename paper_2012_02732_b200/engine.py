@@ -822,6 +822,8 @@ class Engine:
                 # per-output taps (variant 0) vs register-blocked rows (1); the
                 # rows kernel refuses layouts it cannot vectorise
                 cands = [(d.kind, 0, 1), (d.kind, 1, 1)]
+                if t.kind == "pool" and p[SP_C] <= 256:
+                    cands.append((d.kind, 2, 1))  # row-staged (sep_rows.cu), thin wide maps
             elif t.kind == "sep2":
                 P = p[SP_P]
                 cands = sorted({(K_SEP2, 0, sep2_cluster(P, r)) for r in (1, 2, 3, 4, 7) if r <= P})

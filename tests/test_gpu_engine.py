@@ -760,6 +760,34 @@ def test_spatial_rows_variant(h, batch):
     eng.close()
 
 
+@pytest.mark.parametrize("c,h,batch", [(11, 37, 2), (22, 28, 3), (24, 23, 2), (11, 56, 1)])
+def test_pool_rows_variant(c, h, batch):
+    """Row-staged pool (K_POOL variant 2, sep_rows.cu pool_rows_kernel) forced
+    on every pool: max / avg (count_include_pad both ways), stride 1 / 2,
+    residual add, channel-slice stores, 44-byte pixels."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_POOL, SLOT_MULTI
+    torch.manual_seed(10)
+    m = RowsCase(c).eval()
+    x = torch.randn(batch, c, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="simt").prepare(x)
+    n = 0
+    for d in eng.ops[:len(eng.program.tasks)]:
+        if d.kind == K_POOL:
+            d.variant = 2
+            n += 1
+    assert n >= 5
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 class Shifted(nn.Module):
     def __init__(self, c):
         super().__init__()
