@@ -22,7 +22,7 @@ METRICS = [
     ("sm__cycles_elapsed.avg", "cycles", 1),
     ("dram__bytes_read.sum", "DRAM read (B)", 1),
     ("dram__bytes_write.sum", "DRAM write (B)", 1),
-    ("sm__pipe_tensor_op_gmma_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %", 1),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %", 1),
     ("sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "tc inst %", 1),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %", 1),
     ("launch__registers_per_thread", "regs/thread", 1),
