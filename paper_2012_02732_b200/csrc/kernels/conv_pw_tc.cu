@@ -104,6 +104,9 @@ struct PwArgs {
   const float* __restrict__ res;
   int M, K, P, Q, act, pre_relu, has_res, kblocks, ovec;  // ovec: float4 output / residual rows
   int64_t out_sn, out_sh, out_sw, res_sn, res_sh, res_sw;
+  // implicit GEMM (IM2COL): a tile = RT whole output rows of one image (RT*Q
+  // <= 128 pixels); K block kq = 32 channels of tap (kq / CB) of an R x S window
+  int mtiles, RT, ptiles, CB, S, sh, sw, ph, pw;
 };
 
 }  // namespace
@@ -112,7 +115,12 @@ struct PwArgs {
 // training step's current parameters) and the split warps split them into
 // tf32 hi / lo beside the activations; otherwise the prepare-time 3xTF32
 // copies are loaded as they are.
-template <int BN, bool WSPLIT>
+// IM2COL: k x k / strided convs as an implicit GEMM whose activation operand
+// is gathered by TMA: one 4-D box [32 channels][Q columns][RT rows][1 image]
+// per (tile, tap, channel block) from the NHWC input, at the tap's shifted
+// (and, for stride 2, element-strided) coordinates — the hardware zero-fills
+// the padding, and the box lands as the tile's 128-B swizzled K-major rows.
+template <int BN, bool WSPLIT, bool IM2COL = false>
 __global__ void __launch_bounds__(PW_THREADS, 1)
     conv_pw_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                       const __grid_constant__ CUtensorMap tbl, PwArgs a) {
@@ -129,8 +137,9 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
   const uint32_t sbase = su32(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n0 = blockIdx.y * BN;
-  const int mtiles = (a.M + PW_BM - 1) / PW_BM;
+  const int mtiles = a.mtiles;
   const int ntl = mtiles > (int)blockIdx.x ? (mtiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const uint32_t a_tx = IM2COL ? (uint32_t)(a.RT * a.Q * PW_BK * 4) : (uint32_t)L::A_BYTES;
   const int kb = a.kblocks;
   const int total = ntl * kb;  // (tile, K block) sequence of this CTA
 
@@ -170,11 +179,19 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
       for (int q = 0; q < total; ++q) {
         const int s = q % S;
         if (q >= S) mbar_wait_parity(su32(&empty[s]), (uint32_t)(((q / S) - 1) & 1));
-        const int m0 = ((int)blockIdx.x + (q / kb) * (int)gridDim.x) * PW_BM;
-        const int k0 = (q % kb) * PW_BK;
+        const int tg = (int)blockIdx.x + (q / kb) * (int)gridDim.x;  // tile
+        const int kq = q % kb;
+        const int k0 = kq * PW_BK;
         const uint32_t st = sbase + s * L::STAGE;
-        mbar_expect_tx(su32(&full[s]), L::A_BYTES + (WSPLIT ? 1 : 2) * L::B_BYTES);
-        tma_load_2d(st, &ta, k0, m0, su32(&full[s]));
+        mbar_expect_tx(su32(&full[s]), a_tx + (WSPLIT ? 1 : 2) * L::B_BYTES);
+        if constexpr (IM2COL) {
+          const int nb = tg / a.ptiles, p0 = (tg - nb * a.ptiles) * a.RT;
+          const int tap = kq / a.CB, c0 = (kq - tap * a.CB) * PW_BK;
+          const int r = tap / a.S, sx = tap - r * a.S;
+          tma_load_4d(st, &ta, c0, sx - a.pw, p0 * a.sh - a.ph + r, nb, su32(&full[s]));
+        } else {
+          tma_load_2d(st, &ta, k0, tg * PW_BM, su32(&full[s]));
+        }
         tma_load_2d(st + 2 * L::A_BYTES, &tbh, k0, n0, su32(&full[s]));
         if constexpr (!WSPLIT) tma_load_2d(st + 2 * L::A_BYTES + L::B_BYTES, &tbl, k0, n0, su32(&full[s]));
       }
@@ -256,10 +273,23 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
       const int b = t & 1;
       mbar_wait_parity(su32(&acc_full[b]), (uint32_t)((t >> 1) & 1));
       pw_fence_after();
-      const int m = ((int)blockIdx.x + t * (int)gridDim.x) * PW_BM + row;
-      const bool ok = m < a.M;
-      const int qq = m % a.Q, tt = m / a.Q;
-      const int pp = tt % a.P, nb = tt / a.P;
+      const int tg = (int)blockIdx.x + t * (int)gridDim.x;
+      int qq, pp, nb;
+      bool ok;
+      if constexpr (IM2COL) {  // tile = RT output rows of one image; rows past RT*Q hold no pixel
+        nb = tg / a.ptiles;
+        const int rr = row / a.Q;
+        qq = row - rr * a.Q;
+        pp = (tg - nb * a.ptiles) * a.RT + rr;
+        ok = rr < a.RT && pp < a.P;
+      } else {
+        const int m = tg * PW_BM + row;
+        ok = m < a.M;
+        qq = m % a.Q;
+        const int tt = m / a.Q;
+        pp = tt % a.P;
+        nb = tt / a.P;
+      }
       float* o = a.out + (ok ? nb * a.out_sn + pp * a.out_sh + qq * a.out_sw : 0) + n0;
       const float* rp = (a.has_res && ok) ? a.res + nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + n0 : nullptr;
       const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * 2 * BN);
@@ -309,7 +339,7 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
   }
 }
 
-template <int BN, bool WSPLIT>
+template <int BN, bool WSPLIT, bool IM2COL = false>
 static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   const int64_t* p = op.params;
   const int N = (int)p[SP_N], H = (int)p[SP_H], W = (int)p[SP_W], C = (int)p[SP_C];
@@ -336,18 +366,46 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   const void* in = reinterpret_cast<const void*>(op.ptrs[PT_IN]);
   const void* whi = reinterpret_cast<const void*>(WSPLIT ? op.ptrs[PT_W] : op.ptrs[PT_W_TC_HI]);
   const void* wlo = reinterpret_cast<const void*>(WSPLIT ? op.ptrs[PT_W] : op.ptrs[PT_W_TC_LO]);
-  if (p[SP_R] != 1 || p[SP_S] != 1 || p[SP_STRIDE_H] != 1 || p[SP_STRIDE_W] != 1 || p[SP_PAD_H] || p[SP_PAD_W] ||
-      in_sc != 1 || C % 4 || (in_sw & 3) || (op.ptrs[PT_IN] & 15) || in_sn != (int64_t)H * W * in_sw ||
-      in_sh != (int64_t)W * in_sw || osc != 1 || (a.has_res && rsc != 1) || !whi || !wlo ||
-      (!WSPLIT && Kpad % PW_BK))
+  const int R = (int)p[SP_R], S = (int)p[SP_S];
+  const int sh = (int)p[SP_STRIDE_H], sw = (int)p[SP_STRIDE_W];
+  if (IM2COL) {
+    // NHWC input (any pixel / row / image strides that are 16-B multiples),
+    // whole 128-B channel blocks per tap, output rows of <= 128 pixels
+    if (in_sc != 1 || C % PW_BK || (in_sw & 3) || (in_sh & 3) || (in_sn & 3) || (op.ptrs[PT_IN] & 15) ||
+        Q > PW_BM || Q * sw > 256 || (sh != 1 && sh != 2) || (sw != 1 && sw != 2) || osc != 1 ||
+        (a.has_res && rsc != 1) || !whi || !wlo || Kpad % PW_BK || Kpad != R * S * C)
+      return (int)cudaErrorInvalidValue;
+  } else if (R != 1 || S != 1 || sh != 1 || sw != 1 || p[SP_PAD_H] || p[SP_PAD_W] ||
+             in_sc != 1 || C % 4 || (in_sw & 3) || (op.ptrs[PT_IN] & 15) || in_sn != (int64_t)H * W * in_sw ||
+             in_sh != (int64_t)W * in_sw || osc != 1 || (a.has_res && rsc != 1) || !whi || !wlo ||
+             (!WSPLIT && Kpad % PW_BK)) {
     return (int)cudaErrorInvalidValue;
+  }
   // float4 epilogue rows when output (and residual) rows are 16-B aligned
   // (e.g. not for an 11-channel NHWC map: scalar stores)
   a.ovec = !((op.ptrs[PT_OUT] & 15) || (a.out_sw & 3) || (a.out_sh & 3) || (a.out_sn & 3) ||
              (a.has_res && ((op.ptrs[PT_RES] & 15) || (a.res_sw & 3) || (a.res_sh & 3) || (a.res_sn & 3))));
   a.kblocks = WSPLIT ? (C + PW_BK - 1) / PW_BK : Kpad / PW_BK;
   CUtensorMap ta, tbh, tbl;
-  {
+  a.mtiles = (a.M + PW_BM - 1) / PW_BM;
+  if (IM2COL) {
+    a.RT = std::min(PW_BM / Q, P);
+    if (a.RT * sh > 256) a.RT = 256 / sh;
+    a.ptiles = (P + a.RT - 1) / a.RT;
+    a.mtiles = N * a.ptiles;
+    a.CB = C / PW_BK;
+    a.S = S;
+    a.sh = sh;
+    a.sw = sw;
+    a.ph = (int)p[SP_PAD_H];
+    a.pw = (int)p[SP_PAD_W];
+    const uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)N};
+    const uint64_t strides[3] = {(uint64_t)in_sw * 4, (uint64_t)in_sh * 4, (uint64_t)in_sn * 4};
+    const uint32_t box[4] = {PW_BK, (uint32_t)(Q * sw), (uint32_t)(a.RT * sh), 1};
+    const uint32_t es[4] = {1, (uint32_t)sw, (uint32_t)sh, 1};
+    if (!encode_tmap_f32(&ta, in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, es))
+      return (int)cudaErrorInvalidValue;
+  } else {
     const uint64_t dims[2] = {(uint64_t)C, (uint64_t)a.M};
     const uint64_t strides[1] = {(uint64_t)in_sw * 4};
     const uint32_t box[2] = {PW_BK, PW_BM};
@@ -363,9 +421,8 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
       return (int)cudaErrorInvalidValue;
   }
   const int ntn = (K + BN - 1) / BN;
-  const int mtiles = (a.M + PW_BM - 1) / PW_BM;
-  const int gx = std::max(1, std::min(mtiles, std::max(1, 148 / ntn)));
-  return (int)launch_k(conv_pw_tc_kernel<BN, WSPLIT>, dim3((unsigned)gx, (unsigned)ntn), dim3(PW_THREADS),
+  const int gx = std::max(1, std::min(a.mtiles, std::max(1, 148 / ntn)));
+  return (int)launch_k(conv_pw_tc_kernel<BN, WSPLIT, IM2COL>, dim3((unsigned)gx, (unsigned)ntn), dim3(PW_THREADS),
                        (size_t)PwSmem<BN>::TOTAL, st, 1u, ta, tbh, tbl, a);
 }
 
@@ -381,6 +438,11 @@ int launch_conv_pw_tc(const sw_op_desc& op, void* stream) {
     case 8164: return launch_pw<64, true>(op, st);
     case 8196: return launch_pw<96, true>(op, st);
     case 8228: return launch_pw<128, true>(op, st);
+    // 8400 + BN: k x k / strided implicit GEMM, TMA im2col boxes (pre-split weights)
+    case 8448: return launch_pw<48, false, true>(op, st);
+    case 8464: return launch_pw<64, false, true>(op, st);
+    case 8496: return launch_pw<96, false, true>(op, st);
+    case 8528: return launch_pw<128, false, true>(op, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }
@@ -391,6 +453,11 @@ void init_pw_tc_kernels() {
   SW_PW_ATTR(48, false) SW_PW_ATTR(64, false) SW_PW_ATTR(96, false) SW_PW_ATTR(128, false)
   SW_PW_ATTR(48, true) SW_PW_ATTR(64, true) SW_PW_ATTR(96, true) SW_PW_ATTR(128, true)
 #undef SW_PW_ATTR
+#define SW_PW_ATTR_I(BN_)                                                                                \
+  cudaFuncSetAttribute(conv_pw_tc_kernel<BN_, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       PwSmem<BN_>::TOTAL);
+  SW_PW_ATTR_I(48) SW_PW_ATTR_I(64) SW_PW_ATTR_I(96) SW_PW_ATTR_I(128)
+#undef SW_PW_ATTR_I
 }
 
 }  // namespace sw

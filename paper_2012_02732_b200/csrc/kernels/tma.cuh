@@ -121,7 +121,8 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
 // bytes % 16) so the caller can refuse the variant.
 inline bool encode_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
                             const uint64_t* strides_bytes, const uint32_t* box,
-                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE,
+                            const uint32_t* elem_strides = nullptr) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -141,7 +142,7 @@ inline bool encode_tmap_f32(CUtensorMap* m, const void* base, int rank, const ui
   for (int i = 0; i < rank; ++i) {
     d[i] = dims[i];
     b[i] = box[i];
-    e[i] = 1;
+    e[i] = elem_strides ? elem_strides[i] : 1;  // traversal stride (box spans b[i] elements, loads ceil(b/e))
   }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), d, s, b, e,

@@ -134,7 +134,9 @@ PWTC_TILES = (48, 64, 96, 128)
 
 
 def pw_tc_bn(variant: int) -> int:
-    return variant - (8100 if variant >= 8100 else 8000)
+    """BN of a conv_pw_tc.cu variant: 8000 + BN (pre-split weights), 8100 + BN
+    (in-kernel split), 8400 + BN (k x k implicit GEMM, TMA im2col boxes)."""
+    return variant - (8400 if variant >= 8400 else 8100 if variant >= 8100 else 8000)
 TCS_MAX_M = 4096  # pixels per image batch up to which those variants are candidates
 # the bf16 variants stay in the weight-streaming regime their tolerance was
 # stated for (DESIGN §7): more bf16 layers compound the bf16 rounding
@@ -143,7 +145,7 @@ BF16_TUNE_RTOL = 3e-2  # autotuner check of a bf16 candidate: |d| <= 3e-2 * max(
 
 
 def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
-                    bf16: bool = False) -> list[tuple[int, int, int]]:
+                    bf16: bool = False, stride=(1, 1)) -> list[tuple[int, int, int]]:
     """(kernel kind, variant, split) choices the prepare-time autotuner times."""
     out = []
     if M <= 8 and R == 1 and S == 1 and tuple(pad) == (0, 0):
@@ -204,6 +206,15 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
                 continue
             out.append((K_CONV_TC, 8000 + bn, 1))  # prepare-time 3xTF32 weight copies
             out.append((K_CONV_TC, 8100 + bn, 1))  # fp32 weights split in the kernel
+    if M >= 4096 and (not pointwise or tuple(stride) != (1, 1)):
+        # large-batch k x k / strided conv: the same persistent kernel as an
+        # implicit GEMM over TMA im2col boxes (conv_pw_tc.cu IM2COL; refuses
+        # channel counts that are not whole 32-channel blocks)
+        for bn in PWTC_TILES:
+            if (bn > 2 * max(K, 16) and bn != 48) or \
+                    (bn < K and math.ceil(K / bn) * bn - K >= bn // 2 and bn != 128):
+                continue
+            out.append((K_CONV_TC, 8400 + bn, 1))
     if M <= TCS_MAX_M:
         # weight-streaming swap-AB tcgen05 kernel (conv_tcs.cu): out channels on
         # the UMMA M side, NT pixels per tile, split-K cluster <= 16
@@ -838,7 +849,7 @@ class Engine:
                           if SEP_TMA_FIRST <= v < SEP_ROW_FIRST and 2 <= math.ceil(K / bn) <= 8]
             else:
                 cands = conv_candidates(M, K, Kdim, p[SP_R], p[SP_S], (p[SP_PAD_H], p[SP_PAD_W]),
-                                        bf16=p[SP_WS_KIND] == 1)
+                                        bf16=p[SP_WS_KIND] == 1, stride=(p[SP_STRIDE_H], p[SP_STRIDE_W]))
             timed = []
             for kind, variant, split in cands:
                 trial.kind = kind

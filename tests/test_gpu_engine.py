@@ -463,6 +463,62 @@ class SepBN(nn.Module):
         return y + self.res(x) if self.res is not None else y
 
 
+@pytest.mark.parametrize("bn", [48, 64, 96, 128])
+@pytest.mark.parametrize("cin,cout,k,s,h,batch,res", [
+    (64, 64, 3, 1, 28, 8, False),       # ResNet-style 3x3, whole-row tiles (4 rows of 28)
+    (32, 96, 3, 2, 29, 10, True),       # stride 2 (element-strided boxes), odd size, residual
+    (64, 48, (1, 7), 1, 17, 16, False),  # Inception 1x7: asymmetric window / padding
+    (128, 128, 1, 2, 28, 24, False),    # strided 1x1 downsample
+    (32, 40, 5, 1, 14, 24, True),       # 5x5, K not a multiple of the N tile
+])
+def test_tcgen05_im2col_persistent(bn, cin, cout, k, s, h, batch, res):
+    """conv_pw_tc.cu IM2COL (variants 8400 + BN) forced: k x k / strided convs
+    as a persistent implicit GEMM over TMA im2col boxes (4-D tensor map,
+    shifted / element-strided coordinates, zero-filled padding)."""
+    from paper_2012_02732_b200 import _native as N
+    from paper_2012_02732_b200.engine import K_CONV_TC, SLOT_MULTI, SP_SPLIT_K
+    from paper_2012_02732_b200.networks import randomize_bn
+    torch.manual_seed(11)
+    kh, kw = (k, k) if isinstance(k, int) else k
+    pad = (kh // 2, kw // 2)
+
+    class M(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.lead = nn.Conv2d(cin, cin, 1, bias=False)
+            self.c = nn.Conv2d(cin, cout, (kh, kw), s, pad, bias=False)
+            self.bn = nn.BatchNorm2d(cout)
+            self.r = nn.Conv2d(cin, cout, 1, s, 0, bias=False) if res else None
+            self.tail = nn.Conv2d(cout, 8, 1)
+
+        def forward(self, x):
+            h0 = torch.relu(self.lead(x))
+            y = self.bn(self.c(h0))
+            if self.r is not None:
+                y = y + self.r(h0)
+            return self.tail(torch.relu(y))
+
+    m = M().eval()
+    randomize_bn(m)
+    x = torch.randn(batch, cin, h, h)
+    with torch.no_grad():
+        ref = m(x)
+    eng = Engine(m, conv_impl="tc").prepare(x)
+    idx = [t.tid for t in eng.program.tasks if t.kind == "conv" and (t.name == "c" or t.name.startswith("c."))]
+    assert len(idx) == 1, [t.name for t in eng.program.tasks]
+    d = eng.ops[idx[0]]
+    d.kind = K_CONV_TC
+    d.variant = 8400 + bn
+    d.params[SP_SPLIT_K] = 1
+    N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
+    eng._capture(SLOT_MULTI, eng.schedule, False)
+    eng.load_input_device(x)
+    eng.replay(multi=True)
+    eng.synchronize()
+    close(eng.device_output().cpu(), ref)
+    eng.close()
+
+
 @pytest.mark.parametrize("variant", [20, 21, 22, 23])
 @pytest.mark.parametrize("cin,cout,k,s,h,batch,lead,res", [
     (32, 11, 7, 2, 111, 2, True, False),   # NASNet stem sep1: 32 → 11 channels, 7x7 s2 on 111x111
