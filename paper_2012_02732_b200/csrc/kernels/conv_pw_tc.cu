@@ -104,9 +104,10 @@ struct PwArgs {
   const float* __restrict__ res;
   int M, K, P, Q, act, pre_relu, has_res, kblocks, ovec;  // ovec: float4 output / residual rows
   int64_t out_sn, out_sh, out_sw, res_sn, res_sh, res_sw;
-  // implicit GEMM (IM2COL): a tile = RT whole output rows of one image (RT*Q
-  // <= 128 pixels); K block kq = 32 channels of tap (kq / CB) of an R x S window
-  int mtiles, RT, ptiles, CB, S, sh, sw, ph, pw;
+  // implicit GEMM (IM2COL): a tile = RT output rows x CQ columns of one image
+  // (RT whole rows when Q <= 128, else one row in nseg column segments);
+  // K block kq = 32 channels (zero-filled past C) of tap (kq / CB) of R x S
+  int mtiles, RT, CQ, nseg, ptiles, CB, C, S, sh, sw, ph, pw;
 };
 
 }  // namespace
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
   const int n0 = blockIdx.y * BN;
   const int mtiles = a.mtiles;
   const int ntl = mtiles > (int)blockIdx.x ? (mtiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const uint32_t a_tx = IM2COL ? (uint32_t)(a.RT * a.Q * PW_BK * 4) : (uint32_t)L::A_BYTES;
+  const uint32_t a_tx = IM2COL ? (uint32_t)(a.RT * a.CQ * PW_BK * 4) : (uint32_t)L::A_BYTES;
   const int kb = a.kblocks;
   const int total = ntl * kb;  // (tile, K block) sequence of this CTA
 
@@ -181,14 +182,17 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
         if (q >= S) mbar_wait_parity(su32(&empty[s]), (uint32_t)(((q / S) - 1) & 1));
         const int tg = (int)blockIdx.x + (q / kb) * (int)gridDim.x;  // tile
         const int kq = q % kb;
-        const int k0 = kq * PW_BK;
+        int k0 = kq * PW_BK;
         const uint32_t st = sbase + s * L::STAGE;
         mbar_expect_tx(su32(&full[s]), a_tx + (WSPLIT ? 1 : 2) * L::B_BYTES);
         if constexpr (IM2COL) {
-          const int nb = tg / a.ptiles, p0 = (tg - nb * a.ptiles) * a.RT;
+          const int nb = tg / a.ptiles, rem = tg - nb * a.ptiles;
+          const int prow = rem / a.nseg, seg = rem - prow * a.nseg;
+          const int p0 = prow * a.RT, q0 = seg * a.CQ;
           const int tap = kq / a.CB, c0 = (kq - tap * a.CB) * PW_BK;
           const int r = tap / a.S, sx = tap - r * a.S;
-          tma_load_4d(st, &ta, c0, sx - a.pw, p0 * a.sh - a.ph + r, nb, su32(&full[s]));
+          k0 = tap * a.C + c0;  // weight columns of (tap, channel block); past C the activations are zero
+          tma_load_4d(st, &ta, c0, q0 * a.sw - a.pw + sx, p0 * a.sh - a.ph + r, nb, su32(&full[s]));
         } else {
           tma_load_2d(st, &ta, k0, tg * PW_BM, su32(&full[s]));
         }
@@ -276,12 +280,14 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
       const int tg = (int)blockIdx.x + t * (int)gridDim.x;
       int qq, pp, nb;
       bool ok;
-      if constexpr (IM2COL) {  // tile = RT output rows of one image; rows past RT*Q hold no pixel
+      if constexpr (IM2COL) {  // tile = RT x CQ output pixels of one image; rows past RT*CQ hold none
         nb = tg / a.ptiles;
-        const int rr = row / a.Q;
-        qq = row - rr * a.Q;
-        pp = (tg - nb * a.ptiles) * a.RT + rr;
-        ok = rr < a.RT && pp < a.P;
+        const int rem = tg - nb * a.ptiles;
+        const int prow = rem / a.nseg, seg = rem - prow * a.nseg;
+        const int rr = row / a.CQ;
+        qq = seg * a.CQ + (row - rr * a.CQ);
+        pp = prow * a.RT + rr;
+        ok = rr < a.RT && pp < a.P && qq < a.Q;
       } else {
         const int m = tg * PW_BM + row;
         ok = m < a.M;
@@ -371,9 +377,9 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   if (IM2COL) {
     // NHWC input (any pixel / row / image strides that are 16-B multiples),
     // whole 128-B channel blocks per tap, output rows of <= 128 pixels
-    if (in_sc != 1 || C % PW_BK || (in_sw & 3) || (in_sh & 3) || (in_sn & 3) || (op.ptrs[PT_IN] & 15) ||
-        Q > PW_BM || Q * sw > 256 || (sh != 1 && sh != 2) || (sw != 1 && sw != 2) || osc != 1 ||
-        (a.has_res && rsc != 1) || !whi || !wlo || Kpad % PW_BK || Kpad != R * S * C)
+    if (in_sc != 1 || C % 4 || (in_sw & 3) || (in_sh & 3) || (in_sn & 3) || (op.ptrs[PT_IN] & 15) ||
+        (sh != 1 && sh != 2) || (sw != 1 && sw != 2) || osc != 1 || (a.has_res && rsc != 1) || !whi || !wlo ||
+        Kpad % PW_BK || Kpad < R * S * C)
       return (int)cudaErrorInvalidValue;
   } else if (R != 1 || S != 1 || sh != 1 || sw != 1 || p[SP_PAD_H] || p[SP_PAD_W] ||
              in_sc != 1 || C % 4 || (in_sw & 3) || (op.ptrs[PT_IN] & 15) || in_sn != (int64_t)H * W * in_sw ||
@@ -389,11 +395,21 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   CUtensorMap ta, tbh, tbl;
   a.mtiles = (a.M + PW_BM - 1) / PW_BM;
   if (IM2COL) {
-    a.RT = std::min(PW_BM / Q, P);
-    if (a.RT * sh > 256) a.RT = 256 / sh;
-    a.ptiles = (P + a.RT - 1) / a.RT;
+    if (Q <= PW_BM) {
+      a.RT = std::min(PW_BM / Q, P);
+      if (a.RT * sh > 256) a.RT = 256 / sh;
+      a.nseg = 1;
+      a.CQ = Q;
+    } else {
+      a.RT = 1;
+      a.nseg = (Q + PW_BM - 1) / PW_BM;
+      a.CQ = (Q + a.nseg - 1) / a.nseg;
+    }
+    a.ptiles = (P + a.RT - 1) / a.RT * a.nseg;
     a.mtiles = N * a.ptiles;
-    a.CB = C / PW_BK;
+    a.CB = (C + PW_BK - 1) / PW_BK;
+    a.C = C;
+    a.kblocks = R * S * a.CB;
     a.S = S;
     a.sh = sh;
     a.sw = sw;
@@ -401,7 +417,7 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
     a.pw = (int)p[SP_PAD_W];
     const uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)N};
     const uint64_t strides[3] = {(uint64_t)in_sw * 4, (uint64_t)in_sh * 4, (uint64_t)in_sn * 4};
-    const uint32_t box[4] = {PW_BK, (uint32_t)(Q * sw), (uint32_t)(a.RT * sh), 1};
+    const uint32_t box[4] = {PW_BK, (uint32_t)(a.CQ * sw), (uint32_t)(a.RT * sh), 1};
     const uint32_t es[4] = {1, (uint32_t)sw, (uint32_t)sh, 1};
     if (!encode_tmap_f32(&ta, in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, es))
       return (int)cudaErrorInvalidValue;

@@ -206,7 +206,7 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
                 continue
             out.append((K_CONV_TC, 8000 + bn, 1))  # prepare-time 3xTF32 weight copies
             out.append((K_CONV_TC, 8100 + bn, 1))  # fp32 weights split in the kernel
-    if M >= 4096 and (not pointwise or tuple(stride) != (1, 1)):
+    if M >= 1024 and (not pointwise or tuple(stride) != (1, 1)):
         # large-batch k x k / strided conv: the same persistent kernel as an
         # implicit GEMM over TMA im2col boxes (conv_pw_tc.cu IM2COL; refuses
         # channel counts that are not whole 32-channel blocks)

@@ -470,6 +470,10 @@ class SepBN(nn.Module):
     (64, 48, (1, 7), 1, 17, 16, False),  # Inception 1x7: asymmetric window / padding
     (128, 128, 1, 2, 28, 24, False),    # strided 1x1 downsample
     (32, 40, 5, 1, 14, 24, True),       # 5x5, K not a multiple of the N tile
+    (80, 96, 3, 1, 31, 6, False),       # 80 channels: partial 32-channel blocks (zero-filled boxes)
+    (48, 64, 5, 1, 35, 4, True),        # Inception 5x5 on 48 channels
+    (32, 64, 3, 1, 140, 1, False),      # 140-wide rows: two 70-column segments per output row
+    (32, 32, 3, 2, 263, 1, False),      # stride 2, 132-wide output rows: column segments + strided boxes
 ])
 def test_tcgen05_im2col_persistent(bn, cin, cout, k, s, h, batch, res):
     """conv_pw_tc.cu IM2COL (variants 8400 + BN) forced: k x k / strided convs
