@@ -108,6 +108,8 @@ struct PwArgs {
   // (RT whole rows when Q <= 128, else one row in nseg column segments);
   // K block kq = 32 channels (zero-filled past C) of tap (kq / CB) of R x S
   int mtiles, RT, CQ, nseg, ptiles, CB, C, S, sh, sw, ph, pw;
+  // IM2COL: K blocks per accumulation chunk (see PROMO in the kernel)
+  int kchunk;
 };
 
 }  // namespace
@@ -121,7 +123,7 @@ struct PwArgs {
 // per (tile, tap, channel block) from the NHWC input, at the tap's shifted
 // (and, for stride 2, element-strided) coordinates — the hardware zero-fills
 // the padding, and the box lands as the tile's 128-B swizzled K-major rows.
-template <int BN, bool WSPLIT, bool IM2COL = false>
+template <int BN, bool WSPLIT, bool IM2COL = false, bool PROMO = IM2COL>
 __global__ void __launch_bounds__(PW_THREADS, 1)
     conv_pw_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                       const __grid_constant__ CUtensorMap tbl, PwArgs a) {
@@ -236,35 +238,47 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
     constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                ((uint32_t)(PW_BM >> 4) << 24);
     const uint64_t a0 = pw_desc_sw128(sbase);
+    // PROMO (IM2COL): a tile's K blocks run in chunks of a.kchunk, each into a
+    // fresh accumulator pair (chunk parity), so no TMEM accumulation chain is
+    // longer than one chunk; the epilogue sums the chunks in fp32 registers.
+    // (The tensor pipe's fp32 accumulate truncates: over the 27-45 K blocks of
+    // an implicit-GEMM 3x3 / 5x5 layer one chain biased outputs by ~-1.3e-6
+    // relative, enough to move Inception-v3's logits past the fp32 gate.)
+    const int G = PROMO ? a.kchunk : kb;
+    int u = 0;  // accumulation unit (tile, or tile chunk) sequence of this CTA
 #pragma unroll 1
     for (int t = 0; t < ntl; ++t) {
-      const int b = t & 1;
-      if (t >= 2) mbar_wait_parity(su32(&acc_free[b]), (uint32_t)(((t >> 1) - 1) & 1));
-      pw_fence_after();
-      const uint32_t dmain = tmem + (uint32_t)(b * 2 * BN), dcorr = dmain + BN;
 #pragma unroll 1
-      for (int kq = 0; kq < kb; ++kq) {
-        const int q = t * kb + kq;
-        const int s = q % S;
-        mbar_wait_parity(su32(&ready[s]), (uint32_t)((q / S) & 1));
+      for (int j0 = 0; j0 < kb; j0 += G, ++u) {
+        const int b = u & 1;
+        const int j1 = min(kb, j0 + G);
+        if (u >= 2) mbar_wait_parity(su32(&acc_free[b]), (uint32_t)(((u >> 1) - 1) & 1));
         pw_fence_after();
-        if (pw_elect()) {
-          const uint64_t st = a0 + (uint64_t)((s * L::STAGE) >> 4);
+        const uint32_t dmain = tmem + (uint32_t)(b * 2 * BN), dcorr = dmain + BN;
+#pragma unroll 1
+        for (int kq = j0; kq < j1; ++kq) {
+          const int q = t * kb + kq;
+          const int s = q % S;
+          mbar_wait_parity(su32(&ready[s]), (uint32_t)((q / S) & 1));
+          pw_fence_after();
+          if (pw_elect()) {
+            const uint64_t st = a0 + (uint64_t)((s * L::STAGE) >> 4);
 #pragma unroll
-          for (int ks = 0; ks < PW_BK / 8; ++ks) {
-            const uint64_t ah = st + (uint64_t)(ks * 2);  // +32 B inside the swizzle atom
-            const uint64_t al = ah + (uint64_t)(L::A_BYTES >> 4);
-            const uint64_t bh = ah + (uint64_t)((2 * L::A_BYTES) >> 4);
-            const uint64_t bl = bh + (uint64_t)(L::B_BYTES >> 4);
-            const uint32_t acc = (kq | ks) ? 1u : 0u;
-            pw_mma(dmain, ah, bh, idesc, acc);
-            pw_mma(dcorr, ah, bl, idesc, acc);
-            pw_mma(dcorr, al, bh, idesc, 1u);
+            for (int ks = 0; ks < PW_BK / 8; ++ks) {
+              const uint64_t ah = st + (uint64_t)(ks * 2);  // +32 B inside the swizzle atom
+              const uint64_t al = ah + (uint64_t)(L::A_BYTES >> 4);
+              const uint64_t bh = ah + (uint64_t)((2 * L::A_BYTES) >> 4);
+              const uint64_t bl = bh + (uint64_t)(L::B_BYTES >> 4);
+              const uint32_t acc = (kq != j0 || ks) ? 1u : 0u;
+              pw_mma(dmain, ah, bh, idesc, acc);
+              pw_mma(dcorr, ah, bl, idesc, acc);
+              pw_mma(dcorr, al, bh, idesc, 1u);
+            }
+            pw_commit(su32(&empty[s]));
+            if (kq == j1 - 1) pw_commit(su32(&acc_full[b]));
           }
-          pw_commit(su32(&empty[s]));
-          if (kq == kb - 1) pw_commit(su32(&acc_full[b]));
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else {
@@ -272,11 +286,14 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
     pdl_wait();  // residual / output buffers of earlier tasks
     const int quad = warp & 3;  // TMEM lanes 32*quad .. +31
     const int row = quad * 32 + lane;
+    int u = 0;  // accumulation unit sequence (as the MMA issuer counts it)
 #pragma unroll 1
     for (int t = 0; t < ntl; ++t) {
       const int b = t & 1;
-      mbar_wait_parity(su32(&acc_full[b]), (uint32_t)((t >> 1) & 1));
-      pw_fence_after();
+      if constexpr (!PROMO) {
+        mbar_wait_parity(su32(&acc_full[b]), (uint32_t)((t >> 1) & 1));
+        pw_fence_after();
+      }
       const int tg = (int)blockIdx.x + t * (int)gridDim.x;
       int qq, pp, nb;
       bool ok;
@@ -298,6 +315,57 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
       }
       float* o = a.out + (ok ? nb * a.out_sn + pp * a.out_sh + qq * a.out_sw : 0) + n0;
       const float* rp = (a.has_res && ok) ? a.res + nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + n0 : nullptr;
+      if constexpr (PROMO) {
+        // sum the tile's chunk accumulators (main + correction) in fp32
+        // registers, releasing each TMEM pair as soon as it is read
+        float racc[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) racc[j] = 0.f;
+#pragma unroll 1
+        for (int j0 = 0; j0 < kb; j0 += a.kchunk, ++u) {
+          const int bu = u & 1;
+          mbar_wait_parity(su32(&acc_full[bu]), (uint32_t)((u >> 1) & 1));
+          pw_fence_after();
+          const uint32_t tu = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(bu * 2 * BN);
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16], w[16];
+            pw_ld16(tu + (uint32_t)c0, v);
+            pw_ld16(tu + (uint32_t)(BN + c0), w);
+            pw_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) racc[c0 + j] += v[j] + w[j];
+          }
+          pw_fence_before();
+          __syncwarp();
+          if (lane == 0) pw_arrive(su32(&acc_free[bu]));
+        }
+        if (ok) {
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            const int nv = min(16, a.K - n0 - c0);
+            if (nv <= 0) break;
+            if (a.ovec && nv == 16) {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) {
+                float4 x = make_float4(racc[c0 + j], racc[c0 + j + 1], racc[c0 + j + 2], racc[c0 + j + 3]);
+                x = f4add(x, *reinterpret_cast<const float4*>(bias_s + c0 + j));
+                if (rp) x = f4add(x, *reinterpret_cast<const float4*>(rp + c0 + j));
+                *reinterpret_cast<float4*>(o + c0 + j) = act4(x, a.act);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (j >= nv) break;
+                float x = racc[c0 + j] + bias_s[c0 + j];
+                if (rp) x += rp[c0 + j];
+                o[c0 + j] = apply_act(x, a.act);
+              }
+            }
+          }
+        }
+        continue;
+      }
       const uint32_t tl = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * 2 * BN);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -394,6 +462,7 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   a.kblocks = WSPLIT ? (C + PW_BK - 1) / PW_BK : Kpad / PW_BK;
   CUtensorMap ta, tbh, tbl;
   a.mtiles = (a.M + PW_BM - 1) / PW_BM;
+  a.kchunk = a.kblocks;
   if (IM2COL) {
     if (Q <= PW_BM) {
       a.RT = std::min(PW_BM / Q, P);
@@ -410,6 +479,9 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
     a.CB = (C + PW_BK - 1) / PW_BK;
     a.C = C;
     a.kblocks = R * S * a.CB;
+    // chunks of <= 8 K blocks (256 products), balanced across the tile's K
+    const int nch = (a.kblocks + 7) / 8;
+    a.kchunk = (a.kblocks + nch - 1) / nch;
     a.S = S;
     a.sh = sh;
     a.sw = sw;

@@ -122,7 +122,8 @@ def test_conv_candidates_tcgen05_variants():
     variants (two-stage 2000 + N, persistent 3000 + N, swizzled 4000 + N) are
     offered only for pointwise convs with M >= 4096 (5000 + N, swizzled one
     tile per CTA, for any pointwise conv), persistent ones only at
-    split 1; k x k convs never get TMA variants; tiny M gets the GEMV."""
+    split 1; k x k convs get no pointwise TMA variants, only the TMA-im2col
+    persistent ones (8400 + N, M >= 1024); tiny M gets the GEMV."""
     from paper_2012_02732_b200.engine import K_CONV, K_CONV_TC, conv_candidates
     big = conv_candidates(200704, 88, 264, 1, 1, (0, 0))
     tc = {(v, s) for k, v, s in big if k == K_CONV_TC}
@@ -134,6 +135,8 @@ def test_conv_candidates_tcgen05_variants():
     assert not any(k == K_CONV_TC and 2000 <= v < 5000 for k, v, _ in small)
     assert any(k == K_CONV_TC and v >= 5000 for k, v, _ in small)  # swizzled one-tile variants: any M
     kxk = conv_candidates(200704, 64, 576, 3, 3, (1, 1))
-    assert not any(k == K_CONV_TC and v >= 1000 for k, v, _ in kxk)
+    assert not any(k == K_CONV_TC and 1000 <= v < 8400 for k, v, _ in kxk)
+    assert {v for k, v, s in kxk if k == K_CONV_TC and v >= 8400} == {8464, 8496, 8528}  # 48: a 64-channel layer would pad to 96
+    assert not any(k == K_CONV_TC and v >= 8400 for k, v, _ in conv_candidates(512, 64, 576, 3, 3, (1, 1)))
     gemv = conv_candidates(1, 1000, 1056, 1, 1, (0, 0))
     assert (K_CONV, 8, 1) in gemv
