@@ -108,8 +108,10 @@ struct PwArgs {
   // (RT whole rows when Q <= 128, else one row in nseg column segments);
   // K block kq = 32 channels (zero-filled past C) of tap (kq / CB) of R x S
   int mtiles, RT, CQ, nseg, ptiles, CB, C, S, sh, sw, ph, pw;
-  // IM2COL: K blocks per accumulation chunk (see PROMO in the kernel)
-  int kchunk;
+  // IM2COL: K blocks per accumulation chunk (see PROMO in the kernel);
+  // split > 1: the K blocks split over a (1, 1, split) cluster, one tile per
+  // CTA, partial tiles reduced through DSMEM in rank order
+  int kchunk, split;
 };
 
 }  // namespace
@@ -143,7 +145,11 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
   const int mtiles = a.mtiles;
   const int ntl = mtiles > (int)blockIdx.x ? (mtiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const uint32_t a_tx = IM2COL ? (uint32_t)(a.RT * a.CQ * PW_BK * 4) : (uint32_t)L::A_BYTES;
-  const int kb = a.kblocks;
+  // split-K (IM2COL, a.split > 1): cluster rank z owns K blocks
+  // [kb_lo, kb_lo + kb) of the layer's a.kblocks
+  const int zr = (PROMO && a.split > 1) ? (int)blockIdx.z : 0;
+  const int kb_lo = PROMO ? (zr * a.kblocks) / a.split : 0;
+  const int kb = PROMO ? ((zr + 1) * a.kblocks) / a.split - kb_lo : a.kblocks;
   const int total = ntl * kb;  // (tile, K block) sequence of this CTA
 
   if (tid == 0) {
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
         const int s = q % S;
         if (q >= S) mbar_wait_parity(su32(&empty[s]), (uint32_t)(((q / S) - 1) & 1));
         const int tg = (int)blockIdx.x + (q / kb) * (int)gridDim.x;  // tile
-        const int kq = q % kb;
+        const int kq = kb_lo + q % kb;
         int k0 = kq * PW_BK;
         const uint32_t st = sbase + s * L::STAGE;
         mbar_expect_tx(su32(&full[s]), a_tx + (WSPLIT ? 1 : 2) * L::B_BYTES);
@@ -340,6 +346,14 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
           __syncwarp();
           if (lane == 0) pw_arrive(su32(&acc_free[bu]));
         }
+        if (a.split > 1) {
+          // one tile per CTA: the ring is quiescent (every MMA has completed);
+          // park the partial tile [BN][128 rows] for the rank-ordered sum
+          float* part = reinterpret_cast<float*>(smem);
+#pragma unroll
+          for (int j = 0; j < BN; ++j) part[j * PW_BM + row] = racc[j];
+          continue;
+        }
         if (ok) {
 #pragma unroll
           for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -403,6 +417,63 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
       if (lane == 0) pw_arrive(su32(&acc_free[b]));
     }
   }
+  if constexpr (PROMO) {
+    if (a.split > 1) {
+      // every rank's partial is parked in its smem: rank 0's epilogue warps
+      // sum ranks 0..split-1 in order (DSMEM loads), add bias / residual /
+      // activation and store; the second cluster barrier keeps the peers'
+      // shared memory alive until those loads are done
+      __syncwarp();
+      asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
+      cluster_wait();
+      if (zr == 0 && warp >= 6) {
+        const int row = (warp & 3) * 32 + lane;
+        const int tg = (int)blockIdx.x;
+        const int nb = tg / a.ptiles;
+        const int rem = tg - nb * a.ptiles;
+        const int prow = rem / a.nseg, seg = rem - prow * a.nseg;
+        const int rr = row / a.CQ;
+        const int qq = seg * a.CQ + (row - rr * a.CQ), pp = prow * a.RT + rr;
+        const bool ok = ntl > 0 && rr < a.RT && pp < a.P && qq < a.Q;
+        if (ok) {
+          float* o = a.out + nb * a.out_sn + pp * a.out_sh + qq * a.out_sw + n0;
+          const float* rp = a.has_res ? a.res + nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + n0 : nullptr;
+          const uint32_t part = sbase + (uint32_t)(row * 4);
+          const int nv = min(BN, a.K - n0);
+#pragma unroll 1
+          for (int j0 = 0; j0 < nv; j0 += 4) {
+            float x[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+            for (int z = 0; z < a.split; ++z) {
+              const uint32_t src = mapa_rank(part + (uint32_t)(j0 * PW_BM * 4), (uint32_t)z);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                float v;
+                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(src + (uint32_t)(i * PW_BM * 4)));
+                x[i] += v;
+              }
+            }
+            if (a.ovec && j0 + 4 <= nv) {
+              float4 y = f4add(make_float4(x[0], x[1], x[2], x[3]), *reinterpret_cast<const float4*>(bias_s + j0));
+              if (rp) y = f4add(y, *reinterpret_cast<const float4*>(rp + j0));
+              *reinterpret_cast<float4*>(o + j0) = act4(y, a.act);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                if (j0 + i >= nv) break;
+                float y = x[i] + bias_s[j0 + i];
+                if (rp) y += rp[j0 + i];
+                o[j0 + i] = apply_act(y, a.act);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
+      cluster_wait();
+    }
+  }
   pw_fence_before();
   __syncthreads();
   if (warp == 5) {
@@ -463,6 +534,7 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
   CUtensorMap ta, tbh, tbl;
   a.mtiles = (a.M + PW_BM - 1) / PW_BM;
   a.kchunk = a.kblocks;
+  a.split = 1;
   if (IM2COL) {
     if (Q <= PW_BM) {
       a.RT = std::min(PW_BM / Q, P);
@@ -480,8 +552,10 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
     a.C = C;
     a.kblocks = R * S * a.CB;
     // chunks of <= 8 K blocks (256 products), balanced across the tile's K
-    const int nch = (a.kblocks + 7) / 8;
-    a.kchunk = (a.kblocks + nch - 1) / nch;
+    a.split = std::max(1, std::min((int)p[SP_SPLIT_K], a.kblocks));
+    const int kbr = (a.kblocks + a.split - 1) / a.split;
+    const int nch = (kbr + 7) / 8;
+    a.kchunk = (kbr + nch - 1) / nch;
     a.S = S;
     a.sh = sh;
     a.sw = sw;
@@ -509,9 +583,11 @@ static int launch_pw(const sw_op_desc& op, cudaStream_t st) {
       return (int)cudaErrorInvalidValue;
   }
   const int ntn = (K + BN - 1) / BN;
-  const int gx = std::max(1, std::min(a.mtiles, std::max(1, 148 / ntn)));
-  return (int)launch_k(conv_pw_tc_kernel<BN, WSPLIT, IM2COL>, dim3((unsigned)gx, (unsigned)ntn), dim3(PW_THREADS),
-                       (size_t)PwSmem<BN>::TOTAL, st, 1u, ta, tbh, tbl, a);
+  // split-K: one tile per CTA (the cluster reduces it); else persistent
+  const int gx = a.split > 1 ? a.mtiles : std::max(1, std::min(a.mtiles, std::max(1, 148 / ntn)));
+  if (a.split > 8) return (int)cudaErrorInvalidValue;
+  return (int)launch_k(conv_pw_tc_kernel<BN, WSPLIT, IM2COL>, dim3((unsigned)gx, (unsigned)ntn, (unsigned)a.split),
+                       dim3(PW_THREADS), (size_t)PwSmem<BN>::TOTAL, st, (unsigned)a.split, ta, tbh, tbl, a);
 }
 
 int launch_conv_pw_tc(const sw_op_desc& op, void* stream) {

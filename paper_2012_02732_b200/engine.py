@@ -209,12 +209,18 @@ def conv_candidates(M: int, K: int, Kdim: int, R: int, S: int, pad,
     if M >= 1024 and (not pointwise or tuple(stride) != (1, 1)):
         # large-batch k x k / strided conv: the same persistent kernel as an
         # implicit GEMM over TMA im2col boxes (conv_pw_tc.cu IM2COL; refuses
-        # channel counts that are not whole 32-channel blocks)
+        # channel counts that are not multiples of 4)
         for bn in PWTC_TILES:
             if (bn > 2 * max(K, 16) and bn != 48) or \
                     (bn < K and math.ceil(K / bn) * bn - K >= bn // 2 and bn != 128):
                 continue
             out.append((K_CONV_TC, 8400 + bn, 1))
+            # split-K over a (1, 1, split) cluster, one tile per CTA, DSMEM
+            # rank-ordered sum: layers with few pixel tiles (batch 1)
+            ctas = math.ceil(M / 128) * math.ceil(K / bn)
+            for split in (2, 4, 8):
+                if split <= ktiles // 2 and ctas * split <= 2 * NUM_SMS:
+                    out.append((K_CONV_TC, 8400 + bn, split))
     if M <= TCS_MAX_M:
         # weight-streaming swap-AB tcgen05 kernel (conv_tcs.cu): out channels on
         # the UMMA M side, NT pixels per tile, split-K cluster <= 16
@@ -905,6 +911,8 @@ class Engine:
                 return cd(M / 128)
             bm, bn = PW_TILES[variant] if variant >= 16 else SIMT_TILES[variant]
             return cd(M / bm) * cd(K / bn) * max(1, split)
+        if kind == K_CONV_TC and variant >= 8400 and split > 1:
+            return cd(M / 128) * cd(K / pw_tc_bn(variant)) * split  # one tile per CTA
         if kind == K_CONV_TC and variant >= 8000:
             ntn = cd(K / pw_tc_bn(variant))
             return min(cd(M / 128), max(1, NUM_SMS // ntn)) * ntn

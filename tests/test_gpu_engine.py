@@ -475,10 +475,13 @@ class SepBN(nn.Module):
     (32, 64, 3, 1, 140, 1, False),      # 140-wide rows: two 70-column segments per output row
     (32, 32, 3, 2, 263, 1, False),      # stride 2, 132-wide output rows: column segments + strided boxes
 ])
-def test_tcgen05_im2col_persistent(bn, cin, cout, k, s, h, batch, res):
+@pytest.mark.parametrize("split", [1, 3, 4])
+def test_tcgen05_im2col_persistent(bn, cin, cout, k, s, h, batch, res, split):
     """conv_pw_tc.cu IM2COL (variants 8400 + BN) forced: k x k / strided convs
     as a persistent implicit GEMM over TMA im2col boxes (4-D tensor map,
-    shifted / element-strided coordinates, zero-filled padding)."""
+    shifted / element-strided coordinates, zero-filled padding); split > 1:
+    the K blocks over a (1, 1, split) cluster, partial tiles summed in rank
+    order through DSMEM (uneven K ranges at split 3)."""
     from paper_2012_02732_b200 import _native as N
     from paper_2012_02732_b200.engine import K_CONV_TC, SLOT_MULTI, SP_SPLIT_K
     from paper_2012_02732_b200.networks import randomize_bn
@@ -513,7 +516,7 @@ def test_tcgen05_im2col_persistent(bn, cin, cout, k, s, h, batch, res):
     d = eng.ops[idx[0]]
     d.kind = K_CONV_TC
     d.variant = 8400 + bn
-    d.params[SP_SPLIT_K] = 1
+    d.params[SP_SPLIT_K] = split
     N.check(N.lib().sw_engine_set_ops(eng._h, len(eng.program.tasks), eng.ops))
     eng._capture(SLOT_MULTI, eng.schedule, False)
     eng.load_input_device(x)
