@@ -598,6 +598,17 @@ def roofline_us(t: Task, hbm_gbs: float, tflops: float) -> float:
 
 _DEBUG_TUNE = bool(os.environ.get("SW_DEBUG_TUNE"))
 
+
+def _torch_done(dev) -> None:
+    """Wait for torch's current stream on `dev`.  The engine launches on its
+    own non-blocking stream, which is not ordered after torch's: a torch-side
+    write into the arena / input buffer (a copy, a fill) must complete before
+    the next engine call reads it.  (Without this, a replay right after
+    load_input_device could read the tail of the input before the copy
+    landed — the last image of a batch came out wrong in a rare test run.)"""
+    torch.cuda.current_stream(dev).synchronize()
+
+
 class Engine:
     """Nimble-style AoT engine around a static ``nn.Module`` (eval mode, fp32)."""
 
@@ -732,6 +743,7 @@ class Engine:
         t3 = time.perf_counter()
         if self.conv_impl == "auto":
             self.d_in.copy_(ex.reshape(-1).to(dev))
+            _torch_done(dev)
             self._signature = self._tuning_signature()  # before tuning rewrites the ops
             if not self._load_tuning():
                 self._autotune()
@@ -824,6 +836,7 @@ class Engine:
         gen = torch.Generator(device=self.arena.device).manual_seed(1234)
         words = self.arena.numel() // 4
         self.arena[: 4 * words].view(torch.float32).normal_(generator=gen)
+        _torch_done(self.arena.device)
         self.tuning_rejected = {}
         for t in self.program.tasks:
             if t.kind not in ("conv", "sepconv", "sep2", "dwconv", "pool"):
@@ -884,6 +897,7 @@ class Engine:
                     trial.kind, trial.variant = cand[1], cand[2]
                     trial.params[SP_SPLIT_K] = cand[3]
                     self._out_tensor(t).fill_(float("nan"))
+                    _torch_done(self.arena.device)
                     N.check(lib.sw_engine_run_op(self._h, C.byref(trial)))
                     err = (self._out_tensor(t) - ref_out).abs().max().item()
                     # bf16 candidates are checked at the bf16 tolerance
@@ -1087,6 +1101,7 @@ class Engine:
     def load_input_device(self, x: torch.Tensor):
         """Place a batch in the device input buffer (for device-resident replay)."""
         self.d_in.copy_(x.detach().reshape(-1).to(self.d_in.device, torch.float32))
+        _torch_done(self.d_in.device)
 
     def replay(self, multi: bool = True, io: bool = False):
         slot = (SLOT_MULTI_IO if multi else SLOT_SINGLE_IO) if io else \

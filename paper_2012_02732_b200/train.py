@@ -1096,6 +1096,7 @@ class TrainEngine:
         for m, img, rb in running_image(b):
             self._dev_view(rb, torch.float32).copy_(torch.from_numpy(img).to(dev))
         self._dev_view(b.ones, torch.float32).fill_(1.0)
+        torch.cuda.current_stream(dev).synchronize()  # the engine's stream is not ordered after torch's
         self.ops = lower_train(b, base)
         self.h_in = torch.empty(tuple(x.shape), dtype=torch.float32).pin_memory()
         self.h_lab = torch.empty((x.shape[0],), dtype=torch.int32).pin_memory()
@@ -1168,6 +1169,7 @@ class TrainEngine:
         b = self.builder
         self._dev_view(b.input, torch.float32).copy_(x.detach().reshape(-1).to(self.arena.device))
         self._dev_view(b.labels, torch.int32).copy_(y.detach().to(torch.int32).reshape(-1).to(self.arena.device))
+        torch.cuda.current_stream(self.arena.device).synchronize()  # see engine._torch_done
 
     def replay(self, multi: bool = True, io: bool = False):
         slot = (SLOT_MULTI_IO if multi else SLOT_SINGLE_IO) if io else (SLOT_MULTI if multi else SLOT_SINGLE)
