@@ -305,6 +305,11 @@ int sw_engine_run_op(sw_engine* e, const sw_op_desc* op);
 /* A root node on its own stream prefetches the range given to
  * sw_engine_set_prefetch (the packed weights) into L2 at graph start. */
 #define SW_ENGINE_L2_PREFETCH 32u
+/* With SW_ENGINE_PDL: the captured graph's cross-stream task -> task edges
+ * (the sync edges of the plan) become programmatic edges too, so a task on
+ * another stream launches as soon as its producers have triggered and waits
+ * for their completion in griddepcontrol.wait, as same-stream successors do. */
+#define SW_ENGINE_XSTREAM_PDL 64u
 int sw_engine_set_flags(sw_engine* e, uint32_t flags);
 
 /* ---- training step (paper_2012_02732_b200/train.py) ---- */

@@ -107,6 +107,7 @@ struct Slot {
   bool io_in_custom = false, io_out_custom = false;  // re-pointed at a caller buffer
   const void* io_in_ptr = nullptr;                    // the caller buffer it points at
   bool with_io = false;                               // captured with host staging copies
+  int64_t xpdl_edges = 0;                             // task edges re-typed programmatic
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -118,6 +119,7 @@ struct Slot {
     with_io = false;
     io_in_custom = io_out_custom = false;
     io_in_ptr = nullptr;
+    xpdl_edges = 0;
   }
 };
 
@@ -345,6 +347,48 @@ int sw_engine_set_io(sw_engine* e, uint64_t host_in, uint64_t dev_in, int64_t in
   return SW_OK;
 }
 
+// SW_ENGINE_XSTREAM_PDL: re-type every full task -> task kernel edge of a
+// captured graph (the plan's cross-stream sync edges; same-stream edges are
+// programmatic already when captured with PDL) as a programmatic edge.  Every
+// task kernel is launched by launch_k under the PDL protocol — constants
+// before griddepcontrol.wait, every dependent read and every write after it —
+// so a successor may be resident before its producers finish, exactly as a
+// same-stream successor is; the wait covers all of a node's programmatic
+// producers.  Edges touching non-task nodes (staging copies, prefetch,
+// fork / join) stay full dependencies.
+static int programmatic_task_edges(Slot& sl) {
+  size_t n = 0;
+  CU(cudaGraphGetEdges_v2(sl.graph, nullptr, nullptr, nullptr, &n));
+  if (n == 0) return SW_OK;
+  std::vector<cudaGraphNode_t> from(n), to(n);
+  std::vector<cudaGraphEdgeData> ed(n);
+  CU(cudaGraphGetEdges_v2(sl.graph, from.data(), to.data(), ed.data(), &n));
+  std::vector<cudaGraphNode_t> rf, rt;
+  std::vector<cudaGraphEdgeData> re;
+  for (size_t i = 0; i < n; ++i) {
+    if (ed[i].type != cudaGraphDependencyTypeDefault) continue;
+    if (!sl.node_task.count(from[i]) || !sl.node_task.count(to[i])) continue;
+    cudaGraphNodeType tf, tt;
+    CU(cudaGraphNodeGetType(from[i], &tf));
+    CU(cudaGraphNodeGetType(to[i], &tt));
+    if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel) continue;
+    rf.push_back(from[i]);
+    rt.push_back(to[i]);
+    re.push_back(ed[i]);
+  }
+  if (rf.empty()) return SW_OK;
+  CU(cudaGraphRemoveDependencies_v2(sl.graph, rf.data(), rt.data(), re.data(), rf.size()));
+  std::vector<cudaGraphEdgeData> pe(rf.size());
+  for (auto& x : pe) {
+    x = {};
+    x.from_port = cudaGraphKernelNodePortProgrammatic;
+    x.type = cudaGraphDependencyTypeProgrammatic;
+  }
+  CU(cudaGraphAddDependencies_v2(sl.graph, rf.data(), rt.data(), pe.data(), rf.size()));
+  sl.xpdl_edges = (int64_t)rf.size();
+  return SW_OK;
+}
+
 int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64_t* stream_len,
                       const int32_t* op_kind, const int64_t* op_arg, int64_t n_order, const int64_t* order,
                       int32_t with_io) {
@@ -501,6 +545,9 @@ int sw_engine_capture(sw_engine* e, int32_t slot, int64_t n_streams, const int64
     if (err != cudaSuccess) return abort_capture(cuda_fail(err, "capture D2H"));
   }
   CU(cudaStreamEndCapture(origin, &sl.graph));
+  if ((e->flags & SW_ENGINE_PDL) && (e->flags & SW_ENGINE_XSTREAM_PDL) && !(e->flags & SW_ENGINE_NULL_KERNELS)) {
+    if (int r = programmatic_task_edges(sl)) return r;
+  }
   CU(cudaGraphInstantiateWithFlags(&sl.exec, sl.graph, 0));
   CU(cudaGraphUpload(sl.exec, e->launch));
   return SW_OK;

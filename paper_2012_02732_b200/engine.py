@@ -617,7 +617,7 @@ class Engine:
                  tuning_cache: str | None = None, kernel_io: bool = True, arena: str = "hb",
                  fuse_sep_pairs: bool = False, l2_prefetch: bool = False,
                  max_streams: int | None = None, precision: str = "fp32",
-                 fuse_separable: bool = True):
+                 fuse_separable: bool = True, xstream_pdl: bool = False):
         """conv_impl: "auto" = time SIMT / tcgen05 tile + split-K candidates per
         conv at prepare and keep the fastest (Nimble's kernel selection,
         PAPER.md:405-406); "simt" / "tc" force one family (tests)."""
@@ -627,6 +627,9 @@ class Engine:
         # False: depthwise and pointwise stay separate tasks (the pointwise
         # then runs on the large-batch tcgen05 GEMM; an A/B option at bs256)
         self.fuse_separable = fuse_separable
+        # SW_ENGINE_XSTREAM_PDL: the plan's cross-stream sync edges become
+        # programmatic graph edges too (an A/B option)
+        self.xstream_pdl = xstream_pdl
         if precision not in ("fp32", "bf16"):
             raise ValueError(f"precision must be 'fp32' or 'bf16', not {precision!r}")
         # "bf16": the batch-1 weight-streaming contractions may run in bf16
@@ -762,8 +765,10 @@ class Engine:
         return self
 
     def _flags(self) -> int:
-        """SW_ENGINE_PDL | SW_ENGINE_KERNEL_IO (include/streamweave_b200.h)."""
-        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0) | (32 if self.l2_prefetch else 0)
+        """SW_ENGINE_PDL | SW_ENGINE_KERNEL_IO | SW_ENGINE_L2_PREFETCH |
+        SW_ENGINE_XSTREAM_PDL (include/streamweave_b200.h)."""
+        return (1 if self.pdl else 0) | (4 if self.kernel_io else 0) | (32 if self.l2_prefetch else 0) | \
+            (64 if self.pdl and self.xstream_pdl else 0)
 
     def _tuning_signature(self):
         import hashlib
