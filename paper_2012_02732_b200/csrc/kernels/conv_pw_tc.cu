@@ -348,10 +348,11 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
         }
         if (a.split > 1) {
           // one tile per CTA: the ring is quiescent (every MMA has completed);
-          // park the partial tile [BN][128 rows] for the rank-ordered sum
-          float* part = reinterpret_cast<float*>(smem);
+          // park the partial tile, rows of BN + 4 floats (16-B aligned,
+          // conflict-free float4 rows), for the rank-ordered sum
+          float4* prow = reinterpret_cast<float4*>(smem) + row * (BN / 4 + 1);
 #pragma unroll
-          for (int j = 0; j < BN; ++j) part[j * PW_BM + row] = racc[j];
+          for (int j = 0; j < BN; j += 4) prow[j / 4] = make_float4(racc[j], racc[j + 1], racc[j + 2], racc[j + 3]);
           continue;
         }
         if (ok) {
@@ -419,14 +420,20 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
   }
   if constexpr (PROMO) {
     if (a.split > 1) {
-      // every rank's partial is parked in its smem: rank 0's epilogue warps
-      // sum ranks 0..split-1 in order (DSMEM loads), add bias / residual /
-      // activation and store; the second cluster barrier keeps the peers'
-      // shared memory alive until those loads are done
+      // every rank's partial is parked in its smem: each rank's epilogue
+      // warps sum their channel slice over ranks 0..split-1 in order (DSMEM
+      // loads), add bias / residual / activation and store; the second
+      // cluster barrier keeps every CTA's shared memory alive until all those
+      // loads are done
       __syncwarp();
       asm volatile("barrier.cluster.arrive.aligned;" ::: "memory");
       cluster_wait();
-      if (zr == 0 && warp >= 6) {
+      if (warp >= 6) {
+        // rank z owns the 4-channel groups [z*G/split, (z+1)*G/split) of the
+        // tile: it sums every rank's partial of those channels in rank order
+        // (float4 DSMEM loads, all ranks' loads of a group in flight at once)
+        // and applies bias / residual / activation — the same bits whichever
+        // rank does it, the reduction spread over the cluster
         const int row = (warp & 3) * 32 + lane;
         const int tg = (int)blockIdx.x;
         const int nb = tg / a.ptiles;
@@ -438,30 +445,38 @@ __global__ void __launch_bounds__(PW_THREADS, 1)
         if (ok) {
           float* o = a.out + nb * a.out_sn + pp * a.out_sh + qq * a.out_sw + n0;
           const float* rp = a.has_res ? a.res + nb * a.res_sn + pp * a.res_sh + qq * a.res_sw + n0 : nullptr;
-          const uint32_t part = sbase + (uint32_t)(row * 4);
+          const uint32_t rowaddr = sbase + (uint32_t)(row * (BN + 4) * 4);
           const int nv = min(BN, a.K - n0);
+          constexpr int G = BN / 4;
+          const int g0 = (zr * G) / a.split, g1 = ((zr + 1) * G) / a.split;
 #pragma unroll 1
-          for (int j0 = 0; j0 < nv; j0 += 4) {
-            float x[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-            for (int z = 0; z < a.split; ++z) {
-              const uint32_t src = mapa_rank(part + (uint32_t)(j0 * PW_BM * 4), (uint32_t)z);
+          for (int g = g0; g < g1; ++g) {
+            const int j0 = 4 * g;
+            if (j0 >= nv) break;
+            float4 v[8];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                float v;
-                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(src + (uint32_t)(i * PW_BM * 4)));
-                x[i] += v;
+            for (int z = 0; z < 8; ++z) {
+              if (z < a.split) {
+                const uint32_t src = mapa_rank(rowaddr + (uint32_t)(j0 * 4), (uint32_t)z);
+                asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v[z].x), "=f"(v[z].y), "=f"(v[z].z), "=f"(v[z].w)
+                             : "r"(src));
               }
             }
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int z = 0; z < 8; ++z)
+              if (z < a.split) x = f4add(x, v[z]);
             if (a.ovec && j0 + 4 <= nv) {
-              float4 y = f4add(make_float4(x[0], x[1], x[2], x[3]), *reinterpret_cast<const float4*>(bias_s + j0));
+              float4 y = f4add(x, *reinterpret_cast<const float4*>(bias_s + j0));
               if (rp) y = f4add(y, *reinterpret_cast<const float4*>(rp + j0));
               *reinterpret_cast<float4*>(o + j0) = act4(y, a.act);
             } else {
+              const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 if (j0 + i >= nv) break;
-                float y = x[i] + bias_s[j0 + i];
+                float y = xs[i] + bias_s[j0 + i];
                 if (rp) y += rp[j0 + i];
                 o[j0 + i] = apply_act(y, a.act);
               }
