@@ -474,6 +474,8 @@ class SepBN(nn.Module):
     (48, 64, 5, 1, 35, 4, True),        # Inception 5x5 on 48 channels
     (32, 64, 3, 1, 140, 1, False),      # 140-wide rows: two 70-column segments per output row
     (32, 32, 3, 2, 263, 1, False),      # stride 2, 132-wide output rows: column segments + strided boxes
+    (528, 176, 1, 1, 14, 1, True),      # NASNet bs1 pointwise (one tap, 17 K blocks), residual
+    (1056, 176, 1, 1, 7, 1, False),     # 7x7 map: one 49-pixel tile, 33 K blocks
 ])
 @pytest.mark.parametrize("split", [1, 3, 4])
 def test_tcgen05_im2col_persistent(bn, cin, cout, k, s, h, batch, res, split):
