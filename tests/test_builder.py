@@ -140,3 +140,20 @@ def test_conv_candidates_tcgen05_variants():
     assert not any(k == K_CONV_TC and v >= 8400 for k, v, _ in conv_candidates(512, 64, 576, 3, 3, (1, 1)))
     gemv = conv_candidates(1, 1000, 1056, 1, 1, (0, 0))
     assert (K_CONV, 8, 1) in gemv
+
+
+def test_engine_capture_flags():
+    """Engine options → SW_ENGINE_* capture flags (include/streamweave_b200.h):
+    PDL 1, KERNEL_IO 4, L2_PREFETCH 32, XSTREAM_PDL 64 (only together with
+    PDL: a programmatic cross-stream edge needs the PDL launch protocol)."""
+    from paper_2012_02732_b200.engine import Engine
+    m = torch.nn.Conv2d(3, 4, 1)
+    assert Engine(m)._flags() == 1 | 4
+    assert Engine(m, xstream_pdl=True)._flags() == 1 | 4 | 64
+    assert Engine(m, pdl=False, xstream_pdl=True)._flags() == 4
+    assert Engine(m, kernel_io=False, l2_prefetch=True)._flags() == 1 | 32
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "include", "streamweave_b200.h")).read()
+    for name, v in [("SW_ENGINE_PDL", 1), ("SW_ENGINE_KERNEL_IO", 4), ("SW_ENGINE_L2_PREFETCH", 32),
+                    ("SW_ENGINE_XSTREAM_PDL", 64)]:
+        assert f"#define {name} {v}u" in hdr
