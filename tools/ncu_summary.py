@@ -105,9 +105,14 @@ def summarize_launches(path: str) -> str:
     return "\n".join(out) + "\n"
 
 
-FAMILY = {"sepconv_kernel": "sepconv", "sepconv_tma_kernel": "sepconv", "conv_simt_kernel": "conv",
-          "conv_tc_kernel": "conv", "pw_tma_kernel": "conv", "conv_gemv_kernel": "conv",
-          "spatial_kernel<0": "dwconv", "spatial_kernel<1": "pool", "global_pool": "gpool", "ew_": "eltwise"}
+# kernel-name substring -> engine task family (first match wins: the
+# sepconv names come before "conv_tc_kernel", a substring of "sepconv_tc_kernel")
+FAMILY = {"sepconv_kernel": "sepconv", "sepconv_tma_kernel": "sepconv", "sepconv_tc_kernel": "sepconv",
+          "sep_rows_kernel": "sepconv", "conv_simt_kernel": "conv", "conv_tc_kernel": "conv",
+          "conv_tc_tma": "conv", "conv_tcs_kernel": "conv", "conv_pw_tc_kernel": "conv",
+          "conv_direct_kernel": "conv", "pw_tma_kernel": "conv", "conv_gemv_kernel": "conv",
+          "spatial_kernel<0": "dwconv", "spatial_kernel<1": "pool", "spatial_rows_kernel<0": "dwconv",
+          "spatial_rows_kernel<1": "pool", "pool_rows_kernel": "pool", "global_pool": "gpool", "ew_": "eltwise"}
 
 
 def traffic_json(path: str) -> dict:
